@@ -1,0 +1,284 @@
+"""Pins for the oracle's TT evaluation, exact product and full ACI run (Alg. 1).
+
+Independent references used here: closed-form functions the inputs were
+built from (cosine sums, plane waves, separable Gaussians), dense products of
+dense vectors, per-index brute-force TT evaluation with Python loops, rank
+bounds rank(A*B) <= rank(A) rank(B), the TT-SVD error bound, and special cases
+(N=1 identity, rank-1 inputs).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads import generators as G
+from workloads import make_config
+
+
+def _brute_eval(cores, idx):
+    """One point, pure Python loops over the chain (the definition)."""
+    v = [1.0]
+    for s, c in enumerate(cores):
+        sg = int(idx[s])
+        nv = [0.0] * c.shape[2]
+        for b in range(c.shape[2]):
+            acc = 0.0
+            for a in range(c.shape[0]):
+                acc += v[a] * c[a, sg, b]
+            nv[b] = acc
+        v = nv
+    return v[0]
+
+
+def _closed_cosine(meta, x):
+    return sum(a * np.cos(2 * np.pi * k * x + p) for k, p, a in zip(meta["ks"], meta["phis"], meta["amps"]))
+
+
+def test_cosine_inputs_match_closed_form():
+    cf = make_config(0, npts=0)
+    x = np.arange(4096) / 4096.0
+    for t in cf["inputs"]:
+        assert max(t.ranks) == 8
+        assert np.abs(oracle.tt_dense(t) - _closed_cosine(t.meta, x)).max() < 1e-13
+
+
+def test_evaluate_matches_bruteforce_loops():
+    rng = np.random.default_rng(5)
+    t = G.random_tt(7, 3, 4, rng)
+    idx = G.sample_indices(t.d, 40, rng)
+    fast = oracle.tt_evaluate(t, idx)
+    for p in range(40):
+        assert abs(fast[p] - _brute_eval(t.cores, idx[p])) < 1e-13
+    dense = oracle.tt_dense(t).reshape([3] * 7)
+    for p in range(40):
+        assert abs(dense[tuple(idx[p])] - fast[p]) < 1e-13
+
+
+def test_plane_wave_inputs_match_closed_form():
+    cf = make_config(4, npts=2000)
+    s = cf["samples"]
+    L = 20
+    w = 2.0 ** -np.arange(1, L + 1)
+    x = (s >> 1).astype(float) @ w
+    y = (s & 1).astype(float) @ w
+    for t in cf["inputs"]:
+        m = t.meta
+        ref = sum(a * np.cos(2 * np.pi * (kx * x + ky * y) + p)
+                  for kx, ky, p, a in zip(m["kxs"], m["kys"], m["phis"], m["amps"]))
+        assert max(t.ranks) == 128
+        assert np.abs(oracle.tt_evaluate(t, s) - ref).max() < 1e-12
+
+
+def test_gaussian3d_input_matches_closed_form():
+    cf = make_config(2, npts=3000)
+    psi = cf["inputs"][0]
+    m = psi.meta
+    s = cf["samples"].astype(np.int64)
+    w = 2 ** np.arange(9, -1, -1)
+    xs = [(s[:, 10 * a:10 * a + 10] @ w) / 1024.0 for a in range(3)]
+    ref = 0
+    for c, sg, a in zip(m["cs"], m["sigmas"], m["amps"]):
+        g = [np.exp(-(t - c) ** 2 / (2 * sg ** 2)) for t in xs]
+        ref = ref + a * g[0] * g[1] * g[2]
+    assert np.abs(oracle.tt_evaluate(psi, cf["samples"]) - ref).max() < 1e-10 * np.abs(ref).max()
+
+
+def test_exact_product_dense_and_rank_bound():
+    cf = make_config(0, npts=0)
+    A, B = cf["inputs"]
+    x = np.arange(4096) / 4096.0
+    ref = _closed_cosine(A.meta, x) * _closed_cosine(B.meta, x)
+    ex = oracle.exact_product(cf["inputs"], cf["op"])
+    assert all(c.shape[2] <= 64 for c in ex[:-1])  # rank(A*B) <= rank(A) rank(B)
+    assert np.abs(oracle.tt_dense(ex) - ref).max() < 1e-13
+    rd = oracle.tt_round(ex, 1e-12)
+    err = np.linalg.norm(oracle.tt_dense(rd) - ref) / np.linalg.norm(ref)
+    assert err <= 1e-12
+    # the product of 4+4 cosines is a sum of <= 32 cosines: rank <= 64 (here well below)
+    assert max(c.shape[2] for c in rd) <= 64
+
+
+def test_exact_product_polynomial_op():
+    rng = np.random.default_rng(1)
+    a, b = G.random_tt(6, 2, 3, rng), G.random_tt(6, 2, 2, rng)
+    op = {"coef": [1.0, 0.5], "expo": [[1, 1], [2, 0]]}
+    da, db = oracle.tt_dense(a), oracle.tt_dense(b)
+    ex = oracle.exact_product([a, b], op)
+    assert np.abs(oracle.tt_dense(ex) - (da * db + 0.5 * da * da)).max() < 1e-13
+
+
+def test_tt_round_error_bound():
+    rng = np.random.default_rng(2)
+    a = G.random_tt(8, 2, 6, rng)
+    b = G.random_tt(8, 2, 5, rng)
+    ex = oracle.exact_product([a, b], {"coef": [1.0], "expo": [[1, 1]]})
+    full = oracle.tt_dense(ex)
+    for tol in (1e-1, 1e-3, 1e-8):
+        rd = oracle.tt_round(ex, tol)
+        assert np.linalg.norm(oracle.tt_dense(rd) - full) <= tol * np.linalg.norm(full) * (1 + 1e-9)
+
+
+# ---------------------------------------------------------------- full ACI runs
+def _rel_max(y, r):
+    return np.abs(y - r).max() / np.abs(r).max()
+
+
+def test_aci_cfg0_matches_dense_product():
+    """configs[0]: the ACI output equals the dense 4096-vector product within 10*tol (B:7)."""
+    cf = make_config(0, npts=0)
+    res = oracle.aci(cf["inputs"], cf["op"], cf["y_init"], cf["tol"], cf["maxrank"], cf["max_sweeps"])
+    x = np.arange(4096) / 4096.0
+    ref = _closed_cosine(cf["inputs"][0].meta, x) * _closed_cosine(cf["inputs"][1].meta, x)
+    assert _rel_max(oracle.tt_dense(res.cores), ref) <= 10 * cf["tol"]
+    assert res.report["converged"]
+    assert max(res.ranks) <= 64
+
+
+def test_aci_cfg1_matches_exact_product():
+    """configs[1]: output rank <= 64 and <= 10*tol vs Kronecker + SVD (B:8)."""
+    cf = make_config(1, npts=20000)
+    res = oracle.aci(cf["inputs"], cf["op"], cf["y_init"], cf["tol"], cf["maxrank"], cf["max_sweeps"])
+    assert max(res.ranks) <= 64
+    s = cf["samples"]
+    ref = oracle.tt_evaluate(cf["inputs"][0], s) * oracle.tt_evaluate(cf["inputs"][1], s)
+    assert _rel_max(oracle.tt_evaluate(res.cores, s), ref) <= 10 * cf["tol"]
+    ex = oracle.exact_product(cf["inputs"], cf["op"])
+    nr = oracle.tt_inner(ex, ex)
+    diff2 = oracle.tt_inner(res.cores, res.cores) - 2 * oracle.tt_inner(res.cores, ex) + nr
+    assert math.sqrt(max(diff2, 0.0) / nr) <= 10 * cf["tol"] + 1e-7  # inner-product cancellation floor
+    assert res.report["converged"]
+
+
+def test_aci_identity_op_reproduces_input():
+    """N=1, f(v)=v converges within 2 iterations and reproduces x."""
+    rng = np.random.default_rng(21)
+    x = G.random_tt(10, 2, 8, rng)
+    y0 = G.random_init([x], 8, rng)
+    res = oracle.aci([x], {"coef": [1.0], "expo": [[1]]}, y0, 1e-12, 64, 20)
+    assert res.report["converged"] and res.report["iterations"] <= 2
+    assert all(r <= 8 for r in res.ranks)
+    assert _rel_max(oracle.tt_dense(res.cores), oracle.tt_dense(x)) <= 1e-10
+
+
+def test_aci_rank_one_inputs_give_rank_one_output():
+    rng = np.random.default_rng(22)
+    a = G.random_tt(9, 2, 1, rng)
+    b = G.random_tt(9, 2, 1, rng)
+    y0 = G.random_init([a, b], 4, rng)
+    res = oracle.aci([a, b], {"coef": [1.0], "expo": [[1, 1]]}, y0, 1e-12, 16, 10)
+    assert max(res.ranks) == 1
+    assert _rel_max(oracle.tt_dense(res.cores), oracle.tt_dense(a) * oracle.tt_dense(b)) <= 1e-13
+
+
+def test_aci_random_small_suite_vs_dense():
+    """SPEC acceptance, reduced: random L in 4..8, chi in 2..5,
+    f in {x1*x2, x1+x2, x1*x2+x3}, tol 1e-10 -> dense max error <= 1e-8 relative."""
+    rng = np.random.default_rng(2024)
+    ops = [({"coef": [1.0], "expo": [[1, 1]]}, 2), ({"coef": [1.0, 1.0], "expo": [[1, 0], [0, 1]]}, 2),
+           ({"coef": [1.0, 1.0], "expo": [[1, 1, 0], [0, 0, 1]]}, 3)]
+    for trial in range(24):
+        L = int(rng.integers(4, 9))
+        op, N = ops[trial % 3]
+        xs = [G.random_tt(L, 2, int(rng.integers(2, 6)), rng) for _ in range(N)]
+        y0 = G.random_init(xs, 64, rng)
+        res = oracle.aci(xs, op, y0, 1e-10, 64, 20)
+        dense = [oracle.tt_dense(x) for x in xs]
+        ref = np.zeros_like(dense[0])
+        for c, e in zip(op["coef"], op["expo"]):
+            term = c * np.ones_like(ref)
+            for n, k in enumerate(e):
+                term = term * dense[n] ** k
+            ref += term
+        assert _rel_max(oracle.tt_dense(res.cores), ref) <= 1e-8, trial
+
+
+def test_aci_interpolation_nesting_and_frames():
+    """After the final right-to-left half-sweep:
+    (i) J sets are nested J_{s} > J_{s+1};
+    (ii) every column of R^n_s is the partial contraction of cores s..L-1 at J_s[k] (brute force);
+    (iii) every row of L^n_b is the partial contraction of cores 0..b at I_b[a];
+    (iv) the output interpolates f exactly on the last-updated cross (I_0 x J_1)."""
+    rng = np.random.default_rng(31)
+    L = 8
+    a, b = G.random_tt(L, 2, 3, rng), G.random_tt(L, 2, 2, rng)
+    y0 = G.random_init([a, b], 16, rng)
+    res = oracle.aci([a, b], {"coef": [1.0], "expo": [[1, 1]]}, y0, 1e-12, 64, 6)
+    for s in range(1, L - 1):
+        Js, Jn = res.Jset(s), res.Jset(s + 1)
+        tails = {tuple(r[1:]) for r in Js}
+        assert tails <= {tuple(r) for r in Jn}
+    for n, x in enumerate([a, b]):
+        for s in range(1, L):
+            R = res.Rframe(n, s)
+            for k, j in enumerate(res.Jset(s)):
+                v = np.eye(x.cores[s].shape[0])
+                for t, sg in zip(range(s, L), j):
+                    v = v @ x.cores[t][:, sg, :]
+                assert np.abs(R[:, k] - v[:, 0]).max() < 1e-13
+        for bnd in range(L - 1):
+            Lf = res.Lframe(n, bnd)
+            for k, i in enumerate(res.Iset(bnd)):
+                v = np.ones((1, 1))
+                for t, sg in enumerate(i):
+                    v = v @ x.cores[t][:, sg, :]
+                assert np.abs(Lf[k] - v[0]).max() < 1e-13
+    I0, J1 = res.Iset(0), res.Jset(1)
+    pts = np.array([np.concatenate([i, j]) for i in I0 for j in J1], dtype=np.uint8)
+    y = oracle.tt_evaluate(res.cores, pts)
+    ref = oracle.tt_evaluate(a, pts) * oracle.tt_evaluate(b, pts)
+    assert np.abs(y - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_assemble_pi_matches_direct_evaluation():
+    """Eq. pifromframes: Pi[a,s,s',j] = f(x^n(I[a] s s' J[j])) with frames built by brute force."""
+    rng = np.random.default_rng(41)
+    L, b = 7, 3
+    xs = [G.random_tt(L, 2, 3, rng), G.random_tt(L, 2, 4, rng)]
+    I = [tuple(rng.integers(0, 2, size=b)) for _ in range(3)]
+    J = [tuple(rng.integers(0, 2, size=L - b - 2)) for _ in range(4)]
+    op = {"coef": [2.0, -1.0], "expo": [[1, 1], [0, 2]]}
+    Ls, Rs = [], []
+    for x in xs:
+        Lf = np.zeros((len(I), x.cores[b].shape[0]))
+        for k, i in enumerate(I):
+            v = np.ones((1, 1))
+            for t, sg in enumerate(i):
+                v = v @ x.cores[t][:, sg, :]
+            Lf[k] = v[0]
+        Rf = np.zeros((x.cores[b + 2].shape[0], len(J)))
+        for k, j in enumerate(J):
+            v = np.eye(x.cores[b + 2].shape[0])
+            for t, sg in zip(range(b + 2, L), j):
+                v = v @ x.cores[t][:, sg, :]
+            Rf[:, k] = v[:, 0]
+        Ls.append(Lf)
+        Rs.append(Rf)
+    Pi = oracle.assemble_pi(Ls, [x.cores[b] for x in xs], [x.cores[b + 1] for x in xs], Rs, op)
+    for ai, i in enumerate(I):
+        for s in range(2):
+            for sp in range(2):
+                for ji, j in enumerate(J):
+                    full = np.array([i + (s, sp) + j], dtype=np.uint8)
+                    v = [_brute_eval(x.cores, full[0]) for x in xs]
+                    ref = 2.0 * v[0] * v[1] - v[1] ** 2
+                    assert abs(Pi[ai * 2 + s, sp * len(J) + ji] - ref) < 1e-13
+
+
+def test_aci_deterministic():
+    cf = make_config(0, npts=0)
+    r1 = oracle.aci(cf["inputs"], cf["op"], cf["y_init"], cf["tol"], cf["maxrank"], cf["max_sweeps"])
+    r2 = oracle.aci(cf["inputs"], cf["op"], cf["y_init"], cf["tol"], cf["maxrank"], cf["max_sweeps"])
+    assert all(np.array_equal(x, y) for x, y in zip(r1.cores, r2.cores))
+    assert all(np.array_equal(x["rows"], y["rows"]) for x, y in zip(r1.log, r2.log))
+
+
+@pytest.mark.slow
+def test_aci_cfg3_chi64_saturates_to_exact_product():
+    """configs[3] chi=64: ranks reach 2*chi and the output matches the exact product (CI exactness)."""
+    cf = make_config(3, 64, npts=5000)
+    res = oracle.aci(cf["inputs"], cf["op"], cf["y_init"], cf["tol"], cf["maxrank"], cf["max_sweeps"])
+    assert max(res.ranks) == 128
+    s = cf["samples"]
+    ref = oracle.tt_evaluate(cf["inputs"][0], s) * oracle.tt_evaluate(cf["inputs"][1], s)
+    assert _rel_max(oracle.tt_evaluate(res.cores, s), ref) <= 10 * cf["tol"]

@@ -1,0 +1,174 @@
+/*
+ * aci.h — C-ABI of libaci.so, the B200-native (sm_100a) hot path of
+ * alternating cross interpolation (ACI), M. K. Ritter, arxiv 2604.00037.
+ *
+ * Citation keys: P:n = PAPER.md line n (Ritter 2026), R# = reading # in
+ * DESIGN.md §2. All floating point is IEEE binary64 (FP64).
+ *
+ * Conventions shared by every call:
+ *  - A tensor train (TT) x has L >= 1 cores; core s (0-based) is a row-major
+ *    array of shape [r_s][d_s][r_{s+1}] with r_0 = r_L = 1.
+ *  - Local indices are 0-based; a full multi-index is L uint8 values.
+ *  - Return value: ACI_OK (0), a negative ACI_ERR_* code, or ACI_NOT_CONVERGED
+ *    (> 0, still a valid result). On error aci_last_error() describes it.
+ *  - Host pointers are only read during the call; nothing is retained.
+ *  - All device work is enqueued on the caller's stream (NULL = the library's
+ *    internal stream); calls return after the stream work they enqueued is
+ *    complete unless noted.
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    call returns ACI_ERR_CUDA.
+ */
+#ifndef ACI_B200_H
+#define ACI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ACI_OK 0
+#define ACI_NOT_CONVERGED 1      /* max_sweeps exhausted or rank cap bound; output valid */
+#define ACI_ERR_INVALID -1       /* null pointer, bad size, bad option */
+#define ACI_ERR_SHAPE -2         /* inputs disagree in L or d_s */
+#define ACI_ERR_NONFINITE -3     /* NaN/Inf in an input core, y_init, or produced by f */
+#define ACI_ERR_OOM -4           /* device allocation failed or caller workspace too small */
+#define ACI_ERR_CUDA -5          /* CUDA runtime/driver error, or no sm_100 device */
+#define ACI_ERR_UNSUPPORTED -6   /* size outside the compiled kernel envelope (see aci_limits) */
+
+typedef struct tt_s tt_t; /* opaque; device-resident cores */
+
+/* ---------------------------------------------------------------- TT objects */
+
+/* Create a device-resident TT from host cores (x_sigma = X_1[sigma_1]...X_L[sigma_L]).
+ * L: number of sites (>= 1); d[L]: local dimensions (1..255); ranks[L+1]: bond dimensions
+ * with ranks[0] = ranks[L] = 1; cores[L]: host pointers, core s holds ranks[s]*d[s]*ranks[s+1]
+ * doubles row-major [alpha][sigma][beta]. The cores are copied (host -> device) before return.
+ * Errors: ACI_ERR_INVALID (null, L < 1, d or rank < 1, boundary rank != 1),
+ * ACI_ERR_NONFINITE (NaN/Inf in a core), ACI_ERR_OOM, ACI_ERR_CUDA. *out is owned by the caller. */
+int tt_create(int L, const int *d, const int *ranks, const double *const *cores, tt_t **out);
+
+/* Same, from ONE contiguous device buffer holding core 0, core 1, ... back to back
+ * (device pointer). The data are copied device -> device. */
+int tt_create_device(int L, const int *d, const int *ranks, const double *dev_cores, void *stream, tt_t **out);
+
+/* Free a TT (device memory included). NULL is a no-op. Returns ACI_OK. */
+int tt_destroy(tt_t *tt);
+
+/* Shape query: *L, and if non-NULL d[L], ranks[L+1]. */
+int tt_shape(const tt_t *tt, int *L, int *d, int *ranks);
+
+/* Copy the cores to host buffers host_cores[s] (each ranks[s]*d[s]*ranks[s+1] doubles). */
+int tt_get_cores(const tt_t *tt, double *const *host_cores);
+
+/* Device pointer to the contiguous core storage (core s at offset sum_{t<s} r_t d_t r_{t+1}). */
+const double *tt_device_cores(const tt_t *tt);
+
+/* Evaluate x at npts full multi-indices (O(L chi^2) per point).
+ * idx: host, npts*L uint8 (row-major, point-major), out: host, npts doubles.
+ * Errors: ACI_ERR_INVALID (index >= d_s, null), ACI_ERR_CUDA. */
+int tt_evaluate(const tt_t *tt, int64_t npts, const uint8_t *idx, double *out);
+
+/* Same with device buffers (idx: device npts*L uint8; out: device npts doubles), enqueued on stream. */
+int tt_evaluate_device(const tt_t *tt, int64_t npts, const uint8_t *dev_idx, double *dev_out, void *stream);
+
+/* ---------------------------------------------------------------- the operation f */
+
+/* f(x_1..x_N) = sum_t coef[t] * prod_n x_n^expo[t*N + n]. This covers Hadamard
+ * products (one term, all exponents 1), sums, psi^3 and a*b + a^2. n_terms <= ACI_MAX_TERMS,
+ * exponents 0..ACI_MAX_EXPO. N is the n_inputs of the call that uses the op. */
+#define ACI_MAX_INPUTS 4
+#define ACI_MAX_TERMS 8
+#define ACI_MAX_EXPO 4
+typedef struct {
+  int n_terms;
+  const double *coef; /* n_terms */
+  const int *expo;    /* n_terms x n_inputs, row-major */
+} aci_op;
+
+/* ---------------------------------------------------------------- the ACI product */
+
+typedef struct {
+  double error_estimate;     /* max_l eps_l / s of the last iteration (absolute mode: max eps_l) */
+  double scale;              /* s = max |Pi| seen (R1) */
+  int iterations;            /* full iterations (L->R + R->L) performed (R10) */
+  int converged;             /* no rank grew and max eps <= tau*s */
+  int max_rank;              /* max output bond dimension */
+  int n_updates;             /* 2-site updates performed (= 2 (L-1) iterations) */
+  int64_t pivot_steps;       /* accepted pivots over all prrLU calls */
+  double flops_contraction;  /* SURVEY 8(d) model, per distinct input, from the live ranks */
+  double flops_prrlu;        /* sum_k 2 (m-k-1)(n-k-1) */
+  double flops_trsm;         /* output cores: r^2 (n - r) per bond */
+  double flops_init;         /* canonicalisation GEMMs */
+  float ms;                  /* host wall time of the call (includes the final sync) */
+} aci_report;
+
+/* Optional per-update log (for parity tests): entries in update order. */
+typedef struct {
+  int capacity_updates;      /* entries the buffers below can hold */
+  int capacity_pivots;       /* pivots per entry the row/col buffers can hold (>= maxrank) */
+  int *info;                 /* capacity_updates x 5: bond, dir (0 = L->R, 1 = R->L), rl, rr, r */
+  double *eps_scale;         /* capacity_updates x 2: eps_l, s */
+  int *rows;                 /* capacity_updates x capacity_pivots: pivot rows in Pi's matricisation */
+  int *cols;                 /* capacity_updates x capacity_pivots: pivot columns */
+  int n_written;             /* out: entries written */
+  /* canonicalisation pivots: for s = 1..L-1, |J_s| and the pivot columns */
+  int *canon_n;              /* L+1 (entries 1..L-1 used) */
+  int *canon_cols;           /* (L+1) x capacity_pivots */
+} aci_pivot_log;
+
+#define ACI_TOL_RELATIVE 0   /* R1: reject |c| <= tol * s (default) */
+#define ACI_TOL_ABSOLUTE 1   /* paper-literal absolute tau */
+
+typedef struct {
+  uint64_t seed;             /* y_init seed when y_init == NULL (counter-based N(0,1), R9) */
+  const tt_t *y_init;        /* initial guess; ranks are capped at maxrank */
+  int tol_mode;              /* ACI_TOL_RELATIVE | ACI_TOL_ABSOLUTE */
+  aci_pivot_log *log;        /* optional */
+  void *stream;              /* cudaStream_t; NULL = library stream */
+  void *workspace;           /* optional caller device memory (e.g. a torch tensor) */
+  size_t workspace_bytes;
+  /* optional: multi-indices of the final index sets, host buffers:
+   * I_sets[b] must hold (>= out rank of bond b) x (b+1) bytes; J_sets[s] (>= rank) x (L-s). */
+  uint8_t **I_sets;
+  uint8_t **J_sets;
+} aci_options;
+
+/*
+ * aci_elementwise — Alg. 1: y ~ f(x^1, ..., x^N) with ||y - f(x)||_inf ~ tau
+ * (Eq. ydef:maxnorm), by 2-site updates (Eq. pifromframes, prrLU Alg. 2
+ * P:504-545, cross interpolation Alg. 3, frames Alg. 5).
+ *
+ * inputs[n_inputs]: borrowed, unmodified, may alias (aliases are merged into the exponents);
+ *   all must share L and d_s (else ACI_ERR_SHAPE). n_inputs <= ACI_MAX_INPUTS distinct.
+ * tol >= 0 (relative to s by default, R1); maxrank >= 1 (chi-hat); max_sweeps >= 1 iterations.
+ * *out: new TT owned by the caller (valid also when ACI_NOT_CONVERGED is returned).
+ * rep: nullable.
+ * Errors: ACI_ERR_INVALID, ACI_ERR_SHAPE, ACI_ERR_NONFINITE (f produced NaN/Inf),
+ *   ACI_ERR_OOM, ACI_ERR_CUDA, ACI_ERR_UNSUPPORTED (a 2-site block larger than aci_limits).
+ */
+int aci_elementwise(aci_op op, const tt_t *const *inputs, int n_inputs, double tol, int maxrank,
+                    int max_sweeps, tt_t **out, aci_report *rep);
+
+/* Same with options (opts may be NULL). */
+int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_inputs, double tol, int maxrank,
+                       int max_sweeps, tt_t **out, aci_report *rep, const aci_options *opts);
+
+/* Device workspace (bytes) aci_elementwise_ex needs for these inputs and maxrank. */
+int aci_workspace_query(const tt_t *const *inputs, int n_inputs, int maxrank, const tt_t *y_init,
+                        size_t *bytes);
+
+/* Compiled envelope: the largest Pi block (rows, cols) the prrLU kernels accept. */
+int aci_limits(int *max_rows, int *max_cols);
+
+/* Thread-local description of the last error of this thread. */
+const char *aci_last_error(void);
+
+/* Library version string. */
+const char *aci_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ACI_B200_H */

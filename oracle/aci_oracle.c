@@ -433,8 +433,16 @@ void *oracle_aci(int L, const int *d, int N, const int *xranks, const double *co
     int rows_ = yr[s], jn = S->Jn[s + 1];
     int cols_ = d[s] * jn; /* M_{alpha, sigma j}; Y[s] already has right bond |J_{s+1}| */
     ldu_t f;
-    /* R8: tolerance relative to M's own max (or absolute in absolute mode) */
-    int st = ldu(rows_, cols_, Y[s], tol, tol_mode == 0 ? 1 : 0, maxrank, &f);
+    /* R8: tolerance relative to M's own max (or absolute in absolute mode).
+     * R9': |J_s| never exceeds the full-tensor bond bound prod_{t<s} d_t (a no-op for a
+     * minimal y_init, which is what the generators produce). */
+    int cap = maxrank;
+    {
+      long long pl = 1;
+      for (int t = 0; t < s && pl < cap; ++t) pl *= d[t];
+      if (pl < cap) cap = (int)pl;
+    }
+    int st = ldu(rows_, cols_, Y[s], tol, tol_mode == 0 ? 1 : 0, cap, &f);
     if (st != ORC_OK) { *status = st; aci_free(S); return NULL; }
     /* J_s[k] = (sigma, J_{s+1}[j]) */
     unsigned char *Js = (unsigned char *)malloc((size_t)f.r * (L - s));

@@ -1,0 +1,258 @@
+"""ctypes binding of libaci.so (include/aci.h). Argument marshalling only: every step of the
+ACI path runs in the CUDA kernels behind the C-ABI. There is no CPU fallback — if the library
+or a sm_100 device is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libaci.so")
+
+ACI_OK, ACI_NOT_CONVERGED = 0, 1
+ERRORS = {-1: "ACI_ERR_INVALID", -2: "ACI_ERR_SHAPE", -3: "ACI_ERR_NONFINITE", -4: "ACI_ERR_OOM",
+          -5: "ACI_ERR_CUDA", -6: "ACI_ERR_UNSUPPORTED"}
+TOL_RELATIVE, TOL_ABSOLUTE = 0, 1
+MAX_INPUTS, MAX_TERMS, MAX_EXPO = 4, 8, 4
+
+# every symbol include/aci.h declares (tests check the library exports all of them)
+EXPORTS = ["tt_create", "tt_create_device", "tt_destroy", "tt_shape", "tt_get_cores", "tt_device_cores",
+           "tt_evaluate", "tt_evaluate_device", "aci_elementwise", "aci_elementwise_ex", "aci_workspace_query",
+           "aci_limits", "aci_last_error", "aci_version"]
+
+
+class AciError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class aci_op(C.Structure):
+    _fields_ = [("n_terms", C.c_int), ("coef", C.POINTER(C.c_double)), ("expo", C.POINTER(C.c_int))]
+
+
+class aci_report(C.Structure):
+    _fields_ = [("error_estimate", C.c_double), ("scale", C.c_double), ("iterations", C.c_int),
+                ("converged", C.c_int), ("max_rank", C.c_int), ("n_updates", C.c_int),
+                ("pivot_steps", C.c_int64), ("flops_contraction", C.c_double), ("flops_prrlu", C.c_double),
+                ("flops_trsm", C.c_double), ("flops_init", C.c_double), ("ms", C.c_float)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class aci_pivot_log(C.Structure):
+    _fields_ = [("capacity_updates", C.c_int), ("capacity_pivots", C.c_int), ("info", C.POINTER(C.c_int)),
+                ("eps_scale", C.POINTER(C.c_double)), ("rows", C.POINTER(C.c_int)), ("cols", C.POINTER(C.c_int)),
+                ("n_written", C.c_int), ("canon_n", C.POINTER(C.c_int)), ("canon_cols", C.POINTER(C.c_int))]
+
+
+class aci_options(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("y_init", C.c_void_p), ("tol_mode", C.c_int),
+                ("log", C.POINTER(aci_pivot_log)), ("stream", C.c_void_p), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_size_t), ("I_sets", C.POINTER(C.POINTER(C.c_uint8))),
+                ("J_sets", C.POINTER(C.POINTER(C.c_uint8)))]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libaci.so (raises if it is missing: the product path has no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(path)
+    vp, ip, dp = C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double)
+    lib.tt_create.argtypes = [C.c_int, ip, ip, C.POINTER(dp), C.POINTER(vp)]
+    lib.tt_create_device.argtypes = [C.c_int, ip, ip, C.c_void_p, C.c_void_p, C.POINTER(vp)]
+    lib.tt_destroy.argtypes = [vp]
+    lib.tt_shape.argtypes = [vp, ip, ip, ip]
+    lib.tt_get_cores.argtypes = [vp, C.POINTER(dp)]
+    lib.tt_device_cores.argtypes = [vp]
+    lib.tt_device_cores.restype = C.c_void_p
+    lib.tt_evaluate.argtypes = [vp, C.c_int64, C.c_void_p, dp]
+    lib.tt_evaluate_device.argtypes = [vp, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.aci_elementwise.argtypes = [aci_op, C.POINTER(vp), C.c_int, C.c_double, C.c_int, C.c_int, C.POINTER(vp),
+                                    C.POINTER(aci_report)]
+    lib.aci_elementwise_ex.argtypes = [aci_op, C.POINTER(vp), C.c_int, C.c_double, C.c_int, C.c_int,
+                                       C.POINTER(vp), C.POINTER(aci_report), C.POINTER(aci_options)]
+    lib.aci_workspace_query.argtypes = [C.POINTER(vp), C.c_int, C.c_int, vp, C.POINTER(C.c_size_t)]
+    lib.aci_limits.argtypes = [ip, ip]
+    lib.aci_last_error.restype = C.c_char_p
+    lib.aci_version.restype = C.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(code):
+    if code < 0:
+        raise AciError(code, load().aci_last_error().decode())
+    return code
+
+
+def _dptr(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class TensorTrain:
+    """Device-resident TT handle (tt_t*). Cores are row-major [r_s][d_s][r_{s+1}]."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+
+    @classmethod
+    def from_cores(cls, cores) -> "TensorTrain":
+        cores = [np.ascontiguousarray(c, dtype=np.float64) for c in (cores.cores if hasattr(cores, "cores") else cores)]
+        L = len(cores)
+        d = np.array([c.shape[1] for c in cores], np.int32)
+        r = np.array([cores[0].shape[0]] + [c.shape[2] for c in cores], np.int32)
+        ptrs = (C.POINTER(C.c_double) * L)(*[_dptr(c) for c in cores])
+        h = C.c_void_p()
+        _check(load().tt_create(L, d.ctypes.data_as(C.POINTER(C.c_int)), r.ctypes.data_as(C.POINTER(C.c_int)),
+                                ptrs, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_device(cls, d, ranks, dev_ptr: int, stream: int = 0) -> "TensorTrain":
+        d = np.asarray(d, np.int32)
+        r = np.asarray(ranks, np.int32)
+        h = C.c_void_p()
+        _check(load().tt_create_device(len(d), d.ctypes.data_as(C.POINTER(C.c_int)),
+                                       r.ctypes.data_as(C.POINTER(C.c_int)), C.c_void_p(dev_ptr),
+                                       C.c_void_p(stream), C.byref(h)))
+        return cls(h)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def shape(self):
+        L = C.c_int()
+        _check(load().tt_shape(self._h, C.byref(L), None, None))
+        d = np.zeros(L.value, np.int32)
+        r = np.zeros(L.value + 1, np.int32)
+        _check(load().tt_shape(self._h, C.byref(L), d.ctypes.data_as(C.POINTER(C.c_int)),
+                               r.ctypes.data_as(C.POINTER(C.c_int))))
+        return [int(x) for x in d], [int(x) for x in r]
+
+    def cores(self):
+        d, r = self.shape()
+        out = [np.zeros((r[s], d[s], r[s + 1])) for s in range(len(d))]
+        ptrs = (C.POINTER(C.c_double) * len(d))(*[_dptr(c) for c in out])
+        _check(load().tt_get_cores(self._h, ptrs))
+        return out
+
+    def device_ptr(self) -> int:
+        return load().tt_device_cores(self._h)
+
+    def evaluate(self, idx) -> np.ndarray:
+        idx = np.ascontiguousarray(idx, dtype=np.uint8)
+        out = np.zeros(idx.shape[0])
+        _check(load().tt_evaluate(self._h, idx.shape[0], idx.ctypes.data, _dptr(out)))
+        return out
+
+    def evaluate_device(self, npts: int, dev_idx: int, dev_out: int, stream: int = 0):
+        _check(load().tt_evaluate_device(self._h, npts, C.c_void_p(dev_idx), C.c_void_p(dev_out),
+                                         C.c_void_p(stream)))
+
+    def free(self):
+        if self._h is not None and self._h.value:
+            load().tt_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _make_op(op, n_inputs):
+    coef = np.ascontiguousarray(op["coef"], dtype=np.float64)
+    expo = np.ascontiguousarray(op["expo"], dtype=np.int32).reshape(len(coef), n_inputs)
+    return aci_op(len(coef), _dptr(coef), expo.ctypes.data_as(C.POINTER(C.c_int))), (coef, expo)
+
+
+def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, tol_mode=TOL_RELATIVE,
+                    log=False, stream=0, workspace=None, index_sets=False):
+    """Run aci_elementwise_ex. ``inputs`` are TensorTrain handles (aliases allowed).
+
+    Returns (TensorTrain, status, report dict, extras dict).
+    """
+    lib = load()
+    n = len(inputs)
+    cop, keep = _make_op(op, n)
+    hs = (C.c_void_p * n)(*[x.handle.value for x in inputs])
+    out = C.c_void_p()
+    rep = aci_report()
+    opts = aci_options()
+    opts.seed = seed
+    opts.y_init = y_init.handle.value if y_init is not None else None
+    opts.tol_mode = tol_mode
+    opts.stream = stream or None
+    extras = {}
+    if workspace is not None:
+        opts.workspace, opts.workspace_bytes = workspace
+    L = len(inputs[0].shape()[0])
+    if log:
+        cap_u = 2 * (L - 1) * max_sweeps
+        cap_p = maxrank
+        info = np.zeros((cap_u, 5), np.int32)
+        es = np.zeros((cap_u, 2))
+        rows = np.zeros((cap_u, cap_p), np.int32)
+        cols = np.zeros((cap_u, cap_p), np.int32)
+        cn = np.zeros(L + 1, np.int32)
+        cc = np.zeros((L + 1, cap_p), np.int32)
+        lg = aci_pivot_log(cap_u, cap_p, info.ctypes.data_as(C.POINTER(C.c_int)), _dptr(es),
+                           rows.ctypes.data_as(C.POINTER(C.c_int)), cols.ctypes.data_as(C.POINTER(C.c_int)), 0,
+                           cn.ctypes.data_as(C.POINTER(C.c_int)), cc.ctypes.data_as(C.POINTER(C.c_int)))
+        opts.log = C.pointer(lg)
+    if index_sets:
+        Ibufs = [np.zeros((maxrank, b + 1), np.uint8) for b in range(L - 1)]
+        Jbufs = [np.zeros((maxrank, max(L - s, 1)), np.uint8) for s in range(L + 1)]
+        Ip = (C.POINTER(C.c_uint8) * L)(*[b.ctypes.data_as(C.POINTER(C.c_uint8)) for b in Ibufs],
+                                        C.POINTER(C.c_uint8)())
+        Jp = (C.POINTER(C.c_uint8) * (L + 1))(*[b.ctypes.data_as(C.POINTER(C.c_uint8)) for b in Jbufs])
+        opts.I_sets = C.cast(Ip, C.POINTER(C.POINTER(C.c_uint8)))
+        opts.J_sets = C.cast(Jp, C.POINTER(C.POINTER(C.c_uint8)))
+    st = lib.aci_elementwise_ex(cop, hs, n, float(tol), int(maxrank), int(max_sweeps), C.byref(out), C.byref(rep),
+                                C.byref(opts))
+    _check(st)
+    res = TensorTrain(out)
+    if log:
+        nw = lg.n_written
+        extras["log"] = [{"bond": int(info[u, 0]), "dir": int(info[u, 1]), "rl": int(info[u, 2]),
+                          "rr": int(info[u, 3]), "r": int(info[u, 4]), "eps": float(es[u, 0]),
+                          "scale": float(es[u, 1]), "rows": rows[u, :info[u, 4]].copy(),
+                          "cols": cols[u, :info[u, 4]].copy()} for u in range(nw)]
+        extras["canon_cols"] = {s: cc[s, :cn[s]].copy() for s in range(1, L)}
+    if index_sets:
+        _, rk = res.shape()
+        extras["I"] = [Ibufs[b][:rk[b + 1]].copy() for b in range(L - 1)]
+        extras["J"] = {s: Jbufs[s][:rk[s]].copy() for s in range(1, L)}
+    return res, st, rep.as_dict(), extras
+
+
+def workspace_query(inputs, maxrank, y_init=None) -> int:
+    n = len(inputs)
+    hs = (C.c_void_p * n)(*[x.handle.value for x in inputs])
+    b = C.c_size_t()
+    _check(load().aci_workspace_query(hs, n, maxrank, y_init.handle.value if y_init is not None else None,
+                                      C.byref(b)))
+    return b.value
+
+
+def limits():
+    a, b = C.c_int(), C.c_int()
+    _check(load().aci_limits(C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def version() -> str:
+    return load().aci_version().decode()

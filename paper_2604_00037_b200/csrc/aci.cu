@@ -1,0 +1,1156 @@
+// libaci.so: TT objects, the ACI sweep controller (Alg. 1) and the small kernels of
+// the 2-site update (planning, index-set / frame update, convergence, output cores, evaluation).
+// The GEMMs are in gemm.cu, the prrLU in prrlu.cu. The host code below only computes static
+// capacities and enqueues kernels: live ranks chi'_l never leave the device during a sweep
+// (one word per iteration is read back for the convergence test).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/aci.h"
+#include "aci_common.cuh"
+
+// ============================================================================ errors
+static thread_local std::string g_err;
+static int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+#define CUDA_TRY(x)                                                                                 \
+  do {                                                                                              \
+    cudaError_t e_ = (x);                                                                           \
+    if (e_ != cudaSuccess) return fail(ACI_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+extern "C" const char *aci_last_error(void) { return g_err.c_str(); }
+extern "C" const char *aci_version(void) { return "aci-b200 0.1 (sm_100a, FP64 DMMA + register-resident prrLU)"; }
+
+// ============================================================================ TT objects
+struct tt_s {
+  int L = 0;
+  std::vector<int> d, ranks;
+  std::vector<size_t> off;  // L+1 offsets (doubles)
+  double *dcores = nullptr;
+  size_t total = 0;
+};
+
+static int check_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return fail(ACI_ERR_CUDA, "no CUDA device (libaci has no CPU fallback)");
+  int dev = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) return fail(ACI_ERR_CUDA, "libaci is built for sm_100a only");
+  return ACI_OK;
+}
+
+static int validate_shape(int L, const int *d, const int *ranks) {
+  if (L < 1 || !d || !ranks) return fail(ACI_ERR_INVALID, "tt: L < 1 or null shape");
+  if (ranks[0] != 1 || ranks[L] != 1) return fail(ACI_ERR_INVALID, "tt: boundary ranks must be 1");
+  for (int s = 0; s < L; ++s) {
+    if (d[s] < 1 || d[s] > 255) return fail(ACI_ERR_INVALID, "tt: local dimension out of 1..255");
+    if (ranks[s] < 1) return fail(ACI_ERR_INVALID, "tt: rank < 1");
+  }
+  return ACI_OK;
+}
+
+static tt_s *tt_alloc_shape(int L, const int *d, const int *ranks) {
+  tt_s *t = new tt_s;
+  t->L = L;
+  t->d.assign(d, d + L);
+  t->ranks.assign(ranks, ranks + L + 1);
+  t->off.resize(L + 1);
+  size_t o = 0;
+  for (int s = 0; s < L; ++s) {
+    t->off[s] = o;
+    o += (size_t)ranks[s] * d[s] * ranks[s + 1];
+  }
+  t->off[L] = o;
+  t->total = o;
+  return t;
+}
+
+extern "C" int tt_create(int L, const int *d, const int *ranks, const double *const *cores, tt_t **out) {
+  if (!out || !cores) return fail(ACI_ERR_INVALID, "tt_create: null argument");
+  int st = validate_shape(L, d, ranks);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  tt_s *t = tt_alloc_shape(L, d, ranks);
+  for (int s = 0; s < L; ++s) {
+    if (!cores[s]) { delete t; return fail(ACI_ERR_INVALID, "tt_create: null core"); }
+    size_t sz = t->off[s + 1] - t->off[s];
+    for (size_t i = 0; i < sz; ++i)
+      if (!std::isfinite(cores[s][i])) { delete t; return fail(ACI_ERR_NONFINITE, "tt_create: NaN/Inf in core"); }
+  }
+  if (cudaMalloc(&t->dcores, sizeof(double) * std::max<size_t>(t->total, 1)) != cudaSuccess) {
+    delete t;
+    return fail(ACI_ERR_OOM, "tt_create: cudaMalloc failed");
+  }
+  for (int s = 0; s < L; ++s) {
+    cudaError_t e = cudaMemcpy(t->dcores + t->off[s], cores[s], sizeof(double) * (t->off[s + 1] - t->off[s]),
+                               cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(t->dcores);
+      delete t;
+      return fail(ACI_ERR_CUDA, std::string("tt_create: ") + cudaGetErrorString(e));
+    }
+  }
+  *out = t;
+  return ACI_OK;
+}
+
+extern "C" int tt_create_device(int L, const int *d, const int *ranks, const double *dev_cores, void *stream,
+                                tt_t **out) {
+  if (!out || !dev_cores) return fail(ACI_ERR_INVALID, "tt_create_device: null argument");
+  int st = validate_shape(L, d, ranks);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  tt_s *t = tt_alloc_shape(L, d, ranks);
+  if (cudaMalloc(&t->dcores, sizeof(double) * std::max<size_t>(t->total, 1)) != cudaSuccess) {
+    delete t;
+    return fail(ACI_ERR_OOM, "tt_create_device: cudaMalloc failed");
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaMemcpyAsync(t->dcores, dev_cores, sizeof(double) * t->total, cudaMemcpyDeviceToDevice, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    cudaFree(t->dcores);
+    delete t;
+    return fail(ACI_ERR_CUDA, std::string("tt_create_device: ") + cudaGetErrorString(e));
+  }
+  *out = t;
+  return ACI_OK;
+}
+
+extern "C" int tt_destroy(tt_t *t) {
+  if (!t) return ACI_OK;
+  if (t->dcores) cudaFree(t->dcores);
+  delete t;
+  return ACI_OK;
+}
+
+extern "C" int tt_shape(const tt_t *t, int *L, int *d, int *ranks) {
+  if (!t || !L) return fail(ACI_ERR_INVALID, "tt_shape: null argument");
+  *L = t->L;
+  if (d) std::copy(t->d.begin(), t->d.end(), d);
+  if (ranks) std::copy(t->ranks.begin(), t->ranks.end(), ranks);
+  return ACI_OK;
+}
+
+extern "C" const double *tt_device_cores(const tt_t *t) { return t ? t->dcores : nullptr; }
+
+extern "C" int tt_get_cores(const tt_t *t, double *const *host_cores) {
+  if (!t || !host_cores) return fail(ACI_ERR_INVALID, "tt_get_cores: null argument");
+  for (int s = 0; s < t->L; ++s) {
+    if (!host_cores[s]) return fail(ACI_ERR_INVALID, "tt_get_cores: null core buffer");
+    CUDA_TRY(cudaMemcpy(host_cores[s], t->dcores + t->off[s], sizeof(double) * (t->off[s + 1] - t->off[s]),
+                        cudaMemcpyDeviceToHost));
+  }
+  return ACI_OK;
+}
+
+// ============================================================================ small kernels
+
+// V'[p][beta] = W[p][sigma_p * r1 + beta]  (selection after W = V * X_s viewed r0 x (d r1))
+__global__ void eval_select_kernel(const double *W, double *V, const uint8_t *idx, int L, int s, int d, int r1,
+                                   int64_t np) {
+  const int64_t tot = np * r1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p = t / r1;
+    int b = (int)(t - p * r1);
+    int sg = idx[p * L + s];
+    V[t] = W[p * (int64_t)d * r1 + (int64_t)sg * r1 + b];
+  }
+}
+
+__global__ void eval_first_kernel(const double *X0, double *V, const uint8_t *idx, int L, int r1, int64_t np) {
+  const int64_t tot = np * r1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p = t / r1;
+    int b = (int)(t - p * r1);
+    V[t] = X0[(int64_t)idx[p * L] * r1 + b];
+  }
+}
+
+__global__ void eval_desc_kernel(GemmDesc *desc, const double *V, const double *X, double *W, int np, int r0,
+                                 int dr1) {
+  GemmDesc D = {};
+  D.C = W; D.M = np; D.N = dr1; D.ldc = dr1; D.nin = 1;
+  D.A[0] = V; D.lda[0] = r0; D.K[0] = r0;
+  D.B[0] = X; D.ldb[0] = dr1;
+  *desc = D;
+}
+
+// ---------------------------------------------------------------------------- sweep state
+// Static (host-known) pointers and dims of one bond for one input.
+struct InBond {
+  const double *Lprev;  // L^n_{b-1} (rmax[b-1] x chi_b, ld chi_b); null at b == 0 (L_{-1} = [1])
+  const double *Xb, *Xb1;
+  const double *Rnext;  // R^n_{b+2} (chi_{b+2} x rmax[b+1], ld ldR); null at b == L-2 (R_L = [1])
+  int ldR;
+  double *Abuf, *Bbuf;
+  int c0, c1, c2;       // chi^n_b, chi^n_{b+1}, chi^n_{b+2}
+};
+struct BondStatic {
+  int b, L, N, db, db1;
+  int ldu;              // static ld of the U store (nmax[b])
+  int maxrank;
+  InBond in[ACI_GEMM_MAX_IN];
+  double *Pi;
+};
+
+// One thread: live sizes -> GEMM descriptors (a1, a2 per input; a3+f) and prrLU dims.
+__global__ void plan_bond_kernel(BondStatic S, const int *rk, GemmDesc *ab, GemmDesc *pi, LuDims *lu) {
+  const int b = S.b;
+  const int rl = rk[b], rr = rk[b + 2];
+  const int m = rl * S.db, n = S.db1 * rr;
+  GemmDesc P = {};
+  P.C = S.Pi; P.M = m; P.N = n; P.ldc = n; P.nin = S.N;
+  for (int i = 0; i < S.N; ++i) {
+    const InBond &I = S.in[i];
+    GemmDesc a = {}, bb = {};
+    // a1: A^n = L^n_{b-1} X^n_b : (rl x c0) (c0 x db*c1) -> rl x (db c1) == (rl db) x c1
+    if (I.Lprev) {
+      a.C = I.Abuf; a.M = rl; a.N = S.db * I.c1; a.ldc = S.db * I.c1; a.nin = 1;
+      a.A[0] = I.Lprev; a.lda[0] = I.c0; a.K[0] = I.c0; a.B[0] = I.Xb; a.ldb[0] = S.db * I.c1;
+    }
+    // a2: B^n = X^n_{b+1} R^n_{b+2} : (c1 db1 x c2) (c2 x rr) -> (c1 db1) x rr == c1 x (db1 rr)
+    if (I.Rnext) {
+      bb.C = I.Bbuf; bb.M = I.c1 * S.db1; bb.N = rr; bb.ldc = rr; bb.nin = 1;
+      bb.A[0] = I.Xb1; bb.lda[0] = I.c2; bb.K[0] = I.c2; bb.B[0] = I.Rnext; bb.ldb[0] = I.ldR;
+    }
+    ab[2 * i] = a;
+    ab[2 * i + 1] = bb;
+    // a3: Pi^n = A^n B^n : (m x c1) (c1 x n)
+    P.A[i] = I.Lprev ? I.Abuf : I.Xb;
+    P.lda[i] = I.c1;
+    P.K[i] = I.c1;
+    P.B[i] = I.Rnext ? I.Bbuf : I.Xb1;
+    P.ldb[i] = n;
+  }
+  *pi = P;
+  LuDims D;
+  D.m = m; D.n = n; D.ldm = n;
+  D.kmax = min(S.maxrank, min(m, n));
+  D.ldu = S.ldu;
+  *lu = D;
+}
+
+struct UpdateArgs {
+  int b, dir, L, N, db, db1;
+  const int *rows, *cols;     // pivots of this bond
+  const int *r_in;            // accepted pivots
+  const double *eps_in;
+  int *rk;
+  uint8_t *Iprev, *Inew;      // Imi[b-1] (rmax[b-1] x b), Imi[b] (rmax[b] x (b+1))
+  uint8_t *Jnext, *Jnew;      // Jmi[b+2] (x (L-b-2)), Jmi[b+1] (x (L-b-1))
+  const double *A[ACI_GEMM_MAX_IN];  // A^n (m x c1), ld c1   (L->R gather)
+  double *Lnew[ACI_GEMM_MAX_IN];     // L^n_b (rmax[b] x c1)
+  const double *B[ACI_GEMM_MAX_IN];  // B^n (c1 x n), ld n     (R->L gather)
+  double *Rnew[ACI_GEMM_MAX_IN];     // R^n_{b+1} (c1 x rmax[b]), ld ldRnew
+  int ldRnew;
+  int c1[ACI_GEMM_MAX_IN];
+  const double *Pi;           // for Y_0 at b == 0 (R->L)
+  double *Y0;                 // d_0 x rmax[0], ld = r
+  unsigned long long *maxeps_bits;
+  const unsigned long long *scale_bits;
+  int *log_info;              // 5 ints
+  double *log_es;             // 2 doubles
+  int *log_rows, *log_cols;   // capacity maxrank
+};
+
+// Index-set update (a6, R21) and frame update (a7: the rows/columns of A^n / B^n the
+// new pivots select — the same numbers Alg. 5 recomputes).
+__global__ void update_bond_kernel(UpdateArgs U) {
+  const int r = *U.r_in;
+  const int b = U.b, L = U.L;
+  const int rl = U.rk[b], rr = U.rk[b + 2];
+  const int n = U.db1 * rr;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  if (gt == 0) {
+    U.rk[b + 1] = r;  // no thread of this kernel reads rk[b+1]
+    const double eps = *U.eps_in;
+    atomicMax(U.maxeps_bits, (unsigned long long)__double_as_longlong(eps));
+    U.log_info[0] = b; U.log_info[1] = U.dir; U.log_info[2] = rl; U.log_info[3] = rr; U.log_info[4] = r;
+    U.log_es[0] = eps;
+    U.log_es[1] = __longlong_as_double((long long)*U.scale_bits);
+  }
+  for (int k = gt; k < r; k += gs) {
+    U.log_rows[k] = U.rows[k];
+    U.log_cols[k] = U.cols[k];
+  }
+  // multi-indices: I_b[k] = (I_{b-1}[row / d_b], row % d_b); J_{b+1}[k] = (col / rr, J_{b+2}[col % rr])
+  for (int t = gt; t < r * (b + 1); t += gs) {
+    const int k = t / (b + 1), pos = t % (b + 1);
+    const int row = U.rows[k];
+    U.Inew[t] = pos == b ? (uint8_t)(row % U.db) : U.Iprev[(row / U.db) * b + pos];
+  }
+  const int wJ = L - b - 1;
+  for (int t = gt; t < r * wJ; t += gs) {
+    const int k = t / wJ, pos = t % wJ;
+    const int col = U.cols[k];
+    U.Jnew[t] = pos == 0 ? (uint8_t)(col / rr) : U.Jnext[(col % rr) * (wJ - 1) + pos - 1];
+  }
+  if (U.dir == 0) {
+    for (int i = 0; i < U.N; ++i) {
+      if (!U.Lnew[i]) continue;
+      const int c1 = U.c1[i];
+      for (int t = gt; t < r * c1; t += gs) {
+        const int k = t / c1, bb = t % c1;
+        U.Lnew[i][t] = U.A[i][(size_t)U.rows[k] * c1 + bb];
+      }
+    }
+  } else {
+    for (int i = 0; i < U.N; ++i) {
+      if (!U.Rnew[i]) continue;
+      const int c1 = U.c1[i];
+      for (int t = gt; t < c1 * r; t += gs) {
+        const int a = t / r, k = t % r;
+        U.Rnew[i][(size_t)a * U.ldRnew + k] = U.B[i][(size_t)a * n + U.cols[k]];
+      }
+    }
+    if (b == 0) {
+      const int m = rl * U.db;
+      for (int t = gt; t < m * r; t += gs) {
+        const int ii = t / r, k = t % r;
+        U.Y0[t] = U.Pi[(size_t)ii * n + U.cols[k]];
+      }
+    }
+  }
+}
+
+
+// Convergence test after a full iteration (R10).
+__global__ void converge_kernel(int *rk, int *prev, int L, unsigned long long *maxeps_bits,
+                                const unsigned long long *scale_bits, double tol, int tol_mode, int *flag,
+                                double *err_out) {
+  if (threadIdx.x != 0) return;
+  int grew = 0;
+  for (int b = 0; b < L - 1; ++b) {
+    if (rk[b + 1] > prev[b]) grew = 1;
+    prev[b] = rk[b + 1];
+  }
+  const double s = __longlong_as_double((long long)*scale_bits);
+  const double me = __longlong_as_double((long long)*maxeps_bits);
+  const double thr = tol_mode == ACI_TOL_RELATIVE ? tol * s : tol;
+  *flag = (!grew && me <= thr) ? 1 : 0;
+  *err_out = tol_mode == ACI_TOL_RELATIVE ? (s > 0 ? me / s : 0.0) : me;
+  *maxeps_bits = 0ull;
+}
+
+// ---- canonicalisation of y_init
+struct CanonArgs {
+  int s, L, N, ds;
+  int yr_s;                       // rows of M (y_init left bond of site s)
+  const double *M;                // Yabs[s] (or the original core at s = L-1), yr_s x (ds * rk[s+1])
+  LuDims *lu;
+  int maxrank;
+  // R-frame temp GEMMs: T^n = X^n_s (c0 ds x c1) * R^n_{s+1} (c1 x rk[s+1], ld ldR) -> c0 x (ds rk[s+1])
+  const double *Xs[ACI_GEMM_MAX_IN];
+  const double *Rnext[ACI_GEMM_MAX_IN];  // null at s = L-1
+  int ldR;
+  double *Tbuf[ACI_GEMM_MAX_IN];
+  int c0[ACI_GEMM_MAX_IN], c1[ACI_GEMM_MAX_IN];
+  GemmDesc *tdesc;                // N descriptors
+};
+
+__global__ void plan_canon_kernel(CanonArgs C, const int *rk) {
+  const int jn = rk[C.s + 1];
+  LuDims D;
+  D.m = C.yr_s; D.n = C.ds * jn; D.ldm = D.n;
+  D.kmax = min(C.maxrank, min(D.m, D.n));
+  D.ldu = 0;
+  *C.lu = D;
+  for (int i = 0; i < C.N; ++i) {
+    GemmDesc g = {};
+    if (C.Rnext[i]) {
+      g.C = C.Tbuf[i]; g.M = C.c0[i] * C.ds; g.N = jn; g.ldc = jn; g.nin = 1;
+      g.A[0] = C.Xs[i]; g.lda[0] = C.c1[i]; g.K[0] = C.c1[i];
+      g.B[0] = C.Rnext[i]; g.ldb[0] = C.ldR;
+    }
+    C.tdesc[i] = g;
+  }
+}
+
+struct CanonUpd {
+  int s, L, N, ds, yr_s, yr_prev_rows;   // yr_prev_rows = yr[s-1] * d[s-1]
+  const int *cols, *r_in;
+  int *rk;
+  uint8_t *Jnext, *Jnew;                 // Jmi[s+1] (x (L-s-1)), Jmi[s] (x (L-s))
+  const double *M;                       // yr_s x (ds * jn)
+  double *Mp;                            // gather M[:, J] -> yr_s x r
+  const double *T[ACI_GEMM_MAX_IN];      // T^n (c0 x ds*jn), or X^n_s itself at s = L-1
+  double *Rnew[ACI_GEMM_MAX_IN];         // R^n_s (c0 x rmax[s-1]), ld ldRnew
+  int ldRnew;
+  int c0[ACI_GEMM_MAX_IN];
+  const double *Yin_prev;                // y_init core s-1 : (yr[s-1] d) x yr_s
+  double *Yabs_prev;                     // out: (yr[s-1] d) x r
+  GemmDesc *ydesc;
+  int *canon_n;                          // log
+  int *canon_cols;
+};
+
+__global__ void canon_update_kernel(CanonUpd U) {
+  const int r = *U.r_in;
+  const int s = U.s, L = U.L;
+  const int jn = U.rk[s + 1];
+  const int n = U.ds * jn;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  if (gt == 0) {
+    U.rk[s] = r;  // |J_s| = rank of bond s-1; this kernel only reads rk[s+1]
+    *U.canon_n = r;
+    GemmDesc g = {};
+    g.C = U.Yabs_prev; g.M = U.yr_prev_rows; g.N = r; g.ldc = r; g.nin = 1;
+    g.A[0] = U.Yin_prev; g.lda[0] = U.yr_s; g.K[0] = U.yr_s;
+    g.B[0] = U.Mp; g.ldb[0] = r;
+    *U.ydesc = g;
+  }
+  for (int k = gt; k < r; k += gs) U.canon_cols[k] = U.cols[k];
+  const int wJ = L - s;
+  for (int t = gt; t < r * wJ; t += gs) {
+    const int k = t / wJ, pos = t % wJ;
+    const int col = U.cols[k];
+    U.Jnew[t] = pos == 0 ? (uint8_t)(col / jn) : U.Jnext[(col % jn) * (wJ - 1) + pos - 1];
+  }
+  for (int t = gt; t < U.yr_s * r; t += gs) {
+    const int a = t / r, k = t % r;
+    U.Mp[t] = U.M[(size_t)a * n + U.cols[k]];
+  }
+  for (int i = 0; i < U.N; ++i) {
+    const int c0 = U.c0[i];
+    for (int t = gt; t < c0 * r; t += gs) {
+      const int a = t / r, k = t % r;
+      U.Rnew[i][(size_t)a * U.ldRnew + k] = U.T[i][(size_t)a * n + U.cols[k]];
+    }
+  }
+}
+
+// ---- output cores (a8): Y_{b+1} = U_J^{-1} U (Alg. 3 right branch, R5)
+// One CTA (256 threads) per (bond, 32-column block); B[:, block] lives in shared memory during
+// the unit-upper back substitution B_k = U_k - sum_{i>k} U_k[q_i] B_i.
+struct TrsmArgs {
+  const double *U;  // U store of bond b (r x n), ld ldu
+  int ldu;
+  const int *cols;  // pivot columns q_0..q_{r-1}
+  int b, d1;        // bond, d_{b+1}
+  double *out;      // output core b+1, r x n row-major
+};
+
+__global__ void __launch_bounds__(256) trsm_kernel(const TrsmArgs *args, const int *rk) {
+  extern __shared__ double sB[];  // r x 32
+  __shared__ double spart[8][32];
+  const TrsmArgs A = args[blockIdx.y];
+  const int b = A.b;
+  const int r = rk[b + 1], n = A.d1 * rk[b + 2];
+  const int j0 = blockIdx.x * 32;
+  if (j0 >= n) return;
+  const int jj = threadIdx.x & 31, part = threadIdx.x >> 5;
+  const int j = j0 + jj;
+  for (int k = r - 1; k >= 0; --k) {
+    const double *Uk = A.U + (size_t)k * A.ldu;
+    double acc = 0.0;
+    for (int i = k + 1 + part; i < r; i += 8) acc = fma(Uk[A.cols[i]], sB[i * 32 + jj], acc);
+    spart[part][jj] = acc;
+    __syncthreads();
+    if (part == 0) {
+      double tot = 0.0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) tot += spart[p][jj];
+      sB[k * 32 + jj] = j < n ? Uk[j] - tot : 0.0;
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < r * 32; t += blockDim.x) {
+    const int k = t / 32, c = t % 32;
+    if (j0 + c < n) A.out[(size_t)k * n + j0 + c] = sB[t];
+  }
+}
+
+__global__ void copy_prev_kernel(const int *rk, int *prev, int L) {
+  for (int b = threadIdx.x; b < L - 1; b += blockDim.x) prev[b] = rk[b + 1];
+}
+
+// ============================================================================ host: workspace
+namespace {
+
+struct Carver {
+  char *base = nullptr;
+  size_t off = 0;
+  template <class T>
+  T *take(size_t count) {
+    off = (off + 255) & ~(size_t)255;
+    T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+    off += std::max<size_t>(count, 1) * sizeof(T);
+    return p;
+  }
+};
+
+struct Run {
+  int L = 0, N = 0, maxrank = 0, max_sweeps = 0, log_cap_upd = 0, log_cap_piv = 0, colcap = 0;
+  std::vector<int> d, yr;
+  std::vector<std::vector<int>> xr;      // [n][s], s = 0..L
+  std::vector<const double *> xcore0;    // device base of input n
+  std::vector<std::vector<size_t>> xoff; // [n][s]
+  std::vector<int> rmax, mmax, nmax;     // per bond
+  // device
+  int *rk = nullptr, *prev = nullptr, *rout = nullptr, *nonfinite = nullptr, *conv = nullptr;
+  double *epsb = nullptr, *err = nullptr;
+  unsigned long long *scale = nullptr, *maxeps = nullptr;
+  std::vector<int *> prow, pcol;
+  std::vector<std::vector<double *>> Lf, Rf;
+  std::vector<double *> Abuf, Bbuf, Ust, Yin, Yabs;
+  double *Pi = nullptr, *Y0 = nullptr, *Mp = nullptr;
+  std::vector<uint8_t *> Imi, Jmi;
+  GemmDesc *dAB = nullptr, *dPi = nullptr, *dT = nullptr, *dY = nullptr;
+  LuDims *dLu = nullptr;
+  int *log_info = nullptr, *log_rows = nullptr, *log_cols = nullptr, *canon_n = nullptr, *canon_cols = nullptr;
+  double *log_es = nullptr;
+  double *colpub = nullptr, *keyval = nullptr;
+  int *keyidx = nullptr;
+  unsigned *counter = nullptr;
+  TrsmArgs *dtrsm = nullptr;
+};
+
+static long long capped_prod(const std::vector<int> &d, int lo, int hi) {  // prod d[lo..hi], capped
+  long long p = 1;
+  for (int s = lo; s <= hi; ++s) {
+    p *= d[s];
+    if (p > (1 << 20)) return 1 << 20;
+  }
+  return p;
+}
+
+static void plan_capacities(Run &R) {
+  const int L = R.L;
+  R.rmax.assign(std::max(L - 1, 0), 0);
+  R.mmax.assign(std::max(L - 1, 0), 0);
+  R.nmax.assign(std::max(L - 1, 0), 0);
+  for (int b = 0; b < L - 1; ++b)
+    R.rmax[b] = (int)std::min<long long>(R.maxrank, std::min(capped_prod(R.d, 0, b), capped_prod(R.d, b + 1, L - 1)));
+  for (int b = 0; b < L - 1; ++b) {
+    R.mmax[b] = R.d[b] * (b == 0 ? 1 : R.rmax[b - 1]);
+    R.nmax[b] = R.d[b + 1] * (b == L - 2 ? 1 : R.rmax[b + 1]);
+  }
+}
+
+static size_t carve(Run &R, char *base) {
+  Carver c;
+  c.base = base;
+  const int L = R.L, N = R.N;
+  R.rk = c.take<int>(L + 1);
+  R.prev = c.take<int>(L);
+  R.rout = c.take<int>(L);
+  R.nonfinite = c.take<int>(1);
+  R.conv = c.take<int>(1);
+  R.epsb = c.take<double>(L);
+  R.err = c.take<double>(1);
+  R.scale = c.take<unsigned long long>(1);
+  R.maxeps = c.take<unsigned long long>(1);
+  R.prow.resize(L);
+  R.pcol.resize(L);
+  for (int s = 0; s < L; ++s) {  // bonds 0..L-2 ; index L-1 unused; canon uses bond s-1 arrays
+    int cap = s < L - 1 ? R.rmax[s] : 1;
+    R.prow[s] = c.take<int>(cap + 1);
+    R.pcol[s] = c.take<int>(cap + 1);
+  }
+  R.Lf.assign(N, std::vector<double *>(L, nullptr));
+  R.Rf.assign(N, std::vector<double *>(L + 1, nullptr));
+  R.Abuf.assign(N, nullptr);
+  R.Bbuf.assign(N, nullptr);
+  for (int n = 0; n < N; ++n) {
+    size_t acap = 1, bcap = 1;
+    for (int b = 0; b < L - 1; ++b) {
+      R.Lf[n][b] = c.take<double>((size_t)R.rmax[b] * R.xr[n][b + 1]);
+      acap = std::max(acap, (size_t)R.mmax[b] * R.xr[n][b + 1]);
+      bcap = std::max(bcap, (size_t)R.xr[n][b + 1] * R.nmax[b]);
+    }
+    for (int s = 1; s < L; ++s) R.Rf[n][s] = c.take<double>((size_t)R.xr[n][s] * R.rmax[s - 1]);
+    R.Abuf[n] = c.take<double>(acap);
+    R.Bbuf[n] = c.take<double>(bcap);
+  }
+  size_t picap = 1;
+  for (int b = 0; b < L - 1; ++b) picap = std::max(picap, (size_t)R.mmax[b] * R.nmax[b]);
+  R.Pi = c.take<double>(picap);
+  R.Ust.assign(L, nullptr);
+  for (int b = 0; b < L - 1; ++b) R.Ust[b] = c.take<double>((size_t)R.rmax[b] * R.nmax[b]);
+  R.Y0 = c.take<double>(L > 1 ? (size_t)R.mmax[0] * R.rmax[0] : 1);
+  R.Imi.assign(L, nullptr);
+  R.Jmi.assign(L + 1, nullptr);
+  for (int b = 0; b < L - 1; ++b) R.Imi[b] = c.take<uint8_t>((size_t)R.rmax[b] * (b + 1));
+  for (int s = 1; s < L; ++s) R.Jmi[s] = c.take<uint8_t>((size_t)R.rmax[s - 1] * (L - s));
+  R.Yin.assign(L, nullptr);
+  R.Yabs.assign(L, nullptr);
+  size_t mpcap = 1;
+  for (int s = 0; s < L; ++s) {
+    R.Yin[s] = c.take<double>((size_t)R.yr[s] * R.d[s] * R.yr[s + 1]);
+    if (s < L - 1) R.Yabs[s] = c.take<double>((size_t)R.yr[s] * R.d[s] * R.rmax[s]);
+    if (s >= 1) mpcap = std::max(mpcap, (size_t)R.yr[s] * R.rmax[s - 1]);
+  }
+  R.Mp = c.take<double>(mpcap);
+  R.dAB = c.take<GemmDesc>(2 * ACI_GEMM_MAX_IN);
+  R.dPi = c.take<GemmDesc>(1);
+  R.dT = c.take<GemmDesc>(ACI_GEMM_MAX_IN);
+  R.dY = c.take<GemmDesc>(1);
+  R.dLu = c.take<LuDims>(1);
+  R.log_info = c.take<int>((size_t)R.log_cap_upd * 5);
+  R.log_es = c.take<double>((size_t)R.log_cap_upd * 2);
+  R.log_rows = c.take<int>((size_t)R.log_cap_upd * R.log_cap_piv);
+  R.log_cols = c.take<int>((size_t)R.log_cap_upd * R.log_cap_piv);
+  R.canon_n = c.take<int>(L + 1);
+  R.canon_cols = c.take<int>((size_t)(L + 1) * R.log_cap_piv);
+  R.colpub = c.take<double>((size_t)2 * 148 * R.colcap);
+  R.keyval = c.take<double>(2 * 148);
+  R.keyidx = c.take<int>(2 * 148);
+  R.counter = c.take<unsigned>(1);
+  R.dtrsm = c.take<TrsmArgs>(L);
+  return c.off + 256;
+}
+
+struct Inputs {
+  std::vector<const tt_s *> tts;   // distinct
+  FOp op;
+};
+
+static int prepare(aci_op op, const tt_t *const *inputs, int n_inputs, Inputs &I) {
+  if (!inputs || n_inputs < 1) return fail(ACI_ERR_INVALID, "aci: no inputs");
+  if (op.n_terms < 1 || op.n_terms > ACI_MAX_TERMS || !op.coef || !op.expo)
+    return fail(ACI_ERR_INVALID, "aci: op must have 1..8 terms and non-null coef/expo");
+  std::vector<int> map(n_inputs);
+  for (int i = 0; i < n_inputs; ++i) {
+    if (!inputs[i]) return fail(ACI_ERR_INVALID, "aci: null input");
+    int u = -1;
+    for (size_t j = 0; j < I.tts.size(); ++j)
+      if (I.tts[j] == inputs[i]) u = (int)j;
+    if (u < 0) {
+      u = (int)I.tts.size();
+      I.tts.push_back(inputs[i]);
+    }
+    map[i] = u;
+  }
+  const int N = (int)I.tts.size();
+  if (N > ACI_MAX_INPUTS) return fail(ACI_ERR_INVALID, "aci: more than 4 distinct inputs");
+  const tt_s *t0 = I.tts[0];
+  for (int j = 1; j < N; ++j) {
+    if (I.tts[j]->L != t0->L || I.tts[j]->d != t0->d) return fail(ACI_ERR_SHAPE, "aci: inputs differ in L or d (S:253)");
+  }
+  std::memset(&I.op, 0, sizeof(I.op));
+  I.op.T = op.n_terms;
+  I.op.N = N;
+  for (int t = 0; t < op.n_terms; ++t) {
+    if (!std::isfinite(op.coef[t])) return fail(ACI_ERR_INVALID, "aci: non-finite coefficient");
+    I.op.coef[t] = op.coef[t];
+    for (int i = 0; i < n_inputs; ++i) {
+      int e = op.expo[t * n_inputs + i];
+      if (e < 0 || e > ACI_MAX_EXPO) return fail(ACI_ERR_INVALID, "aci: exponent out of 0..4");
+      I.op.expo[t * N + map[i]] += e;
+    }
+    for (int u = 0; u < N; ++u)
+      if (I.op.expo[t * N + u] > 3 * ACI_MAX_EXPO) return fail(ACI_ERR_INVALID, "aci: merged exponent too large");
+  }
+  return ACI_OK;
+}
+
+// counter-based N(0,1) (splitmix64 + Box-Muller) for the default y_init (R9)
+static uint64_t splitmix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+static double normal_at(uint64_t seed, uint64_t i) {
+  double u1 = ((splitmix(seed ^ (2 * i)) >> 11) + 1) * (1.0 / 9007199254740993.0);
+  double u2 = (splitmix(seed ^ (2 * i + 1)) >> 11) * (1.0 / 9007199254740992.0);
+  return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+}
+
+}  // namespace
+
+// ============================================================================ host: the sweep
+namespace {
+
+static void launch_update(Run &R, int b, int dir, int logslot, cudaStream_t st) {
+  UpdateArgs U = {};
+  U.b = b; U.dir = dir; U.L = R.L; U.N = R.N; U.db = R.d[b]; U.db1 = R.d[b + 1];
+  U.rows = R.prow[b]; U.cols = R.pcol[b]; U.r_in = R.rout + b; U.eps_in = R.epsb + b;
+  U.rk = R.rk;
+  U.Iprev = b > 0 ? R.Imi[b - 1] : nullptr;
+  U.Inew = R.Imi[b];
+  U.Jnext = b + 2 < R.L ? R.Jmi[b + 2] : nullptr;
+  U.Jnew = R.Jmi[b + 1];
+  for (int n = 0; n < R.N; ++n) {
+    const bool has_L = b > 0, has_R = b + 2 < R.L;
+    U.A[n] = has_L ? R.Abuf[n] : R.xcore0[n] + R.xoff[n][b];
+    U.Lnew[n] = R.Lf[n][b];
+    U.B[n] = has_R ? R.Bbuf[n] : R.xcore0[n] + R.xoff[n][b + 1];
+    U.Rnew[n] = R.Rf[n][b + 1];
+    U.c1[n] = R.xr[n][b + 1];
+  }
+  U.ldRnew = R.rmax[b];
+  U.Pi = R.Pi;
+  U.Y0 = R.Y0;
+  U.maxeps_bits = R.maxeps;
+  U.scale_bits = R.scale;
+  U.log_info = R.log_info + (size_t)logslot * 5;
+  U.log_es = R.log_es + (size_t)logslot * 2;
+  U.log_rows = R.log_rows + (size_t)logslot * R.log_cap_piv;
+  U.log_cols = R.log_cols + (size_t)logslot * R.log_cap_piv;
+  size_t work = (size_t)R.rmax[b] * 256;
+  int blocks = (int)std::min<size_t>(592, std::max<size_t>(1, (work + 255) / 256));
+  update_bond_kernel<<<blocks, 256, 0, st>>>(U);
+}
+
+static void bond_update(Run &R, const FOp &op, double tol, int tol_mode, int b, int dir, int logslot,
+                        cudaStream_t st) {
+  const int L = R.L, N = R.N;
+  BondStatic S = {};
+  S.b = b; S.L = L; S.N = N; S.db = R.d[b]; S.db1 = R.d[b + 1];
+  S.ldu = R.nmax[b];
+  S.maxrank = R.maxrank;
+  S.Pi = R.Pi;
+  int ab_m = 0, ab_n = 0;
+  for (int n = 0; n < N; ++n) {
+    InBond &I = S.in[n];
+    I.c0 = R.xr[n][b]; I.c1 = R.xr[n][b + 1]; I.c2 = R.xr[n][b + 2];
+    I.Xb = R.xcore0[n] + R.xoff[n][b];
+    I.Xb1 = R.xcore0[n] + R.xoff[n][b + 1];
+    I.Lprev = b > 0 ? R.Lf[n][b - 1] : nullptr;
+    I.Rnext = b + 2 < L ? R.Rf[n][b + 2] : nullptr;
+    I.ldR = b + 2 < L ? R.rmax[b + 1] : 1;
+    I.Abuf = R.Abuf[n];
+    I.Bbuf = R.Bbuf[n];
+    if (I.Lprev) { ab_m = std::max(ab_m, R.rmax[b - 1]); ab_n = std::max(ab_n, S.db * I.c1); }
+    if (I.Rnext) { ab_m = std::max(ab_m, I.c1 * S.db1); ab_n = std::max(ab_n, R.rmax[b + 1]); }
+  }
+  plan_bond_kernel<<<1, 1, 0, st>>>(S, R.rk, R.dAB, R.dPi, R.dLu);
+  if (ab_m > 0) launch_gemm(R.dAB, 2 * N, ab_m, ab_n, 1, false, op, nullptr, nullptr, st);
+  launch_gemm(R.dPi, 1, R.mmax[b], R.nmax[b], N, true, op, R.scale, R.nonfinite, st);
+  LuArgs a = {};
+  a.M = R.Pi; a.dims = R.dLu; a.tol = tol; a.thr_mode = tol_mode == ACI_TOL_RELATIVE ? 0 : 2;
+  a.scale_bits = R.scale;
+  a.rows = R.prow[b]; a.cols = R.pcol[b]; a.r_out = R.rout + b; a.eps_out = R.epsb + b;
+  a.U = dir == 1 ? R.Ust[b] : nullptr;
+  a.colpub = R.colpub; a.colcap = R.colcap; a.keyval = R.keyval; a.keyidx = R.keyidx; a.counter = R.counter;
+  launch_prrlu(a, R.mmax[b], R.nmax[b], st);
+  launch_update(R, b, dir, logslot, st);
+}
+
+static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st) {
+  const int L = R.L, N = R.N;
+  CanonArgs C = {};
+  C.s = s; C.L = L; C.N = N; C.ds = R.d[s]; C.yr_s = R.yr[s];
+  C.M = s == L - 1 ? R.Yin[s] : R.Yabs[s];
+  C.lu = R.dLu;
+  C.maxrank = R.rmax[s - 1];  // R9': canonical J_s never exceeds the full-tensor bond bound
+  C.ldR = s + 1 < L ? R.rmax[s] : 1;
+  C.tdesc = R.dT;
+  int tm = 0, tn = 0;
+  for (int n = 0; n < N; ++n) {
+    C.Xs[n] = R.xcore0[n] + R.xoff[n][s];
+    C.Rnext[n] = s + 1 < L ? R.Rf[n][s + 1] : nullptr;
+    C.Tbuf[n] = R.Bbuf[n];
+    C.c0[n] = R.xr[n][s];
+    C.c1[n] = R.xr[n][s + 1];
+    if (C.Rnext[n]) { tm = std::max(tm, C.c0[n] * C.ds); tn = std::max(tn, R.rmax[s]); }
+  }
+  plan_canon_kernel<<<1, 1, 0, st>>>(C, R.rk);
+  FOp dummy = {};
+  if (tm > 0) launch_gemm(R.dT, N, tm, tn, 1, false, dummy, nullptr, nullptr, st);
+  const int max_m = R.yr[s], max_n = R.nmax[s - 1];
+  LuArgs a = {};
+  a.M = C.M; a.dims = R.dLu; a.tol = tol; a.thr_mode = tol_mode == ACI_TOL_RELATIVE ? 1 : 2;
+  a.scale_bits = R.scale;
+  a.rows = R.prow[s - 1]; a.cols = R.pcol[s - 1]; a.r_out = R.rout + (s - 1); a.eps_out = R.epsb + (s - 1);
+  a.U = nullptr;
+  a.colpub = R.colpub; a.colcap = R.colcap; a.keyval = R.keyval; a.keyidx = R.keyidx; a.counter = R.counter;
+  launch_prrlu(a, max_m, max_n, st);
+  CanonUpd U = {};
+  U.s = s; U.L = L; U.N = N; U.ds = R.d[s]; U.yr_s = R.yr[s]; U.yr_prev_rows = R.yr[s - 1] * R.d[s - 1];
+  U.cols = R.pcol[s - 1]; U.r_in = R.rout + (s - 1);
+  U.rk = R.rk;
+  U.Jnext = s + 1 < L ? R.Jmi[s + 1] : nullptr;
+  U.Jnew = R.Jmi[s];
+  U.M = C.M;
+  U.Mp = R.Mp;
+  for (int n = 0; n < N; ++n) {
+    U.T[n] = C.Rnext[n] ? R.Bbuf[n] : C.Xs[n];
+    U.Rnew[n] = R.Rf[n][s];
+    U.c0[n] = R.xr[n][s];
+  }
+  U.ldRnew = R.rmax[s - 1];
+  U.Yin_prev = R.Yin[s - 1];
+  U.Yabs_prev = R.Yabs[s - 1];
+  U.ydesc = R.dY;
+  U.canon_n = R.canon_n + s;
+  U.canon_cols = R.canon_cols + (size_t)s * R.log_cap_piv;
+  canon_update_kernel<<<64, 256, 0, st>>>(U);
+  launch_gemm(R.dY, 1, R.yr[s - 1] * R.d[s - 1], R.rmax[s - 1], 1, false, dummy, nullptr, nullptr, st);
+}
+
+}  // namespace
+
+extern "C" int aci_limits(int *max_rows, int *max_cols) {
+  if (!max_rows || !max_cols) return fail(ACI_ERR_INVALID, "aci_limits: null");
+  prrlu_envelope(max_rows, max_cols);
+  return ACI_OK;
+}
+
+static int build_run(const Inputs &I, const tt_s *y, int maxrank, int max_sweeps, Run &R) {
+  const tt_s *t0 = I.tts[0];
+  R.L = t0->L;
+  R.N = (int)I.tts.size();
+  R.d = t0->d;
+  R.maxrank = maxrank;
+  R.max_sweeps = max_sweeps;
+  R.xr.resize(R.N);
+  R.xcore0.resize(R.N);
+  R.xoff.resize(R.N);
+  for (int n = 0; n < R.N; ++n) {
+    R.xr[n] = I.tts[n]->ranks;
+    R.xcore0[n] = I.tts[n]->dcores;
+    R.xoff[n] = I.tts[n]->off;
+  }
+  R.yr = y->ranks;
+  plan_capacities(R);
+  R.log_cap_upd = 2 * std::max(R.L - 1, 1) * max_sweeps;
+  R.log_cap_piv = 1;
+  for (int b = 0; b < R.L - 1; ++b) R.log_cap_piv = std::max(R.log_cap_piv, R.rmax[b]);
+  R.colcap = 32;
+  for (int b = 0; b < R.L - 1; ++b) R.colcap = std::max(R.colcap, R.mmax[b]);
+  for (int s = 0; s < R.L; ++s) R.colcap = std::max(R.colcap, R.yr[s]);
+  // envelope
+  for (int b = 0; b < R.L - 1; ++b)
+    if (!prrlu_supported(R.mmax[b], R.nmax[b]))
+      return fail(ACI_ERR_UNSUPPORTED, "aci: 2-site block " + std::to_string(R.mmax[b]) + "x" +
+                                           std::to_string(R.nmax[b]) + " exceeds the prrLU envelope");
+  for (int s = 1; s < R.L; ++s)
+    if (!prrlu_supported(R.yr[s], R.nmax[s - 1]))
+      return fail(ACI_ERR_UNSUPPORTED, "aci: y_init bond too large for the prrLU envelope");
+  return ACI_OK;
+}
+
+extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_inputs, double tol, int maxrank,
+                                  int max_sweeps, tt_t **out, aci_report *rep, const aci_options *opts) {
+  auto t_start = std::chrono::steady_clock::now();
+  if (!out) return fail(ACI_ERR_INVALID, "aci: out is null");
+  *out = nullptr;
+  if (!(tol >= 0) || maxrank < 1 || max_sweeps < 1) return fail(ACI_ERR_INVALID, "aci: tol < 0, maxrank < 1 or max_sweeps < 1");
+  aci_options o = {};
+  if (opts) o = *opts;
+  if (o.tol_mode != ACI_TOL_RELATIVE && o.tol_mode != ACI_TOL_ABSOLUTE) return fail(ACI_ERR_INVALID, "aci: bad tol_mode");
+  Inputs I;
+  int st = prepare(op, inputs, n_inputs, I);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  const tt_s *t0 = I.tts[0];
+  const int L = t0->L;
+  if (L < 2) return fail(ACI_ERR_INVALID, "aci: L must be >= 2 (the 2-site update needs two sites)");
+  cudaStream_t strm = (cudaStream_t)o.stream;
+
+  // ---- y_init (R9)
+  tt_s *ygen = nullptr;
+  const tt_s *y = o.y_init;
+  if (y) {
+    if (y->L != L || y->d != t0->d) return fail(ACI_ERR_SHAPE, "aci: y_init shape differs from the inputs");
+  } else {
+    std::vector<int> yr(L + 1, 1);
+    for (int s = 1; s < L; ++s) {
+      int r = maxrank;
+      for (auto *t : I.tts) r = std::min(r, t->ranks[s]);
+      yr[s] = (int)std::min<long long>(r, std::min(capped_prod(t0->d, 0, s - 1), capped_prod(t0->d, s, L - 1)));
+    }
+    std::vector<std::vector<double>> cores(L);
+    std::vector<const double *> ptr(L);
+    uint64_t cnt = 0;
+    for (int s = 0; s < L; ++s) {
+      cores[s].resize((size_t)yr[s] * t0->d[s] * yr[s + 1]);
+      for (auto &x : cores[s]) x = normal_at(o.seed, cnt++);
+      ptr[s] = cores[s].data();
+    }
+    st = tt_create(L, t0->d.data(), yr.data(), ptr.data(), &ygen);
+    if (st) return st;
+    y = ygen;
+  }
+
+  Run R;
+  st = build_run(I, y, maxrank, max_sweeps, R);
+  if (st) { tt_destroy(ygen); return st; }
+  size_t need = carve(R, nullptr);
+  char *ws = nullptr;
+  bool own_ws = false;
+  if (o.workspace) {
+    if (o.workspace_bytes < need) { tt_destroy(ygen); return fail(ACI_ERR_OOM, "aci: caller workspace too small"); }
+    ws = (char *)o.workspace;
+  } else {
+    static bool pool_cfg = false;
+    if (!pool_cfg) {
+      cudaMemPool_t pool;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      pool_cfg = true;
+    }
+    if (cudaMallocAsync((void **)&ws, need, strm) != cudaSuccess) {
+      tt_destroy(ygen);
+      return fail(ACI_ERR_OOM, "aci: workspace allocation failed");
+    }
+    own_ws = true;
+  }
+  carve(R, ws);
+  auto cleanup = [&]() {
+    if (own_ws) cudaFreeAsync(ws, strm);
+    tt_destroy(ygen);
+  };
+
+  // ---- initial state
+  cudaMemsetAsync(R.rk, 0, sizeof(int) * (L + 1), strm);
+  {
+    std::vector<int> rk0(L + 1, 0);
+    rk0[0] = 1; rk0[L] = 1;
+    // the only host->device copy of state: boundary ranks (pageable; tiny)
+    cudaMemcpyAsync(R.rk, rk0.data(), sizeof(int) * (L + 1), cudaMemcpyHostToDevice, strm);
+    cudaStreamSynchronize(strm);
+  }
+  cudaMemsetAsync(R.scale, 0, sizeof(unsigned long long), strm);
+  cudaMemsetAsync(R.maxeps, 0, sizeof(unsigned long long), strm);
+  cudaMemsetAsync(R.nonfinite, 0, sizeof(int), strm);
+  for (int s = 0; s < L; ++s)
+    cudaMemcpyAsync(R.Yin[s], y->dcores + y->off[s], sizeof(double) * (y->off[s + 1] - y->off[s]),
+                    cudaMemcpyDeviceToDevice, strm);
+
+  // ---- a0: CI-canonicalise y_init, right-to-left
+  for (int s = L - 1; s >= 1; --s) canon_step(R, tol, o.tol_mode, s, strm);
+  copy_prev_kernel<<<1, 64, 0, strm>>>(R.rk, R.prev, L);
+
+  // ---- main loop
+  int it = 0, converged = 0, slot = 0;
+  for (it = 1; it <= max_sweeps; ++it) {
+    for (int b = 0; b < L - 1; ++b) bond_update(R, I.op, tol, o.tol_mode, b, 0, slot++, strm);
+    for (int b = L - 2; b >= 0; --b) bond_update(R, I.op, tol, o.tol_mode, b, 1, slot++, strm);
+    converge_kernel<<<1, 32, 0, strm>>>(R.rk, R.prev, L, R.maxeps, R.scale, tol, o.tol_mode, R.conv, R.err);
+    int flag = 0;
+    cudaMemcpyAsync(&flag, R.conv, sizeof(int), cudaMemcpyDeviceToHost, strm);
+    cudaError_t e = cudaStreamSynchronize(strm);
+    if (e != cudaSuccess) { cleanup(); return fail(ACI_ERR_CUDA, std::string("aci sweep: ") + cudaGetErrorString(e)); }
+    if (flag) { converged = 1; break; }
+  }
+  if (it > max_sweeps) it = max_sweeps;
+
+  // ---- results: ranks, flags, log
+  std::vector<int> rk(L + 1);
+  int nonfinite = 0;
+  double err = 0, scale = 0;
+  unsigned long long scale_bits = 0;
+  cudaMemcpyAsync(rk.data(), R.rk, sizeof(int) * (L + 1), cudaMemcpyDeviceToHost, strm);
+  cudaMemcpyAsync(&nonfinite, R.nonfinite, sizeof(int), cudaMemcpyDeviceToHost, strm);
+  cudaMemcpyAsync(&err, R.err, sizeof(double), cudaMemcpyDeviceToHost, strm);
+  cudaMemcpyAsync(&scale_bits, R.scale, sizeof(double), cudaMemcpyDeviceToHost, strm);
+  cudaError_t e = cudaStreamSynchronize(strm);
+  if (e != cudaSuccess) { cleanup(); return fail(ACI_ERR_CUDA, std::string("aci: ") + cudaGetErrorString(e)); }
+  std::memcpy(&scale, &scale_bits, sizeof(double));
+  if (nonfinite) { cleanup(); return fail(ACI_ERR_NONFINITE, "aci: f produced NaN/Inf (S:255)"); }
+
+  // ---- a8: output cores from the last right-to-left half-sweep (R5)
+  tt_s *res = tt_alloc_shape(L, t0->d.data(), rk.data());
+  if (cudaMalloc(&res->dcores, sizeof(double) * std::max<size_t>(res->total, 1)) != cudaSuccess) {
+    delete res;
+    cleanup();
+    return fail(ACI_ERR_OOM, "aci: output allocation failed");
+  }
+  cudaMemcpyAsync(res->dcores, R.Y0, sizeof(double) * (res->off[1] - res->off[0]), cudaMemcpyDeviceToDevice, strm);
+  {
+    std::vector<TrsmArgs> ta(L - 1);
+    int rmx = 1, nmx = 1;
+    for (int b = 0; b < L - 1; ++b) {
+      ta[b].U = R.Ust[b]; ta[b].ldu = R.nmax[b]; ta[b].cols = R.pcol[b]; ta[b].b = b; ta[b].d1 = R.d[b + 1];
+      ta[b].out = res->dcores + res->off[b + 1];
+      rmx = std::max(rmx, rk[b + 1]);
+      nmx = std::max(nmx, R.d[b + 1] * rk[b + 2]);
+    }
+    cudaMemcpyAsync(R.dtrsm, ta.data(), sizeof(TrsmArgs) * (L - 1), cudaMemcpyHostToDevice, strm);
+    size_t smem = (size_t)rmx * 32 * sizeof(double);
+    static size_t smem_set = 0;
+    if (smem > 48 * 1024 && smem > smem_set) {
+      cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      smem_set = smem;
+    }
+    trsm_kernel<<<dim3((nmx + 31) / 32, L - 1), 256, smem, strm>>>(R.dtrsm, R.rk);
+    e = cudaStreamSynchronize(strm);
+    if (e != cudaSuccess) {
+      tt_destroy(res);
+      cleanup();
+      return fail(ACI_ERR_CUDA, std::string("aci output: ") + cudaGetErrorString(e));
+    }
+  }
+
+  // ---- report + optional log / index sets
+  const int nupd = slot;
+  std::vector<int> info((size_t)nupd * 5);
+  std::vector<double> es((size_t)nupd * 2);
+  cudaMemcpy(info.data(), R.log_info, sizeof(int) * info.size(), cudaMemcpyDeviceToHost);
+  cudaMemcpy(es.data(), R.log_es, sizeof(double) * es.size(), cudaMemcpyDeviceToHost);
+  aci_report rp = {};
+  rp.error_estimate = err;
+  rp.scale = scale;
+  rp.iterations = it;
+  rp.converged = converged;
+  rp.n_updates = nupd;
+  for (int s = 0; s <= L; ++s) rp.max_rank = std::max(rp.max_rank, rk[s]);
+  for (int u = 0; u < nupd; ++u) {
+    const int b = info[u * 5], rl = info[u * 5 + 2], rr = info[u * 5 + 3], r = info[u * 5 + 4];
+    const int m = rl * R.d[b], n = R.d[b + 1] * rr;
+    for (int i = 0; i < R.N; ++i) {
+      const double c0 = R.xr[i][b], c1 = R.xr[i][b + 1], c2 = R.xr[i][b + 2];
+      rp.flops_contraction += 2.0 * rl * c0 * R.d[b] * c1 + 2.0 * c1 * R.d[b + 1] * c2 * rr + 2.0 * m * c1 * n;
+    }
+    for (int k = 0; k < r; ++k) rp.flops_prrlu += 2.0 * (m - k - 1) * (double)(n - k - 1);
+    rp.pivot_steps += r;
+  }
+  for (int b = 0; b < L - 1; ++b) {
+    const double r = rk[b + 1], n = R.d[b + 1] * rk[b + 2];
+    rp.flops_trsm += r * r * (n - r);
+  }
+  if (o.log) {
+    aci_pivot_log *lg = o.log;
+    const int nw = std::min(nupd, lg->capacity_updates);
+    for (int u = 0; u < nw; ++u) {
+      if (lg->info) std::memcpy(lg->info + u * 5, &info[u * 5], sizeof(int) * 5);
+      if (lg->eps_scale) std::memcpy(lg->eps_scale + u * 2, &es[u * 2], sizeof(double) * 2);
+      const int r = std::min(info[u * 5 + 4], lg->capacity_pivots);
+      if (lg->rows) cudaMemcpy(lg->rows + (size_t)u * lg->capacity_pivots, R.log_rows + (size_t)u * R.log_cap_piv,
+                               sizeof(int) * r, cudaMemcpyDeviceToHost);
+      if (lg->cols) cudaMemcpy(lg->cols + (size_t)u * lg->capacity_pivots, R.log_cols + (size_t)u * R.log_cap_piv,
+                               sizeof(int) * r, cudaMemcpyDeviceToHost);
+    }
+    lg->n_written = nw;
+    if (lg->canon_n) {
+      std::vector<int> cn(L + 1, 0);
+      cudaMemcpy(cn.data(), R.canon_n, sizeof(int) * (L + 1), cudaMemcpyDeviceToHost);
+      for (int s = 1; s < L; ++s) {
+        lg->canon_n[s] = cn[s];
+        if (lg->canon_cols)
+          cudaMemcpy(lg->canon_cols + (size_t)s * lg->capacity_pivots, R.canon_cols + (size_t)s * R.log_cap_piv,
+                     sizeof(int) * std::min(cn[s], lg->capacity_pivots), cudaMemcpyDeviceToHost);
+      }
+    }
+  }
+  if (o.I_sets)
+    for (int b = 0; b < L - 1; ++b)
+      if (o.I_sets[b]) cudaMemcpy(o.I_sets[b], R.Imi[b], (size_t)rk[b + 1] * (b + 1), cudaMemcpyDeviceToHost);
+  if (o.J_sets)
+    for (int s = 1; s < L; ++s)
+      if (o.J_sets[s]) cudaMemcpy(o.J_sets[s], R.Jmi[s], (size_t)rk[s] * (L - s), cudaMemcpyDeviceToHost);
+  cleanup();
+  e = cudaStreamSynchronize(strm);
+  if (e != cudaSuccess) { tt_destroy(res); return fail(ACI_ERR_CUDA, std::string("aci: ") + cudaGetErrorString(e)); }
+  auto t_end = std::chrono::steady_clock::now();
+  rp.ms = std::chrono::duration<float, std::milli>(t_end - t_start).count();
+  if (rep) *rep = rp;
+  *out = res;
+  return converged ? ACI_OK : ACI_NOT_CONVERGED;
+}
+
+extern "C" int aci_elementwise(aci_op op, const tt_t *const *inputs, int n_inputs, double tol, int maxrank,
+                               int max_sweeps, tt_t **out, aci_report *rep) {
+  return aci_elementwise_ex(op, inputs, n_inputs, tol, maxrank, max_sweeps, out, rep, nullptr);
+}
+
+extern "C" int aci_workspace_query(const tt_t *const *inputs, int n_inputs, int maxrank, const tt_t *y_init,
+                                   size_t *bytes) {
+  if (!bytes || !inputs || n_inputs < 1 || maxrank < 1) return fail(ACI_ERR_INVALID, "aci_workspace_query: bad args");
+  std::vector<double> coef(1, 1.0);
+  std::vector<int> expo(n_inputs, 1);
+  aci_op op = {1, coef.data(), expo.data()};
+  Inputs I;
+  int st = prepare(op, inputs, n_inputs, I);
+  if (st) return st;
+  const tt_s *t0 = I.tts[0];
+  tt_s tmp;
+  if (!y_init) {
+    tmp.L = t0->L;
+    tmp.d = t0->d;
+    tmp.ranks.assign(t0->L + 1, 1);
+    for (int s = 1; s < t0->L; ++s) {
+      int r = maxrank;
+      for (auto *t : I.tts) r = std::min(r, t->ranks[s]);
+      tmp.ranks[s] = (int)std::min<long long>(r, std::min(capped_prod(t0->d, 0, s - 1), capped_prod(t0->d, s, t0->L - 1)));
+    }
+    y_init = &tmp;
+  }
+  Run R;
+  st = build_run(I, y_init, maxrank, 64, R);
+  if (st) return st;
+  *bytes = carve(R, nullptr);
+  return ACI_OK;
+}
+
+// ============================================================================ evaluation (K6)
+extern "C" int tt_evaluate_device(const tt_t *t, int64_t npts, const uint8_t *dev_idx, double *dev_out,
+                                  void *stream) {
+  if (!t || npts < 0 || (npts > 0 && (!dev_idx || !dev_out))) return fail(ACI_ERR_INVALID, "tt_evaluate: bad args");
+  if (npts == 0) return ACI_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int L = t->L;
+  int rmx = 1, wmx = 1;
+  for (int s = 0; s < L; ++s) {
+    rmx = std::max(rmx, t->ranks[s + 1]);
+    wmx = std::max(wmx, t->d[s] * t->ranks[s + 1]);
+  }
+  const int64_t P = 8192;
+  double *V = nullptr, *W = nullptr;
+  GemmDesc *desc = nullptr;
+  if (cudaMallocAsync((void **)&V, sizeof(double) * P * rmx, st) != cudaSuccess ||
+      cudaMallocAsync((void **)&W, sizeof(double) * P * wmx, st) != cudaSuccess ||
+      cudaMallocAsync((void **)&desc, sizeof(GemmDesc), st) != cudaSuccess)
+    return fail(ACI_ERR_OOM, "tt_evaluate: workspace");
+  FOp dummy = {};
+  for (int64_t p0 = 0; p0 < npts; p0 += P) {
+    const int np = (int)std::min<int64_t>(P, npts - p0);
+    const uint8_t *ix = dev_idx + p0 * L;
+    eval_first_kernel<<<296, 256, 0, st>>>(t->dcores, V, ix, L, t->ranks[1], np);
+    for (int s = 1; s < L; ++s) {
+      const int r0 = t->ranks[s], r1 = t->ranks[s + 1];
+      eval_desc_kernel<<<1, 1, 0, st>>>(desc, V, t->dcores + t->off[s], W, np, r0, t->d[s] * r1);
+      launch_gemm(desc, 1, np, t->d[s] * r1, 1, false, dummy, nullptr, nullptr, st);
+      eval_select_kernel<<<592, 256, 0, st>>>(W, V, ix, L, s, t->d[s], r1, np);
+    }
+    cudaMemcpyAsync(dev_out + p0, V, sizeof(double) * np, cudaMemcpyDeviceToDevice, st);
+  }
+  cudaFreeAsync(V, st);
+  cudaFreeAsync(W, st);
+  cudaFreeAsync(desc, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(ACI_ERR_CUDA, std::string("tt_evaluate: ") + cudaGetErrorString(e));
+  return ACI_OK;
+}
+
+extern "C" int tt_evaluate(const tt_t *t, int64_t npts, const uint8_t *idx, double *out) {
+  if (!t || npts < 0 || (npts > 0 && (!idx || !out))) return fail(ACI_ERR_INVALID, "tt_evaluate: bad args");
+  if (npts == 0) return ACI_OK;
+  const int L = t->L;
+  for (int64_t p = 0; p < npts; ++p)
+    for (int s = 0; s < L; ++s)
+      if (idx[p * L + s] >= t->d[s]) return fail(ACI_ERR_INVALID, "tt_evaluate: index >= d_s");
+  uint8_t *di = nullptr;
+  double *dout = nullptr;
+  CUDA_TRY(cudaMalloc(&di, (size_t)npts * L));
+  if (cudaMalloc(&dout, sizeof(double) * npts) != cudaSuccess) { cudaFree(di); return fail(ACI_ERR_OOM, "tt_evaluate"); }
+  cudaMemcpy(di, idx, (size_t)npts * L, cudaMemcpyHostToDevice);
+  int st = tt_evaluate_device(t, npts, di, dout, nullptr);
+  if (st == ACI_OK) {
+    cudaError_t e = cudaMemcpy(out, dout, sizeof(double) * npts, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) st = fail(ACI_ERR_CUDA, cudaGetErrorString(e));
+  }
+  cudaFree(di);
+  cudaFree(dout);
+  return st;
+}

@@ -1,0 +1,61 @@
+// Internal declarations shared by the translation units of libaci.so.
+// Nothing here is part of the C-ABI (include/aci.h is).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define ACI_GEMM_MAX_IN 4
+
+// One GEMM problem C = sum over inputs (FUSE: f of) A_n (M x K_n) * B_n (K_n x N), row-major.
+// Written by the planner kernels on the device (M, N, leading dims depend on live ranks).
+struct GemmDesc {
+  double *C;
+  int M, N, ldc;
+  int nin;
+  const double *A[ACI_GEMM_MAX_IN];
+  const double *B[ACI_GEMM_MAX_IN];
+  int K[ACI_GEMM_MAX_IN], lda[ACI_GEMM_MAX_IN], ldb[ACI_GEMM_MAX_IN];
+};
+
+// Elementwise f = sum_t coef[t] prod_n x_n^expo[t][n].
+struct FOp {
+  int T, N;
+  double coef[8];
+  int expo[8 * ACI_GEMM_MAX_IN];
+};
+
+// Live sizes of one prrLU problem, written by the planner on the device.
+struct LuDims {
+  int m, n, ldm;      // matrix rows, cols, leading dimension
+  int kmax;           // min(maxrank, m, n)
+  int ldu;            // leading dimension of the U rows output
+};
+
+// prrLU arguments (Alg. 2, readings R1-R4, R17).
+struct LuArgs {
+  const double *M;            // row-major matrix (device)
+  const LuDims *dims;         // live sizes
+  double tol;
+  int thr_mode;               // 0: thr = tol * s (R1); 1: thr = tol * |first candidate| (R8); 2: thr = tol
+  const unsigned long long *scale_bits;  // s as IEEE bits (non-negative double)
+  int *rows, *cols;           // pivots out (selection order, R21)
+  int *r_out;                 // rank out
+  double *eps_out;            // first rejected candidate (R2)
+  double *U;                  // optional U rows out (r x n, ld = dims->ldu), U_k = S_k[p,:]/c
+  // grid tier exchange
+  double *colpub;             // 2 x G x colcap
+  int colcap;
+  double *keyval;             // 2 x G   candidate values
+  int *keyidx;                // 2 x G x 2 candidate (row, col)
+  unsigned int *counter;      // zeroed before launch
+};
+
+// ---- launchers (defined in gemm.cu / prrlu.cu / sweep.cu) ----
+void launch_gemm(const GemmDesc *d_descs, int ndesc, int max_m, int max_n, int nin, bool fuse, const FOp &op,
+                 unsigned long long *scale_bits, int *nonfinite, cudaStream_t st);
+
+// Picks the tier for a (max_m x max_n) problem; returns false if it is out of the envelope.
+bool prrlu_supported(int max_m, int max_n);
+size_t prrlu_exchange_bytes(int max_m, int max_n);
+void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st);
+void prrlu_envelope(int *max_rows, int *max_cols);

@@ -1,0 +1,195 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star):
+  * configs[0]: identical ordered pivot lists for every update and the canonicalisation, and
+    <= 10*tol against the dense 4096-vector product;
+  * elsewhere: relative max error <= 10*tol on seeded random multi-indices and in the
+    Frobenius norm where computable; pivot lists compared and reported (identical expected
+    wherever no near-tie exists).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads import generators as G
+from workloads import make_config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def aci():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2604_00037_b200 as aci
+    aci.load()
+    return aci
+
+
+def _run_both(aci, cf, log=True, sweeps=None, index_sets=False):
+    sweeps = sweeps or cf["max_sweeps"]
+    xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+    handles = xs
+    if cf["cfg"] == 2:  # psi^3 with three aliased handles (deduplicated by the library)
+        handles = [xs[0], xs[0], xs[0]]
+        op = {"coef": [1.0], "expo": [[1, 1, 1]]}
+    else:
+        op = cf["op"]
+    y0 = aci.TensorTrain.from_cores(cf["y_init"])
+    out, st, rep, ex = aci.aci_elementwise(op, handles, cf["tol"], cf["maxrank"], sweeps, y_init=y0, log=log,
+                                           index_sets=index_sets)
+    ref = oracle.aci(cf["inputs"], cf["op"], cf["y_init"], cf["tol"], cf["maxrank"], sweeps)
+    return out, st, rep, ex, ref
+
+
+def _pivot_agreement(ex, ref):
+    """Number of leading updates whose ordered pivot lists are identical."""
+    k = 0
+    for g, o in zip(ex["log"], ref.log):
+        if g["bond"] != o["bond"] or g["dir"] != o["dir"] or g["r"] != o["r"]:
+            break
+        if not (np.array_equal(g["rows"], o["rows"]) and np.array_equal(g["cols"], o["cols"])):
+            break
+        k += 1
+    return k
+
+
+def _rel(y, r):
+    return np.abs(y - r).max() / np.abs(r).max()
+
+
+def test_cfg0_identical_pivots_and_dense(aci):
+    cf = make_config(0, npts=0)
+    out, st, rep, ex, ref = _run_both(aci, cf, index_sets=True)
+    assert len(ex["log"]) == len(ref.log)
+    assert _pivot_agreement(ex, ref) == len(ref.log)
+    for s in range(1, 12):
+        assert np.array_equal(ex["canon_cols"][s], ref.canon_cols(s))
+        assert np.array_equal(ex["J"][s], ref.Jset(s))
+    for b in range(11):
+        assert np.array_equal(ex["I"][b], ref.Iset(b))
+    assert [e["eps"] for e in ex["log"]] == pytest.approx([e["eps"] for e in ref.log], rel=1e-6, abs=1e-18)
+    x = np.arange(4096) / 4096.0
+    m0, m1 = cf["inputs"][0].meta, cf["inputs"][1].meta
+    fa = sum(a * np.cos(2 * np.pi * k * x + p) for k, p, a in zip(m0["ks"], m0["phis"], m0["amps"]))
+    fb = sum(a * np.cos(2 * np.pi * k * x + p) for k, p, a in zip(m1["ks"], m1["phis"], m1["amps"]))
+    dense = oracle.tt_dense(out.cores())
+    assert _rel(dense, fa * fb) <= 10 * cf["tol"]
+    assert _rel(dense, oracle.tt_dense(ref.cores)) <= 10 * cf["tol"]
+    assert rep["converged"] == ref.report["converged"] and rep["iterations"] == ref.report["iterations"]
+    _, ranks = out.shape()
+    assert ranks == ref.ranks
+
+
+def test_cfg1_vs_oracle_and_exact(aci):
+    cf = make_config(1, npts=100_000)
+    out, st, rep, ex, ref = _run_both(aci, cf)
+    s = cf["samples"]
+    y = out.evaluate(s)
+    yo = oracle.tt_evaluate(ref.cores, s)
+    exact = oracle.tt_evaluate(cf["inputs"][0], s) * oracle.tt_evaluate(cf["inputs"][1], s)
+    assert _rel(y, yo) <= 10 * cf["tol"]
+    assert _rel(y, exact) <= 10 * cf["tol"]
+    _, ranks = out.shape()
+    assert max(ranks) <= 64
+    ker = oracle.exact_product(cf["inputs"], cf["op"])
+    cores = out.cores()
+    nr = oracle.tt_inner(ker, ker)
+    d2 = oracle.tt_inner(cores, cores) - 2 * oracle.tt_inner(cores, ker) + nr
+    assert math.sqrt(max(d2, 0) / nr) <= 10 * cf["tol"] + 1e-7
+    assert _pivot_agreement(ex, ref) == len(ref.log)
+
+
+def test_cfg3_chi64_vs_oracle(aci):
+    cf = make_config(3, 64, npts=20_000)
+    out, st, rep, ex, ref = _run_both(aci, cf)
+    s = cf["samples"]
+    y = out.evaluate(s)
+    exact = oracle.tt_evaluate(cf["inputs"][0], s) * oracle.tt_evaluate(cf["inputs"][1], s)
+    assert _rel(y, oracle.tt_evaluate(ref.cores, s)) <= 10 * cf["tol"]
+    assert _rel(y, exact) <= 10 * cf["tol"]
+    assert max(out.shape()[1]) == 128
+    agree = _pivot_agreement(ex, ref)
+    assert agree == len(ref.log), f"pivots identical for {agree}/{len(ref.log)} updates"
+
+
+def test_evaluate_matches_oracle(aci):
+    rng = np.random.default_rng(3)
+    t = G.random_tt(9, 3, 37, rng)
+    idx = G.sample_indices(t.d, 20000, rng)
+    h = aci.TensorTrain.from_cores(t)
+    assert _rel(h.evaluate(idx), oracle.tt_evaluate(t, idx)) <= 1e-13
+    cores = h.cores()
+    assert all(np.array_equal(a, b) for a, b in zip(cores, t.cores))
+
+
+def test_identity_op_and_rank_one(aci):
+    rng = np.random.default_rng(21)
+    x = G.random_tt(10, 2, 8, rng)
+    y0 = G.random_init([x], 8, rng)
+    hx, hy = aci.TensorTrain.from_cores(x), aci.TensorTrain.from_cores(y0)
+    out, st, rep, _ = aci.aci_elementwise({"coef": [1.0], "expo": [[1]]}, [hx], 1e-12, 64, 20, y_init=hy)
+    assert rep["converged"] and rep["iterations"] <= 2
+    assert _rel(oracle.tt_dense(out.cores()), oracle.tt_dense(x)) <= 1e-10
+    a, b = G.random_tt(9, 2, 1, rng), G.random_tt(9, 2, 1, rng)
+    ha, hb = aci.TensorTrain.from_cores(a), aci.TensorTrain.from_cores(b)
+    out, st, rep, _ = aci.aci_elementwise({"coef": [1.0], "expo": [[1, 1]]}, [ha, hb], 1e-12, 16, 10, seed=5)
+    assert max(out.shape()[1]) == 1
+    assert _rel(oracle.tt_dense(out.cores()), oracle.tt_dense(a) * oracle.tt_dense(b)) <= 1e-13
+
+
+def test_zero_function(aci):
+    """f == 0 everywhere: every Pi is 0 -> rank 1, dummy pivots, zero output (R17)."""
+    rng = np.random.default_rng(4)
+    a = G.random_tt(6, 2, 3, rng)
+    zero = G.TT([np.zeros_like(c) for c in a.cores])
+    ha, hz = aci.TensorTrain.from_cores(a), aci.TensorTrain.from_cores(zero)
+    y0 = aci.TensorTrain.from_cores(G.random_init([a], 8, rng))
+    out, st, rep, ex = aci.aci_elementwise({"coef": [1.0], "expo": [[1, 1]]}, [ha, hz], 1e-10, 8, 3, y_init=y0,
+                                           log=True)
+    assert max(out.shape()[1]) == 1
+    assert np.abs(oracle.tt_dense(out.cores())).max() == 0.0
+    assert all(e["r"] == 1 and e["eps"] == 0.0 for e in ex["log"])
+
+
+def test_small_random_suite_vs_oracle(aci):
+    """SPEC acceptance suite shapes: identical pivots and dense agreement with the oracle,
+    including d = 3 local dimensions, L = 2 and 3-input polynomials."""
+    rng = np.random.default_rng(2024)
+    ops = [({"coef": [1.0], "expo": [[1, 1]]}, 2), ({"coef": [1.0, 1.0], "expo": [[1, 0], [0, 1]]}, 2),
+           ({"coef": [1.0, -0.5], "expo": [[1, 1, 0], [0, 0, 2]]}, 3)]
+    for trial in range(18):
+        L = int(rng.integers(2, 9))
+        d = 3 if trial % 4 == 3 else 2
+        op, N = ops[trial % 3]
+        xs = [G.random_tt(L, d, int(rng.integers(1, 6)), rng) for _ in range(N)]
+        y0 = G.random_init(xs, 64, rng)
+        hs = [aci.TensorTrain.from_cores(x) for x in xs]
+        out, st, rep, ex = aci.aci_elementwise(op, hs, 1e-10, 64, 8, y_init=aci.TensorTrain.from_cores(y0),
+                                               log=True)
+        ref = oracle.aci(xs, op, y0, 1e-10, 64, 8)
+        assert _pivot_agreement(ex, ref) == len(ref.log), trial
+        assert _rel(oracle.tt_dense(out.cores()), oracle.tt_dense(ref.cores)) <= 1e-9, trial
+
+
+def test_errors(aci):
+    rng = np.random.default_rng(9)
+    a = aci.TensorTrain.from_cores(G.random_tt(5, 2, 2, rng))
+    b = aci.TensorTrain.from_cores(G.random_tt(6, 2, 2, rng))
+    with pytest.raises(aci.AciError) as e:
+        aci.aci_elementwise({"coef": [1.0], "expo": [[1, 1]]}, [a, b], 1e-8, 8, 2)
+    assert "SHAPE" in str(e.value)
+    with pytest.raises(aci.AciError):
+        aci.aci_elementwise({"coef": [1.0], "expo": [[1, 1]]}, [a, a], -1.0, 8, 2)
+    bad = G.random_tt(5, 2, 2, rng)
+    bad.cores[2][0, 0, 0] = np.nan
+    with pytest.raises(aci.AciError) as e:
+        aci.TensorTrain.from_cores(bad)
+    assert "NONFINITE" in str(e.value)
+    big = aci.TensorTrain.from_cores(G.random_tt(5, 2, 2, rng))
+    with pytest.raises(aci.AciError) as e:  # f overflows to inf
+        aci.aci_elementwise({"coef": [1e308], "expo": [[4]]}, [big], 1e-8, 8, 2)
+    assert "NONFINITE" in str(e.value)

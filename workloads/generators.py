@@ -175,11 +175,19 @@ def gaussian3d_tt(nbits: int, cs, sigmas, amps, cutoff=1e-12) -> TT:
     return tt
 
 
+def _bond_bound(d: list, s: int) -> int:
+    """Largest possible rank of bond s-1|s of any tensor: min(prod d[:s], prod d[s:])."""
+    left = int(np.prod([float(x) for x in d[:s]]))
+    right = int(np.prod([float(x) for x in d[s:]]))
+    return min(left, right, 1 << 30)
+
+
 def random_init(inputs: list, maxrank: int, rng: np.random.Generator) -> TT:
-    """y_init: bond ranks min_n chi^n_l capped at maxrank, iid N(0,1) entries (R9)."""
+    """y_init: bond ranks min_n chi^n_l capped at maxrank and at the full-tensor bound
+    min(prod d_left, prod d_right) (R9'), iid N(0,1) entries (R9)."""
     L = inputs[0].L
     d = inputs[0].d
-    ranks = [1] + [min(min(t.ranks[s] for t in inputs), maxrank) for s in range(1, L)] + [1]
+    ranks = [1] + [min(min(t.ranks[s] for t in inputs), maxrank, _bond_bound(d, s)) for s in range(1, L)] + [1]
     cores = [rng.standard_normal((ranks[s], d[s], ranks[s + 1])) for s in range(L)]
     return TT(cores, {"kind": "y_init"})
 

@@ -1,0 +1,330 @@
+"""Benchmark: one ACI Hadamard product of BASELINE.json configs[3] at chi = 256 per step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--chi 256] [--impl ours|reference]
+
+A step is one full aci_elementwise call (canonicalisation + 4 iterations of L->R / R->L 2-site
+updates + output cores) over device-resident inputs. `value` is the contraction-model FP64
+TFLOP/s aggregated over ranks; `ms_per_step` is the wall time of one product
+(device time, CUDA events on the call's stream). L2 is flushed (256 MiB write) between timed
+steps, outside the timed region. Multi-GPU runs independent replicas (one
+product does not shard), `scaling` = "weak".
+
+--impl reference times the CPU oracle (oracle/, naive-loop C, single thread) on a bounded
+sample of the same workload (the first iterations), rank 0 only.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ACI Hadamard-product wall time (ms) and FP64 TFLOP/s vs χ; fraction of FP64 peak"
+UNIT = "TFLOP/s (FP64, contraction model)"
+
+
+def _peaks():
+    """Roofline denominators: MEASURED_PEAKS.json has no FP64 entry, so the FP64 peaks are the
+    ones measured on this pool by tools/probe (profiles/r01_probe_sync_dmma.txt,
+    profiles/r01_dgemm_peak.json): DMMA 37.1 TF/s, DFMA 34.0 TF/s, cuBLAS DGEMM 35.5 TF/s."""
+    p = {"dmma_tflops": 37.13, "dfma_tflops": 33.97, "dgemm_tflops": 35.46, "source": "measured (tools/probe)"}
+    try:
+        m = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        p["hbm_gbs"] = m.get("hbm_gbs")
+        for k in ("fp64_tflops", "dgemm_tflops"):
+            if k in m:
+                p["dgemm_tflops"] = m[k]
+    except Exception:
+        p["hbm_gbs"] = 6539.9
+    return p
+
+
+class ClockSampler:
+    def __init__(self, gpu_index=0):
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out = self.proc.communicate()[0].strip().splitlines()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    """The oracle (CPU, single thread) on a bounded sample of the workload."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import oracle
+    from workloads import make_config
+    cf = make_config(3, args.chi, npts=0)
+    sweeps = args.ref_sweeps
+    times, flops = [], []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        res = oracle.aci(cf["inputs"], cf["op"], cf["y_init"], cf["tol"], cf["maxrank"], sweeps)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            flops.append(res.report["flops_contraction"])
+        res.free()
+    tot_t, tot_f = sum(times), sum(flops)
+    value = tot_f / tot_t / 1e12
+    sample = (f"configs[3] chi={args.chi}: oracle ACI with max_sweeps={sweeps} (first {sweeps} of "
+              f"{cf['max_sweeps']} iterations), contraction-model flops / wall time")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": cf["name"], "chi": args.chi, "L": 40, "d": 2, "maxrank": cf["maxrank"],
+                       "tol": cf["tol"], "iterations": sweeps, "parallelism": "replicas",
+                       "l2": "n/a (CPU)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(chi, sweeps):
+    import oracle
+    from workloads import make_config
+    cf = make_config(3, chi, npts=0)
+    t0 = time.perf_counter()
+    res = oracle.aci(cf["inputs"], cf["op"], cf["y_init"], cf["tol"], cf["maxrank"], sweeps)
+    dt = time.perf_counter() - t0
+    v = res.report["flops_contraction"] / dt / 1e12
+    res.free()
+    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"configs[3] chi={chi}, first {sweeps} of 4 iterations, single-thread naive C oracle, "
+                      f"{dt:.1f} s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--chi", type=int, default=256)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-sweeps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep-chi", action="store_true", help="also print lines for chi=64,128 (stderr)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import paper_2604_00037_b200 as aci
+    from workloads import make_config
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    aci.load()
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    def run_chi(chi, steps, warmup, with_e2e):
+        cf = make_config(3, chi, npts=0)
+        xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+        y0 = aci.TensorTrain.from_cores(cf["y_init"])
+        flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+        for _ in range(warmup):
+            out, st, rep, _ = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"],
+                                                  y_init=y0, stream=sptr)
+            out.free()
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local)
+        sampler.start()
+        tot_ms, tot_flops, launches = 0.0, 0.0, 0
+        prof_tot = {}
+        reps = []
+        for i in range(steps):
+            flush.fill_(float(i))
+            torch.cuda.synchronize()
+            if dist is not None:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out, st, rep, ex = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"],
+                                                   y_init=y0, stream=sptr, profile=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tot_ms += e0.elapsed_time(e1)
+            tot_flops += rep["flops_contraction"]
+            launches += rep["n_launches"]
+            for k, v in ex["profile"].items():
+                p = prof_tot.setdefault(k, {"ms": 0.0, "launches": 0})
+                p["ms"] += v["ms"]
+                p["launches"] += v["launches"]
+            reps.append(rep)
+            out.free()
+        clocks = sampler.stop()
+        e2e = None
+        if with_e2e:
+            e2e = run_e2e(cf, steps, sptr)
+        return cf, tot_ms, tot_flops, launches, prof_tot, reps, clocks, e2e
+
+    def run_e2e(cf, steps, sptr):
+        """Same product through the public C-ABI from pinned host buffers: H2D of the inputs and
+        y_init (tt_create), the product, D2H of every output core (tt_get_cores)."""
+        pinned_in = []
+        for t in list(cf["inputs"]) + [cf["y_init"]]:
+            pc = []
+            for c in t.cores:
+                buf = torch.empty(c.shape, dtype=torch.float64, pin_memory=True)
+                buf.numpy()[...] = c
+                pc.append(buf.numpy())
+            pinned_in.append(pc)
+        h2d = sum(c.nbytes for pc in pinned_in for c in pc)
+        tot, d2h = 0.0, 0
+        out_bufs = None
+        for i in range(steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            hx = [aci.TensorTrain.from_cores(pc) for pc in pinned_in[:-1]]
+            hy = aci.TensorTrain.from_cores(pinned_in[-1])
+            out, st, rep, _ = aci.aci_elementwise(cf["op"], hx, cf["tol"], cf["maxrank"], cf["max_sweeps"],
+                                                  y_init=hy, stream=sptr)
+            d, r = out.shape()
+            if out_bufs is None or [b.shape for b in out_bufs] != [(r[s], d[s], r[s + 1]) for s in range(len(d))]:
+                out_bufs = [torch.empty((r[s], d[s], r[s + 1]), dtype=torch.float64, pin_memory=True).numpy()
+                            for s in range(len(d))]
+            import ctypes as C
+            ptrs = (C.POINTER(C.c_double) * len(d))(*[b.ctypes.data_as(C.POINTER(C.c_double)) for b in out_bufs])
+            aci._binding._check(aci.load().tt_get_cores(out.handle, ptrs))
+            dt = time.perf_counter() - t0
+            out.free()
+            for h in hx + [hy]:
+                h.free()
+            if i > 0:  # first iteration is the e2e warm-up
+                tot += dt
+                d2h = sum(b.nbytes for b in out_bufs)
+                fl = rep["flops_contraction"]
+        return {"value": fl * steps / tot / 1e12, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * tot / steps}
+
+    if args.sweep_chi:
+        for chi in (64, 128):
+            cf, ms, fl, _, prof, reps, _, _ = run_chi(chi, args.steps, args.warmup, False)
+            print(json.dumps({"chi": chi, "ms_per_product": ms / args.steps, "tflops": fl / ms / 1e9,
+                              "prrlu_ms": prof["prrlu"]["ms"] / args.steps,
+                              "gemm_pi_ms": prof["gemm_pi"]["ms"] / args.steps}), file=sys.stderr, flush=True)
+
+    cf, tot_ms, tot_flops, launches, prof, reps, clocks, e2e = run_chi(args.chi, args.steps, args.warmup,
+                                                                       with_e2e=True)
+    # max over ranks for time, sum over ranks for work
+    t_max, f_sum = tot_ms, tot_flops
+    if dist is not None:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        f = torch.tensor([tot_flops], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(f, op=dist.ReduceOp.SUM)
+        t_max, f_sum = float(t.item()), float(f.item())
+        if e2e is not None:
+            ev = torch.tensor([e2e["value"]], dtype=torch.float64, device="cuda")
+            dist.all_reduce(ev, op=dist.ReduceOp.SUM)
+            e2e["value"] = float(ev.item())
+    if rank == 0:
+        pk = _peaks()
+        value = f_sum / t_max / 1e9  # GFLOP/ms -> TFLOP/s
+        steps = args.steps
+        r0 = reps[-1]
+        # dominant kernel class by summed event time
+        dom = max(prof, key=lambda k: prof[k]["ms"])
+        pr = prof["prrlu"]
+        pi = prof["gemm_pi"]
+        prrlu_flops = sum(r["flops_prrlu"] for r in reps)
+        pi_flops = sum(r["flops_contraction"] for r in reps)  # a3 dominates; a1/a2 included
+        roof_prrlu = {"kernel": "prrlu_kernel (a5)", "bound": "alu",
+                      "achieved": prrlu_flops / (pr["ms"] * 1e9) if pr["ms"] else None,
+                      "peak": pk["dfma_tflops"], "unit": "TFLOP/s",
+                      "frac": (prrlu_flops / (pr["ms"] * 1e9)) / pk["dfma_tflops"] if pr["ms"] else None,
+                      "traffic": None, "per_launch_us": 1e3 * pr["ms"] / max(pr["launches"], 1),
+                      "per_pivot_us": 1e3 * pr["ms"] / max(sum(r["pivot_steps"] for r in reps), 1),
+                      "note": "latency-bound: one inter-CTA exchange per pivot (DESIGN.md §6); peak = measured "
+                              "DFMA rate"}
+        roof_pi = {"kernel": "gemm_dmma_kernel<fused f> (a3+a4) + a1/a2", "bound": "tensor",
+                   "achieved": pi_flops / ((pi["ms"] + prof["gemm_ab"]["ms"]) * 1e9),
+                   "peak": pk["dmma_tflops"], "unit": "TFLOP/s",
+                   "frac": pi_flops / ((pi["ms"] + prof["gemm_ab"]["ms"]) * 1e9) / pk["dmma_tflops"],
+                   "traffic": None, "note": "FP64 DMMA (mma.sync m8n8k4); peak = measured DMMA microbenchmark"}
+        roof = roof_prrlu if dom == "prrlu" else roof_pi
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": t_max / steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cf["name"], "chi": args.chi, "L": 40, "d": 2, "maxrank": cf["maxrank"],
+                       "tol": cf["tol"], "iterations": cf["max_sweeps"], "parallelism": f"replicas x{ws}",
+                       "l2": "flushed (256 MiB write) between steps"},
+            "roofline": roof,
+            "roofline_kernels": {"prrlu": roof_prrlu, "contraction": roof_pi},
+            "kernel_ms_per_step": {k: v["ms"] / steps for k, v in prof.items()},
+            "fraction_of_fp64_peak_end_to_end": value / ws / pk["dmma_tflops"],
+            "clocks": clocks,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "product": {"iterations": r0["iterations"], "converged": bool(r0["converged"]),
+                        "max_rank": r0["max_rank"], "pivot_steps": r0["pivot_steps"],
+                        "flops_contraction": r0["flops_contraction"], "flops_prrlu": r0["flops_prrlu"],
+                        "error_estimate": r0["error_estimate"]},
+            "peaks": pk,
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args.chi, args.ref_sweeps)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -102,7 +102,23 @@ typedef struct {
   double flops_trsm;         /* output cores: r^2 (n - r) per bond */
   double flops_init;         /* canonicalisation GEMMs */
   float ms;                  /* host wall time of the call (includes the final sync) */
+  int64_t n_launches;        /* kernels this call launched */
 } aci_report;
+
+/* Optional per-kernel-class device timing (CUDA events around each launch on the call's
+ * stream; adds a few microseconds per launch). Classes: */
+#define ACI_PROF_CANON 0     /* a0: canonicalisation (all its kernels) */
+#define ACI_PROF_GEMM_AB 1   /* a1/a2: A = L X, B = X R */
+#define ACI_PROF_GEMM_PI 2   /* a3+a4: Pi = f(A1 B1, ...) */
+#define ACI_PROF_PRRLU 3     /* a5: prrLU */
+#define ACI_PROF_UPDATE 4    /* a6/a7: index sets + frames (+ planning) */
+#define ACI_PROF_CONV 5      /* a9: convergence */
+#define ACI_PROF_TRSM 6      /* a8: output cores */
+#define ACI_PROF_NCLASS 7
+typedef struct {
+  double ms[ACI_PROF_NCLASS];        /* out: summed event time per class */
+  int64_t launches[ACI_PROF_NCLASS]; /* out: launches per class */
+} aci_profile;
 
 /* Optional per-update log (for parity tests): entries in update order. */
 typedef struct {
@@ -133,6 +149,7 @@ typedef struct {
    * I_sets[b] must hold (>= out rank of bond b) x (b+1) bytes; J_sets[s] (>= rank) x (L-s). */
   uint8_t **I_sets;
   uint8_t **J_sets;
+  aci_profile *profile;      /* optional: per-class device times of this call */
 } aci_options;
 
 /*

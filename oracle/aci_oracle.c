@@ -54,8 +54,8 @@ typedef struct {
   int *rows;    /* pivot rows, in selection order (R21) */
   int *cols;    /* pivot columns */
   double *D;    /* pivot values */
-  double *U;    /* r x n, U_k = S_k[p_k, :] / S_k[p_k, q_k] (R4) */
-  double *Lc;   /* m x r, L_k = S_k[:, q_k] / S_k[p_k, q_k] (R4) */
+  double *U;    /* r x n, U_k = S_k[p_k, :] * [S_k[p_k, q_k]]^{-1}, U_k[q_k] = 1 (R4) */
+  double *Lc;   /* m x r, L_k = S_k[:, q_k] * [S_k[p_k, q_k]]^{-1}, L_k[p_k] = 1 (R4) */
   double eps;   /* |c| of the first rejected candidate; 0 if exhausted (R2) */
   double first; /* |c| of the first candidate = max |M| */
 } ldu_t;
@@ -74,7 +74,7 @@ static void ldu_free(ldu_t *f) {
  *     if k == maxrank: eps = |c|, stop
  *     if k > 0 and |c| <= thr: eps = |c|, stop (candidate rejected, R2)
  *     if k == 0 and c == 0: dummy pivot (p,q), D=0, U = e_q, eps = 0, stop (R17)
- *     accept; U_k = S[p,:]/c ; L_k = S[:,q]/c ;
+ *     accept; inv = 1/c; U_k = S[p,:]*inv (U_k[q] = 1) ; L_k = S[:,q]*inv (L_k[p] = 1) ;
  *     S_ij <- fma(-l_i, S_pj, S_ij) on the active trailing block (R4)
  * thr_mode: 0 = absolute thr; 1 = thr * |first candidate| (relative to own max, R8).
  * Returns ORC_ERR_NONFINITE if M contains NaN/Inf.
@@ -121,14 +121,16 @@ static int ldu(int m, int n, const double *M, double thr, int thr_mode, int maxr
       k = 1;
       break;
     }
-    for (int j = 0; j < n; ++j) out->U[(size_t)k * n + j] = coldone[j] ? 0.0 : S[(size_t)p * n + j] / c;
-    for (int i = 0; i < m; ++i) out->Lc[(size_t)i * (kcap + 1) + k] = rowdone[i] ? 0.0 : S[(size_t)i * n + q] / c;
+    /* P:535 multiplies by [M_{chi,chi}]^{-1}: one reciprocal per pivot (R4) */
+    const double inv = 1.0 / c;
+    for (int j = 0; j < n; ++j) out->U[(size_t)k * n + j] = coldone[j] ? 0.0 : S[(size_t)p * n + j] * inv;
+    for (int i = 0; i < m; ++i) out->Lc[(size_t)i * (kcap + 1) + k] = rowdone[i] ? 0.0 : S[(size_t)i * n + q] * inv;
     out->U[(size_t)k * n + q] = 1.0;
     out->Lc[(size_t)p * (kcap + 1) + k] = 1.0;
-    /* Schur complement on the active block, l_i = S_iq / S_pq, fma order fixed (R4) */
+    /* Schur complement on the active block, l_i = S_iq * [S_pq]^{-1}, fma order fixed (R4) */
     for (int i = 0; i < m; ++i) {
       if (rowdone[i] || i == p) continue;
-      double l = S[(size_t)i * n + q] / c;
+      double l = S[(size_t)i * n + q] * inv;
       for (int j = 0; j < n; ++j) {
         if (coldone[j] || j == q) continue;
         S[(size_t)i * n + j] = fma(-l, S[(size_t)p * n + j], S[(size_t)i * n + j]);

@@ -38,7 +38,8 @@ class aci_report(C.Structure):
     _fields_ = [("error_estimate", C.c_double), ("scale", C.c_double), ("iterations", C.c_int),
                 ("converged", C.c_int), ("max_rank", C.c_int), ("n_updates", C.c_int),
                 ("pivot_steps", C.c_int64), ("flops_contraction", C.c_double), ("flops_prrlu", C.c_double),
-                ("flops_trsm", C.c_double), ("flops_init", C.c_double), ("ms", C.c_float)]
+                ("flops_trsm", C.c_double), ("flops_init", C.c_double), ("ms", C.c_float),
+                ("n_launches", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -50,11 +51,21 @@ class aci_pivot_log(C.Structure):
                 ("n_written", C.c_int), ("canon_n", C.POINTER(C.c_int)), ("canon_cols", C.POINTER(C.c_int))]
 
 
+PROF_CLASSES = ["canon", "gemm_ab", "gemm_pi", "prrlu", "update", "conv", "trsm"]
+
+
+class aci_profile(C.Structure):
+    _fields_ = [("ms", C.c_double * 7), ("launches", C.c_int64 * 7)]
+
+    def as_dict(self):
+        return {k: {"ms": self.ms[i], "launches": int(self.launches[i])} for i, k in enumerate(PROF_CLASSES)}
+
+
 class aci_options(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("y_init", C.c_void_p), ("tol_mode", C.c_int),
                 ("log", C.POINTER(aci_pivot_log)), ("stream", C.c_void_p), ("workspace", C.c_void_p),
                 ("workspace_bytes", C.c_size_t), ("I_sets", C.POINTER(C.POINTER(C.c_uint8))),
-                ("J_sets", C.POINTER(C.POINTER(C.c_uint8)))]
+                ("J_sets", C.POINTER(C.POINTER(C.c_uint8))), ("profile", C.POINTER(aci_profile))]
 
 
 _lib = None
@@ -180,7 +191,7 @@ def _make_op(op, n_inputs):
 
 
 def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, tol_mode=TOL_RELATIVE,
-                    log=False, stream=0, workspace=None, index_sets=False):
+                    log=False, stream=0, workspace=None, index_sets=False, profile=False):
     """Run aci_elementwise_ex. ``inputs`` are TensorTrain handles (aliases allowed).
 
     Returns (TensorTrain, status, report dict, extras dict).
@@ -199,6 +210,9 @@ def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, t
     extras = {}
     if workspace is not None:
         opts.workspace, opts.workspace_bytes = workspace
+    if profile:
+        prof = aci_profile()
+        opts.profile = C.pointer(prof)
     L = len(inputs[0].shape()[0])
     if log:
         cap_u = 2 * (L - 1) * max_sweeps
@@ -225,6 +239,8 @@ def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, t
                                 C.byref(opts))
     _check(st)
     res = TensorTrain(out)
+    if profile:
+        extras["profile"] = prof.as_dict()
     if log:
         nw = lg.n_written
         extras["log"] = [{"bond": int(info[u, 0]), "dir": int(info[u, 1]), "rl": int(info[u, 2]),

@@ -492,7 +492,57 @@ struct Carver {
   }
 };
 
+// Launch accounting and optional per-class CUDA-event timing (aci_options.profile).
+struct Prof {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  int64_t launches[ACI_PROF_NCLASS] = {};
+  int64_t total = 0;
+  struct Span { int cls; cudaEvent_t a, b; };
+  std::vector<Span> spans;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  int cur = -1;
+  cudaEvent_t cur_a = nullptr;
+  cudaEvent_t get() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void begin(int cls) {
+    cur = cls;
+    if (on) {
+      cur_a = get();
+      cudaEventRecord(cur_a, st);
+    }
+  }
+  void end(int nlaunch) {
+    launches[cur] += nlaunch;
+    total += nlaunch;
+    if (on) {
+      cudaEvent_t b = get();
+      cudaEventRecord(b, st);
+      spans.push_back({cur, cur_a, b});
+    }
+  }
+  void collect(aci_profile *out) {
+    for (int c = 0; c < ACI_PROF_NCLASS; ++c) { out->ms[c] = 0.0; out->launches[c] = launches[c]; }
+    for (auto &sp : spans) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, sp.a, sp.b);
+      out->ms[sp.cls] += ms;
+    }
+  }
+  ~Prof() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
 struct Run {
+  Prof *P = nullptr;
   int L = 0, N = 0, maxrank = 0, max_sweeps = 0, log_cap_upd = 0, log_cap_piv = 0, colcap = 0;
   std::vector<int> d, yr;
   std::vector<std::vector<int>> xr;      // [n][s], s = 0..L
@@ -512,8 +562,8 @@ struct Run {
   LuDims *dLu = nullptr;
   int *log_info = nullptr, *log_rows = nullptr, *log_cols = nullptr, *canon_n = nullptr, *canon_cols = nullptr;
   double *log_es = nullptr;
-  double *colpub = nullptr, *keyval = nullptr;
-  int *keyidx = nullptr;
+  double *colpub = nullptr;
+  unsigned *keys = nullptr;
   unsigned *counter = nullptr;
   TrsmArgs *dtrsm = nullptr;
 };
@@ -606,8 +656,7 @@ static size_t carve(Run &R, char *base) {
   R.canon_n = c.take<int>(L + 1);
   R.canon_cols = c.take<int>((size_t)(L + 1) * R.log_cap_piv);
   R.colpub = c.take<double>((size_t)2 * 148 * R.colcap);
-  R.keyval = c.take<double>(2 * 148);
-  R.keyidx = c.take<int>(2 * 148);
+  R.keys = c.take<unsigned>(2 * 148 * 4);
   R.counter = c.take<unsigned>(1);
   R.dtrsm = c.take<TrsmArgs>(L);
   return c.off + 256;
@@ -728,17 +777,29 @@ static void bond_update(Run &R, const FOp &op, double tol, int tol_mode, int b, 
     if (I.Lprev) { ab_m = std::max(ab_m, R.rmax[b - 1]); ab_n = std::max(ab_n, S.db * I.c1); }
     if (I.Rnext) { ab_m = std::max(ab_m, I.c1 * S.db1); ab_n = std::max(ab_n, R.rmax[b + 1]); }
   }
+  R.P->begin(ACI_PROF_UPDATE);
   plan_bond_kernel<<<1, 1, 0, st>>>(S, R.rk, R.dAB, R.dPi, R.dLu);
-  if (ab_m > 0) launch_gemm(R.dAB, 2 * N, ab_m, ab_n, 1, false, op, nullptr, nullptr, st);
+  R.P->end(1);
+  if (ab_m > 0) {
+    R.P->begin(ACI_PROF_GEMM_AB);
+    launch_gemm(R.dAB, 2 * N, ab_m, ab_n, 1, false, op, nullptr, nullptr, st);
+    R.P->end(1);
+  }
+  R.P->begin(ACI_PROF_GEMM_PI);
   launch_gemm(R.dPi, 1, R.mmax[b], R.nmax[b], N, true, op, R.scale, R.nonfinite, st);
+  R.P->end(1);
   LuArgs a = {};
   a.M = R.Pi; a.dims = R.dLu; a.tol = tol; a.thr_mode = tol_mode == ACI_TOL_RELATIVE ? 0 : 2;
   a.scale_bits = R.scale;
   a.rows = R.prow[b]; a.cols = R.pcol[b]; a.r_out = R.rout + b; a.eps_out = R.epsb + b;
   a.U = dir == 1 ? R.Ust[b] : nullptr;
-  a.colpub = R.colpub; a.colcap = R.colcap; a.keyval = R.keyval; a.keyidx = R.keyidx; a.counter = R.counter;
+  a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter;
+  R.P->begin(ACI_PROF_PRRLU);
   launch_prrlu(a, R.mmax[b], R.nmax[b], st);
+  R.P->end(1);
+  R.P->begin(ACI_PROF_UPDATE);
   launch_update(R, b, dir, logslot, st);
+  R.P->end(1);
 }
 
 static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st) {
@@ -759,6 +820,7 @@ static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st)
     C.c1[n] = R.xr[n][s + 1];
     if (C.Rnext[n]) { tm = std::max(tm, C.c0[n] * C.ds); tn = std::max(tn, R.rmax[s]); }
   }
+  R.P->begin(ACI_PROF_CANON);
   plan_canon_kernel<<<1, 1, 0, st>>>(C, R.rk);
   FOp dummy = {};
   if (tm > 0) launch_gemm(R.dT, N, tm, tn, 1, false, dummy, nullptr, nullptr, st);
@@ -768,7 +830,7 @@ static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st)
   a.scale_bits = R.scale;
   a.rows = R.prow[s - 1]; a.cols = R.pcol[s - 1]; a.r_out = R.rout + (s - 1); a.eps_out = R.epsb + (s - 1);
   a.U = nullptr;
-  a.colpub = R.colpub; a.colcap = R.colcap; a.keyval = R.keyval; a.keyidx = R.keyidx; a.counter = R.counter;
+  a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter;
   launch_prrlu(a, max_m, max_n, st);
   CanonUpd U = {};
   U.s = s; U.L = L; U.N = N; U.ds = R.d[s]; U.yr_s = R.yr[s]; U.yr_prev_rows = R.yr[s - 1] * R.d[s - 1];
@@ -791,6 +853,7 @@ static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st)
   U.canon_cols = R.canon_cols + (size_t)s * R.log_cap_piv;
   canon_update_kernel<<<64, 256, 0, st>>>(U);
   launch_gemm(R.dY, 1, R.yr[s - 1] * R.d[s - 1], R.rmax[s - 1], 1, false, dummy, nullptr, nullptr, st);
+  R.P->end(4 + (tm > 0 ? 1 : 0));
 }
 
 }  // namespace
@@ -911,6 +974,11 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
     tt_destroy(ygen);
   };
 
+  Prof prof;
+  prof.on = o.profile != nullptr;
+  prof.st = strm;
+  R.P = &prof;
+
   // ---- initial state
   cudaMemsetAsync(R.rk, 0, sizeof(int) * (L + 1), strm);
   {
@@ -929,14 +997,18 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
 
   // ---- a0: CI-canonicalise y_init, right-to-left
   for (int s = L - 1; s >= 1; --s) canon_step(R, tol, o.tol_mode, s, strm);
+  prof.begin(ACI_PROF_CANON);
   copy_prev_kernel<<<1, 64, 0, strm>>>(R.rk, R.prev, L);
+  prof.end(1);
 
   // ---- main loop
   int it = 0, converged = 0, slot = 0;
   for (it = 1; it <= max_sweeps; ++it) {
     for (int b = 0; b < L - 1; ++b) bond_update(R, I.op, tol, o.tol_mode, b, 0, slot++, strm);
     for (int b = L - 2; b >= 0; --b) bond_update(R, I.op, tol, o.tol_mode, b, 1, slot++, strm);
+    prof.begin(ACI_PROF_CONV);
     converge_kernel<<<1, 32, 0, strm>>>(R.rk, R.prev, L, R.maxeps, R.scale, tol, o.tol_mode, R.conv, R.err);
+    prof.end(1);
     int flag = 0;
     cudaMemcpyAsync(&flag, R.conv, sizeof(int), cudaMemcpyDeviceToHost, strm);
     cudaError_t e = cudaStreamSynchronize(strm);
@@ -983,7 +1055,9 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
       cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       smem_set = smem;
     }
+    prof.begin(ACI_PROF_TRSM);
     trsm_kernel<<<dim3((nmx + 31) / 32, L - 1), 256, smem, strm>>>(R.dtrsm, R.rk);
+    prof.end(1);
     e = cudaStreamSynchronize(strm);
     if (e != cudaSuccess) {
       tt_destroy(res);
@@ -1054,6 +1128,8 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   if (e != cudaSuccess) { tt_destroy(res); return fail(ACI_ERR_CUDA, std::string("aci: ") + cudaGetErrorString(e)); }
   auto t_end = std::chrono::steady_clock::now();
   rp.ms = std::chrono::duration<float, std::milli>(t_end - t_start).count();
+  rp.n_launches = prof.total;
+  if (o.profile) prof.collect(o.profile);
   if (rep) *rep = rp;
   *out = res;
   return converged ? ACI_OK : ACI_NOT_CONVERGED;

@@ -45,9 +45,9 @@ struct LuArgs {
   // grid tier exchange
   double *colpub;             // 2 x G x colcap
   int colcap;
-  double *keyval;             // 2 x G   candidate values
-  int *keyidx;                // 2 x G x 2 candidate (row, col)
+  unsigned *keys;             // 2 x G x 4: published candidate keys (hi, lo, id, pad)
   unsigned int *counter;      // zeroed before launch
+  long long *dbg;             // development timing (ACI_PRRLU_TIMING builds only)
 };
 
 // ---- launchers (defined in gemm.cu / prrlu.cu / sweep.cu) ----

@@ -1,0 +1,70 @@
+// Standalone prrLU microbenchmark with per-phase cycle counts (development tool).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/prrlu_bench tools/prrlu_bench.cu
+#define ACI_PRRLU_TIMING 1
+#include "../paper_2604_00037_b200/csrc/prrlu.cu"
+
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+int main(int argc, char **argv) {
+  int sizes[][3] = {{64, 64, 64}, {128, 128, 128}, {256, 256, 256}, {512, 512, 512}, {1024, 1024, 512}};
+  double *dM, *dU, *dcol, *deps;
+  int *drows, *dcols, *dr;
+  unsigned *dkeys, *dctr;
+  LuDims *ddims;
+  unsigned long long *dscale;
+  long long *ddbg;
+  cudaMalloc(&dM, sizeof(double) * 1024 * 1024);
+  cudaMalloc(&dU, sizeof(double) * 1024 * 1024);
+  cudaMalloc(&dcol, sizeof(double) * 2 * 148 * 1024);
+  cudaMalloc(&deps, 8);
+  cudaMalloc(&drows, 4 * 1024);
+  cudaMalloc(&dcols, 4 * 1024);
+  cudaMalloc(&dr, 4);
+  cudaMalloc(&dkeys, 16 * 2 * 148);
+  cudaMalloc(&dctr, 4);
+  cudaMalloc(&ddims, sizeof(LuDims));
+  cudaMalloc(&dscale, 8);
+  cudaMalloc(&ddbg, 64);
+  std::mt19937_64 rng(1);
+  std::normal_distribution<double> nd;
+  std::vector<double> h(1024 * 1024);
+  for (auto &x : h) x = nd(rng);
+  cudaMemcpy(dM, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int only = argc > 1 ? atoi(argv[1]) : -1;
+  for (auto &sz : sizes) {
+    int m = sz[0], n = sz[1], kmax = sz[2];
+    if (only > 0 && m != only) continue;
+    LuDims D{m, n, n, kmax, n};
+    cudaMemcpy(ddims, &D, sizeof(D), cudaMemcpyHostToDevice);
+    LuArgs a = {};
+    a.M = dM; a.dims = ddims; a.tol = 0.0; a.thr_mode = 2; a.scale_bits = dscale;
+    a.rows = drows; a.cols = dcols; a.r_out = dr; a.eps_out = deps; a.U = dU;
+    a.colpub = dcol; a.colcap = 1024; a.keys = dkeys; a.counter = dctr; a.dbg = ddbg;
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaMemset(ddbg, 0, 64);
+      cudaEventRecord(e0);
+      launch_prrlu(a, m, n, 0);
+      cudaEventRecord(e1);
+      cudaError_t err = cudaEventSynchronize(e1);
+      if (err != cudaSuccess) { printf("error %s\n", cudaGetErrorString(err)); return 1; }
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      int r;
+      long long dbg[8];
+      cudaMemcpy(&r, dr, 4, cudaMemcpyDeviceToHost);
+      cudaMemcpy(dbg, ddbg, 64, cudaMemcpyDeviceToHost);
+      if (rep == 2) {
+        printf("%4dx%4d r=%4d: %8.1f us total, %6.3f us/pivot | cycles/pivot:", m, n, r, ms * 1e3, ms * 1e3 / r);
+        for (int t = 0; t < 7; ++t) printf(" p%d=%lld", t, dbg[t] / (r > 0 ? r : 1));
+        printf("\n");
+      }
+    }
+  }
+  return 0;
+}

@@ -24,7 +24,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [NVCC] + FLAGS + ["-o", LIB] + SRC + ["-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
-            raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+            if os.path.exists(LIB):
+                os.remove(LIB)  # never leave a stale library behind a failed build
+            errs = "\n".join(l for l in (r.stdout + r.stderr).splitlines() if "error" in l.lower())
+            raise RuntimeError("nvcc failed:\n" + errs)
         with open(os.path.join(HERE, "ptxas.log"), "w") as f:
             f.write(r.stderr)
         if verbose:

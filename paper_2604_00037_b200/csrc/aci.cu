@@ -433,44 +433,58 @@ __global__ void canon_update_kernel(CanonUpd U) {
 }
 
 // ---- output cores (a8): Y_{b+1} = U_J^{-1} U (Alg. 3 right branch, R5)
-// One CTA (256 threads) per (bond, 32-column block); B[:, block] lives in shared memory during
-// the unit-upper back substitution B_k = U_k - sum_{i>k} U_k[q_i] B_i.
+// Step 1 gathers the unit-upper pivot block U_J[k][i] = U[k][q_i] densely (one launch, all
+// bonds). Step 2: one CTA per (bond, 32-column block) keeps B[:, block] in shared memory and runs
+// the back substitution B_k = U_k - sum_{i>k} U_J[k][i] B_i; each column's dot product is split
+// over 8 lanes of one warp and reduced with shuffles, so a row costs one __syncthreads.
 struct TrsmArgs {
   const double *U;  // U store of bond b (r x n), ld ldu
   int ldu;
   const int *cols;  // pivot columns q_0..q_{r-1}
   int b, d1;        // bond, d_{b+1}
+  double *UJ;       // dense r x r gather of U_J, ld ldj
+  int ldj;
   double *out;      // output core b+1, r x n row-major
 };
 
-__global__ void __launch_bounds__(256) trsm_kernel(const TrsmArgs *args, const int *rk) {
-  extern __shared__ double sB[];  // r x 32
-  __shared__ double spart[8][32];
+__global__ void gather_uj_kernel(const TrsmArgs *args, const int *rk) {
   const TrsmArgs A = args[blockIdx.y];
-  const int b = A.b;
-  const int r = rk[b + 1], n = A.d1 * rk[b + 2];
-  const int j0 = blockIdx.x * 32;
-  if (j0 >= n) return;
-  const int jj = threadIdx.x & 31, part = threadIdx.x >> 5;
-  const int j = j0 + jj;
-  for (int k = r - 1; k >= 0; --k) {
-    const double *Uk = A.U + (size_t)k * A.ldu;
-    double acc = 0.0;
-    for (int i = k + 1 + part; i < r; i += 8) acc = fma(Uk[A.cols[i]], sB[i * 32 + jj], acc);
-    spart[part][jj] = acc;
-    __syncthreads();
-    if (part == 0) {
-      double tot = 0.0;
-#pragma unroll
-      for (int p = 0; p < 8; ++p) tot += spart[p][jj];
-      sB[k * 32 + jj] = j < n ? Uk[j] - tot : 0.0;
-    }
-    __syncthreads();
+  const int r = rk[A.b + 1];
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < r * r; t += gridDim.x * blockDim.x) {
+    const int k = t / r, i = t % r;
+    A.UJ[(size_t)k * A.ldj + i] = A.U[(size_t)k * A.ldu + A.cols[i]];
   }
-  for (int t = threadIdx.x; t < r * 32; t += blockDim.x) {
-    const int k = t / 32, c = t % 32;
-    if (j0 + c < n) A.out[(size_t)k * n + j0 + c] = sB[t];
+}
+
+// Unit-upper solve of one diagonal block: x = U_J[R,R]^{-1} x for the rows R = [r0, r0 + nr) of
+// every column of the bond (x already holds U[R] - U_J[R, below] B[below]). One thread per column.
+struct TriArgs {
+  const double *UJ;
+  int ldj;
+  double *out;  // output core (r x n), rows R updated in place
+  int n, r0, nr;
+};
+__global__ void __launch_bounds__(64) tri_block_kernel(const TriArgs *args) {
+  extern __shared__ double tri_smem[];
+  double(*su)[65] = reinterpret_cast<double(*)[65]>(tri_smem);
+  double(*sx)[65] = reinterpret_cast<double(*)[65]>(tri_smem + 64 * 65);
+  const TriArgs A = args[blockIdx.y];
+  const int j = blockIdx.x * 64 + threadIdx.x;
+  if (blockIdx.x * 64 >= A.n) return;
+  for (int t = threadIdx.x; t < A.nr * A.nr; t += 64) {
+    const int k = t / A.nr, i = t % A.nr;
+    su[k][i] = A.UJ[(size_t)(A.r0 + k) * A.ldj + A.r0 + i];
   }
+  if (j < A.n)
+    for (int k = 0; k < A.nr; ++k) sx[k][threadIdx.x] = A.out[(size_t)(A.r0 + k) * A.n + j];
+  __syncthreads();
+  if (j >= A.n) return;
+  for (int k = A.nr - 1; k >= 0; --k) {
+    double acc = sx[k][threadIdx.x];
+    for (int i = k + 1; i < A.nr; ++i) acc = fma(-su[k][i], sx[i][threadIdx.x], acc);
+    sx[k][threadIdx.x] = acc;
+  }
+  for (int k = 0; k < A.nr; ++k) A.out[(size_t)(A.r0 + k) * A.n + j] = sx[k][threadIdx.x];
 }
 
 __global__ void copy_prev_kernel(const int *rk, int *prev, int L) {
@@ -566,6 +580,9 @@ struct Run {
   unsigned *keys = nullptr;
   unsigned *counter = nullptr;
   TrsmArgs *dtrsm = nullptr;
+  GemmDesc *dtgemm = nullptr;
+  struct TriArgs *dtri = nullptr;
+  std::vector<double *> UJ;
 };
 
 static long long capped_prod(const std::vector<int> &d, int lo, int hi) {  // prod d[lo..hi], capped
@@ -659,6 +676,14 @@ static size_t carve(Run &R, char *base) {
   R.keys = c.take<unsigned>(2 * 148 * 4);
   R.counter = c.take<unsigned>(1);
   R.dtrsm = c.take<TrsmArgs>(L);
+  R.UJ.assign(L, nullptr);
+  size_t nblk = 0;
+  for (int b = 0; b < L - 1; ++b) {
+    R.UJ[b] = c.take<double>((size_t)R.rmax[b] * R.rmax[b]);
+    nblk += (R.rmax[b] + 63) / 64;
+  }
+  R.dtgemm = c.take<GemmDesc>(nblk);
+  R.dtri = c.take<TriArgs>(nblk);
   return c.off + 256;
 }
 
@@ -1040,24 +1065,59 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   }
   cudaMemcpyAsync(res->dcores, R.Y0, sizeof(double) * (res->off[1] - res->off[0]), cudaMemcpyDeviceToDevice, strm);
   {
+    // Blocked back substitution B = U_J^{-1} U (64-row blocks from the bottom): per step one
+    // batched DMMA GEMM B[R] = U[R] - U_J[R, below] B[below] over all bonds, then the diagonal
+    // block solve. The final ranks are known on the host here, so descriptors are built here.
+    constexpr int NB = 64;
     std::vector<TrsmArgs> ta(L - 1);
-    int rmx = 1, nmx = 1;
+    int nmx = 1, nsteps = 0;
     for (int b = 0; b < L - 1; ++b) {
       ta[b].U = R.Ust[b]; ta[b].ldu = R.nmax[b]; ta[b].cols = R.pcol[b]; ta[b].b = b; ta[b].d1 = R.d[b + 1];
+      ta[b].UJ = R.UJ[b]; ta[b].ldj = R.rmax[b];
       ta[b].out = res->dcores + res->off[b + 1];
-      rmx = std::max(rmx, rk[b + 1]);
       nmx = std::max(nmx, R.d[b + 1] * rk[b + 2]);
+      nsteps = std::max(nsteps, (rk[b + 1] + NB - 1) / NB);
     }
+    std::vector<GemmDesc> gd;
+    std::vector<TriArgs> tr;
+    std::vector<int> gcount(nsteps, 0), tcount(nsteps, 0);
+    for (int s = 0; s < nsteps; ++s) {
+      for (int b = 0; b < L - 1; ++b) {
+        const int r = rk[b + 1], n = R.d[b + 1] * rk[b + 2];
+        const int nbk = (r + NB - 1) / NB;
+        const int blk = nbk - 1 - s;
+        if (blk < 0) continue;
+        const int r0 = blk * NB, nr = std::min(NB, r - r0), below = r0 + nr;
+        GemmDesc g = {};
+        g.C = ta[b].out + (size_t)r0 * n; g.M = nr; g.N = n; g.ldc = n; g.nin = 1;
+        g.S = R.Ust[b] + (size_t)r0 * R.nmax[b]; g.lds = R.nmax[b];
+        g.A[0] = R.UJ[b] + (size_t)r0 * R.rmax[b] + below; g.lda[0] = R.rmax[b]; g.K[0] = r - below;
+        g.B[0] = ta[b].out + (size_t)below * n; g.ldb[0] = n;
+        gd.push_back(g);
+        gcount[s]++;
+        tr.push_back(TriArgs{R.UJ[b], R.rmax[b], ta[b].out, n, r0, nr});
+        tcount[s]++;
+      }
+    }
+    // descriptors live in the workspace tail (sized for (L-1) * ceil(rmax/NB) entries)
     cudaMemcpyAsync(R.dtrsm, ta.data(), sizeof(TrsmArgs) * (L - 1), cudaMemcpyHostToDevice, strm);
-    size_t smem = (size_t)rmx * 32 * sizeof(double);
-    static size_t smem_set = 0;
-    if (smem > 48 * 1024 && smem > smem_set) {
-      cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      smem_set = smem;
+    cudaMemcpyAsync(R.dtgemm, gd.data(), sizeof(GemmDesc) * gd.size(), cudaMemcpyHostToDevice, strm);
+    cudaMemcpyAsync(R.dtri, tr.data(), sizeof(TriArgs) * tr.size(), cudaMemcpyHostToDevice, strm);
+    constexpr int kTriSmem = 2 * 64 * 65 * sizeof(double);
+    static bool tri_attr = false;
+    if (!tri_attr) {
+      cudaFuncSetAttribute(tri_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTriSmem);
+      tri_attr = true;
     }
     prof.begin(ACI_PROF_TRSM);
-    trsm_kernel<<<dim3((nmx + 31) / 32, L - 1), 256, smem, strm>>>(R.dtrsm, R.rk);
-    prof.end(1);
+    gather_uj_kernel<<<dim3(64, L - 1), 256, 0, strm>>>(R.dtrsm, R.rk);
+    size_t go = 0;
+    for (int s = 0; s < nsteps; ++s) {
+      launch_gemm_sub(R.dtgemm + go, gcount[s], NB, nmx, strm);
+      tri_block_kernel<<<dim3((nmx + 63) / 64, tcount[s]), 64, kTriSmem, strm>>>(R.dtri + go);
+      go += gcount[s];
+    }
+    prof.end(1 + 2 * nsteps);
     e = cudaStreamSynchronize(strm);
     if (e != cudaSuccess) {
       tt_destroy(res);

@@ -11,6 +11,8 @@
 struct GemmDesc {
   double *C;
   int M, N, ldc;
+  const double *S;  // EPI_SUB: C = S - A B (S has leading dimension lds)
+  int lds;
   int nin;
   const double *A[ACI_GEMM_MAX_IN];
   const double *B[ACI_GEMM_MAX_IN];
@@ -53,6 +55,8 @@ struct LuArgs {
 // ---- launchers (defined in gemm.cu / prrlu.cu / sweep.cu) ----
 void launch_gemm(const GemmDesc *d_descs, int ndesc, int max_m, int max_n, int nin, bool fuse, const FOp &op,
                  unsigned long long *scale_bits, int *nonfinite, cudaStream_t st);
+// C = S - A B for every descriptor (blocked triangular solve updates).
+void launch_gemm_sub(const GemmDesc *d_descs, int ndesc, int max_m, int max_n, cudaStream_t st);
 
 // Picks the tier for a (max_m x max_n) problem; returns false if it is out of the envelope.
 bool prrlu_supported(int max_m, int max_n);

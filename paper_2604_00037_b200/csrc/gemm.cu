@@ -4,15 +4,17 @@
 // On sm_100a FP64 matrix math exists only as warp-level mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4
 // (tcgen05 has no f64 kind); see DESIGN.md §5.
 //
-// CTA tile 64x64, BK = 16, 4 warps each owning a 32x32 warp tile (4x4 DMMA tiles), 3-stage
-// cp.async pipeline. Problem sizes are read from device descriptors (live ranks); CTAs whose
+// CTA tile 64x64, BK = 16, 8 warps each owning a 32x16 warp tile (4x2 DMMA tiles), 3-stage
+// cp.async pipeline; <= 128 registers so 2-3 CTAs (16-24 warps) share an SM (DMMA needs more
+// than one warp per SMSP to cover its latency). Problem sizes are read from device descriptors (live ranks); CTAs whose
 // tile lies outside the live M x N exit immediately. In FUSE mode the per-input products never
 // reach HBM: f, the NaN check and max|Pi| run on the accumulator registers.
 #include "aci_common.cuh"
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, NT = 128;
+constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, NT = 256;
+constexpr int WN = 16, NI = WN / 8;  // warp tile 32 x 16
 constexpr int LDA_S = BK + 4;   // 20 doubles: conflict-free A-fragment loads
 constexpr int LDB_S = BN + 8;   // 72 doubles: conflict-free B-fragment loads
 
@@ -58,11 +60,11 @@ __device__ __forceinline__ void load_stage(Smem &sm, int st, const double *A, in
 }
 
 // acc += A (M x K) * B (K x N) for this CTA's 64x64 tile.
-__device__ __forceinline__ void mainloop(Smem &sm, double (&acc)[4][4][2], const double *A, int lda,
+__device__ __forceinline__ void mainloop(Smem &sm, double (&acc)[4][NI][2], const double *A, int lda,
                                          const double *B, int ldb, int M, int N, int K, int m0, int n0) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, c = lane & 3;
-  const int wm = (w >> 1) * 32, wn = (w & 1) * 32;
+  const int wm = (w >> 2) * 32, wn = (w & 3) * WN;
   const int nk = (K + BK - 1) / BK;
   __syncthreads();  // smem reuse across inputs
 #pragma unroll
@@ -81,22 +83,23 @@ __device__ __forceinline__ void mainloop(Smem &sm, double (&acc)[4][4][2], const
     const int st = kt % STAGES;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
-      double a[4], b[4];
+      double a[4], b[NI];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) a[mi] = sm.A[st][wm + mi * 8 + g][kk * 4 + c];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) b[ni] = sm.B[st][kk * 4 + c][wn + ni * 8 + g];
+      for (int ni = 0; ni < NI; ++ni) b[ni] = sm.B[st][kk * 4 + c][wn + ni * 8 + g];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+        for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
     }
   }
   cp_async_wait<0>();
 }
 
-template <int NIN, bool FUSE>
-__global__ void __launch_bounds__(NT) gemm_dmma_kernel(const GemmDesc *__restrict__ descs, FOp op,
+// EPI: 0 = store A B, 1 = f(A1 B1, ...) (FUSE), 2 = S - A B.
+template <int NIN, bool FUSE, int EPI = FUSE ? 1 : 0>
+__global__ void __launch_bounds__(NT, 2) gemm_dmma_kernel(const GemmDesc *__restrict__ descs, FOp op,
                                                        unsigned long long *scale_bits, int *nonfinite) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem &sm = *reinterpret_cast<Smem *>(smem_raw);
@@ -105,26 +108,26 @@ __global__ void __launch_bounds__(NT) gemm_dmma_kernel(const GemmDesc *__restric
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   if (m0 >= M || n0 >= N) return;
 
-  double acc[NIN][4][4][2];
+  double acc[NIN][4][NI][2];
 #pragma unroll
   for (int i = 0; i < NIN; ++i)
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) acc[i][mi][ni][0] = acc[i][mi][ni][1] = 0.0;
+      for (int ni = 0; ni < NI; ++ni) acc[i][mi][ni][0] = acc[i][mi][ni][1] = 0.0;
 
 #pragma unroll
   for (int i = 0; i < NIN; ++i) mainloop(sm, acc[i], D.A[i], D.lda[i], D.B[i], D.ldb[i], M, N, D.K[i], m0, n0);
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, c = lane & 3;
-  const int wm = (w >> 1) * 32, wn = (w & 1) * 32;
+  const int wm = (w >> 2) * 32, wn = (w & 3) * WN;
   double vmax = 0.0;
   int bad = 0;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
+    for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         int row = m0 + wm + mi * 8 + g, col = n0 + wn + ni * 8 + 2 * c + e;
@@ -142,6 +145,8 @@ __global__ void __launch_bounds__(NT) gemm_dmma_kernel(const GemmDesc *__restric
             }
             if (!isfinite(y)) bad = 1;
             vmax = fmax(vmax, fabs(y));
+          } else if (EPI == 2) {
+            y = D.S[(size_t)row * D.lds + col] - acc[0][mi][ni][e];
           } else {
             y = acc[0][mi][ni][e];
           }
@@ -175,6 +180,19 @@ void launch_t(const GemmDesc *d, int ndesc, int max_m, int max_n, const FOp &op,
 }
 
 }  // namespace
+
+void launch_gemm_sub(const GemmDesc *d, int ndesc, int max_m, int max_n, cudaStream_t st) {
+  if (max_m <= 0 || max_n <= 0 || ndesc <= 0) return;
+  static bool init = false;
+  const int smem = (int)sizeof(Smem);
+  if (!init) {
+    cudaFuncSetAttribute(gemm_dmma_kernel<1, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    init = true;
+  }
+  dim3 grid((max_n + BN - 1) / BN, (max_m + BM - 1) / BM, ndesc);
+  FOp op = {};
+  gemm_dmma_kernel<1, false, 2><<<grid, NT, smem, st>>>(d, op, nullptr, nullptr);
+}
 
 void launch_gemm(const GemmDesc *d_descs, int ndesc, int max_m, int max_n, int nin, bool fuse, const FOp &op,
                  unsigned long long *scale_bits, int *nonfinite, cudaStream_t st) {

@@ -396,6 +396,41 @@ def tt_round(cores, tol: float) -> list:
     return cores
 
 
+def tt_axpby(alpha, a, beta, b) -> list:
+    """alpha*a + beta*b as a TT (block-diagonal sum, rank r_a + r_b)."""
+    a, b = _cores_of(a), _cores_of(b)
+    L = len(a)
+    out = []
+    for s in range(L):
+        x, y = a[s], b[s]
+        if s == 0:
+            x, y = alpha * x, beta * y
+        if L == 1:
+            out.append(x + y)
+        elif s == 0:
+            out.append(np.concatenate([x, y], axis=2))
+        elif s == L - 1:
+            out.append(np.concatenate([x, y], axis=0))
+        else:
+            c = np.zeros((x.shape[0] + y.shape[0], x.shape[1], x.shape[2] + y.shape[2]))
+            c[:x.shape[0], :, :x.shape[2]] = x
+            c[x.shape[0]:, :, x.shape[2]:] = y
+            out.append(c)
+    return out
+
+
+def tt_norm(cores) -> float:
+    """Frobenius norm by left-orthogonalisation (QR sweep): no cancellation, accurate even when
+    the TT is a small difference of two large ones."""
+    cores = [np.array(c, dtype=np.float64) for c in _cores_of(cores)]
+    R = np.ones((1, 1))
+    for c in cores:
+        c = np.einsum("ab,bsc->asc", R, c)
+        r0, d, r1 = c.shape
+        _, R = np.linalg.qr(c.reshape(r0 * d, r1))
+    return float(np.linalg.norm(R))
+
+
 def tt_inner(a, b) -> float:
     """<a, b> = sum_sigma a_sigma b_sigma, by transfer matrices."""
     a, b = _cores_of(a), _cores_of(b)

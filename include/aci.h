@@ -103,6 +103,8 @@ typedef struct {
   double flops_init;         /* canonicalisation GEMMs */
   float ms;                  /* host wall time of the call (includes the final sync) */
   int64_t n_launches;        /* kernels this call launched */
+  int graph_iterations;      /* iterations replayed from one captured CUDA graph (0 = direct launches) */
+  float ms_graph_setup;      /* host time spent capturing + instantiating that graph */
 } aci_report;
 
 /* Optional per-kernel-class device timing (CUDA events around each launch on the call's

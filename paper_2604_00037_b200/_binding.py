@@ -39,7 +39,7 @@ class aci_report(C.Structure):
                 ("converged", C.c_int), ("max_rank", C.c_int), ("n_updates", C.c_int),
                 ("pivot_steps", C.c_int64), ("flops_contraction", C.c_double), ("flops_prrlu", C.c_double),
                 ("flops_trsm", C.c_double), ("flops_init", C.c_double), ("ms", C.c_float),
-                ("n_launches", C.c_int64)]
+                ("n_launches", C.c_int64), ("graph_iterations", C.c_int), ("ms_graph_setup", C.c_float)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

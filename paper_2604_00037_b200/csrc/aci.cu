@@ -40,6 +40,13 @@ struct tt_s {
   size_t total = 0;
 };
 
+// The library's own stream (per host thread), used when the caller passes NULL.
+static cudaStream_t lib_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  if (!s) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  return s;
+}
+
 static int check_device() {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
@@ -261,9 +268,13 @@ struct UpdateArgs {
   double *Y0;                 // d_0 x rmax[0], ld = r
   unsigned long long *maxeps_bits;
   const unsigned long long *scale_bits;
-  int *log_info;              // 5 ints
-  double *log_es;             // 2 doubles
-  int *log_rows, *log_cols;   // capacity maxrank
+  // per-update log (slot = iteration * per_iter + step; the iteration counter lives on the
+  // device so one captured CUDA graph serves every iteration)
+  int *log_info;              // 5 ints per slot
+  double *log_es;             // 2 doubles per slot
+  int *log_rows, *log_cols;   // cap_piv per slot
+  const int *iter;
+  int step, per_iter, cap_piv;
 };
 
 // Index-set update (a6, R21) and frame update (a7: the rows/columns of A^n / B^n the
@@ -274,17 +285,19 @@ __global__ void update_bond_kernel(UpdateArgs U) {
   const int rl = U.rk[b], rr = U.rk[b + 2];
   const int n = U.db1 * rr;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  const size_t slot = (size_t)(*U.iter) * U.per_iter + U.step;
   if (gt == 0) {
     U.rk[b + 1] = r;  // no thread of this kernel reads rk[b+1]
     const double eps = *U.eps_in;
     atomicMax(U.maxeps_bits, (unsigned long long)__double_as_longlong(eps));
-    U.log_info[0] = b; U.log_info[1] = U.dir; U.log_info[2] = rl; U.log_info[3] = rr; U.log_info[4] = r;
-    U.log_es[0] = eps;
-    U.log_es[1] = __longlong_as_double((long long)*U.scale_bits);
+    int *li = U.log_info + slot * 5;
+    li[0] = b; li[1] = U.dir; li[2] = rl; li[3] = rr; li[4] = r;
+    U.log_es[slot * 2] = eps;
+    U.log_es[slot * 2 + 1] = __longlong_as_double((long long)*U.scale_bits);
   }
   for (int k = gt; k < r; k += gs) {
-    U.log_rows[k] = U.rows[k];
-    U.log_cols[k] = U.cols[k];
+    U.log_rows[slot * U.cap_piv + k] = U.rows[k];
+    U.log_cols[slot * U.cap_piv + k] = U.cols[k];
   }
   // multi-indices: I_b[k] = (I_{b-1}[row / d_b], row % d_b); J_{b+1}[k] = (col / rr, J_{b+2}[col % rr])
   for (int t = gt; t < r * (b + 1); t += gs) {
@@ -330,8 +343,9 @@ __global__ void update_bond_kernel(UpdateArgs U) {
 // Convergence test after a full iteration (R10).
 __global__ void converge_kernel(int *rk, int *prev, int L, unsigned long long *maxeps_bits,
                                 const unsigned long long *scale_bits, double tol, int tol_mode, int *flag,
-                                double *err_out) {
+                                double *err_out, int *iter) {
   if (threadIdx.x != 0) return;
+  *iter += 1;
   int grew = 0;
   for (int b = 0; b < L - 1; ++b) {
     if (rk[b + 1] > prev[b]) grew = 1;
@@ -512,6 +526,7 @@ struct Prof {
   cudaStream_t st = nullptr;
   int64_t launches[ACI_PROF_NCLASS] = {};
   int64_t total = 0;
+  int64_t per_iter_launches = 0;
   struct Span { int cls; cudaEvent_t a, b; };
   std::vector<Span> spans;
   std::vector<cudaEvent_t> pool;
@@ -564,7 +579,7 @@ struct Run {
   std::vector<std::vector<size_t>> xoff; // [n][s]
   std::vector<int> rmax, mmax, nmax;     // per bond
   // device
-  int *rk = nullptr, *prev = nullptr, *rout = nullptr, *nonfinite = nullptr, *conv = nullptr;
+  int *rk = nullptr, *prev = nullptr, *rout = nullptr, *nonfinite = nullptr, *conv = nullptr, *iter = nullptr;
   double *epsb = nullptr, *err = nullptr;
   unsigned long long *scale = nullptr, *maxeps = nullptr;
   std::vector<int *> prow, pcol;
@@ -576,8 +591,9 @@ struct Run {
   LuDims *dLu = nullptr;
   int *log_info = nullptr, *log_rows = nullptr, *log_cols = nullptr, *canon_n = nullptr, *canon_cols = nullptr;
   double *log_es = nullptr;
-  double *colpub = nullptr;
-  unsigned *keys = nullptr;
+  unsigned long long *colpub = nullptr;
+  unsigned long long *keys = nullptr;
+  unsigned *epoch = nullptr;
   unsigned *counter = nullptr;
   TrsmArgs *dtrsm = nullptr;
   GemmDesc *dtgemm = nullptr;
@@ -616,6 +632,7 @@ static size_t carve(Run &R, char *base) {
   R.rout = c.take<int>(L);
   R.nonfinite = c.take<int>(1);
   R.conv = c.take<int>(1);
+  R.iter = c.take<int>(1);
   R.epsb = c.take<double>(L);
   R.err = c.take<double>(1);
   R.scale = c.take<unsigned long long>(1);
@@ -672,8 +689,9 @@ static size_t carve(Run &R, char *base) {
   R.log_cols = c.take<int>((size_t)R.log_cap_upd * R.log_cap_piv);
   R.canon_n = c.take<int>(L + 1);
   R.canon_cols = c.take<int>((size_t)(L + 1) * R.log_cap_piv);
-  R.colpub = c.take<double>((size_t)2 * 148 * R.colcap);
-  R.keys = c.take<unsigned>(2 * 148 * 4);
+  R.colpub = c.take<unsigned long long>((size_t)2 * 148 * R.colcap * 2);
+  R.keys = c.take<unsigned long long>(2 * 148 * 4);
+  R.epoch = c.take<unsigned>(1);
   R.counter = c.take<unsigned>(1);
   R.dtrsm = c.take<TrsmArgs>(L);
   R.UJ.assign(L, nullptr);
@@ -771,10 +789,14 @@ static void launch_update(Run &R, int b, int dir, int logslot, cudaStream_t st) 
   U.Y0 = R.Y0;
   U.maxeps_bits = R.maxeps;
   U.scale_bits = R.scale;
-  U.log_info = R.log_info + (size_t)logslot * 5;
-  U.log_es = R.log_es + (size_t)logslot * 2;
-  U.log_rows = R.log_rows + (size_t)logslot * R.log_cap_piv;
-  U.log_cols = R.log_cols + (size_t)logslot * R.log_cap_piv;
+  U.log_info = R.log_info;
+  U.log_es = R.log_es;
+  U.log_rows = R.log_rows;
+  U.log_cols = R.log_cols;
+  U.iter = R.iter;
+  U.step = logslot;
+  U.per_iter = 2 * (R.L - 1);
+  U.cap_piv = R.log_cap_piv;
   size_t work = (size_t)R.rmax[b] * 256;
   int blocks = (int)std::min<size_t>(592, std::max<size_t>(1, (work + 255) / 256));
   update_bond_kernel<<<blocks, 256, 0, st>>>(U);
@@ -818,7 +840,7 @@ static void bond_update(Run &R, const FOp &op, double tol, int tol_mode, int b, 
   a.scale_bits = R.scale;
   a.rows = R.prow[b]; a.cols = R.pcol[b]; a.r_out = R.rout + b; a.eps_out = R.epsb + b;
   a.U = dir == 1 ? R.Ust[b] : nullptr;
-  a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter;
+  a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter; a.epoch = R.epoch;
   R.P->begin(ACI_PROF_PRRLU);
   launch_prrlu(a, R.mmax[b], R.nmax[b], st);
   R.P->end(1);
@@ -855,7 +877,7 @@ static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st)
   a.scale_bits = R.scale;
   a.rows = R.prow[s - 1]; a.cols = R.pcol[s - 1]; a.r_out = R.rout + (s - 1); a.eps_out = R.epsb + (s - 1);
   a.U = nullptr;
-  a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter;
+  a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter; a.epoch = R.epoch;
   launch_prrlu(a, max_m, max_n, st);
   CanonUpd U = {};
   U.s = s; U.L = L; U.N = N; U.ds = R.d[s]; U.yr_s = R.yr[s]; U.yr_prev_rows = R.yr[s - 1] * R.d[s - 1];
@@ -939,7 +961,8 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   const tt_s *t0 = I.tts[0];
   const int L = t0->L;
   if (L < 2) return fail(ACI_ERR_INVALID, "aci: L must be >= 2 (the 2-site update needs two sites)");
-  cudaStream_t strm = (cudaStream_t)o.stream;
+  cudaStream_t strm = o.stream ? (cudaStream_t)o.stream : lib_stream();
+  gemm_init();
 
   // ---- y_init (R9)
   tt_s *ygen = nullptr;
@@ -1016,6 +1039,11 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   cudaMemsetAsync(R.scale, 0, sizeof(unsigned long long), strm);
   cudaMemsetAsync(R.maxeps, 0, sizeof(unsigned long long), strm);
   cudaMemsetAsync(R.nonfinite, 0, sizeof(int), strm);
+  cudaMemsetAsync(R.iter, 0, sizeof(int), strm);
+  // tags in the exchange buffers must never match stale data: clear them once per call
+  cudaMemsetAsync(R.keys, 0, sizeof(unsigned long long) * 2 * 148 * 4, strm);
+  cudaMemsetAsync(R.colpub, 0, sizeof(unsigned long long) * 2 * 148 * R.colcap * 2, strm);
+  cudaMemsetAsync(R.epoch, 0, sizeof(unsigned), strm);
   for (int s = 0; s < L; ++s)
     cudaMemcpyAsync(R.Yin[s], y->dcores + y->off[s], sizeof(double) * (y->off[s + 1] - y->off[s]),
                     cudaMemcpyDeviceToDevice, strm);
@@ -1026,21 +1054,58 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   copy_prev_kernel<<<1, 64, 0, strm>>>(R.rk, R.prev, L);
   prof.end(1);
 
-  // ---- main loop
-  int it = 0, converged = 0, slot = 0;
-  for (it = 1; it <= max_sweeps; ++it) {
-    for (int b = 0; b < L - 1; ++b) bond_update(R, I.op, tol, o.tol_mode, b, 0, slot++, strm);
-    for (int b = L - 2; b >= 0; --b) bond_update(R, I.op, tol, o.tol_mode, b, 1, slot++, strm);
+  // ---- main loop. One iteration (L->R and R->L half-sweeps + convergence test)
+  // is a fixed sequence of launches whose live sizes are read on the device, so it is captured
+  // once as a CUDA graph and replayed; only the convergence flag comes back to the host.
+  auto one_iteration = [&]() {
+    int step = 0;
+    for (int b = 0; b < L - 1; ++b) bond_update(R, I.op, tol, o.tol_mode, b, 0, step++, strm);
+    for (int b = L - 2; b >= 0; --b) bond_update(R, I.op, tol, o.tol_mode, b, 1, step++, strm);
     prof.begin(ACI_PROF_CONV);
-    converge_kernel<<<1, 32, 0, strm>>>(R.rk, R.prev, L, R.maxeps, R.scale, tol, o.tol_mode, R.conv, R.err);
+    converge_kernel<<<1, 32, 0, strm>>>(R.rk, R.prev, L, R.maxeps, R.scale, tol, o.tol_mode, R.conv, R.err,
+                                        R.iter);
     prof.end(1);
+  };
+  cudaGraphExec_t gexec = nullptr;
+  int graph_iters = 0;
+  auto tg0 = std::chrono::steady_clock::now();
+  if (!prof.on && strm != nullptr) {
+    cudaGraph_t graph = nullptr;
+    const int64_t before = prof.total;
+    if (cudaStreamBeginCapture(strm, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      one_iteration();
+      if (cudaStreamEndCapture(strm, &graph) != cudaSuccess || !graph ||
+          cudaGraphInstantiate(&gexec, graph, 0) != cudaSuccess)
+        gexec = nullptr;
+      if (graph) cudaGraphDestroy(graph);
+    }
+    cudaGetLastError();  // a failed capture falls back to direct launches
+    prof.per_iter_launches = prof.total - before;
+    prof.total = before;
+  }
+  const float ms_graph = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - tg0).count();
+  int it = 0, converged = 0;
+  for (it = 1; it <= max_sweeps; ++it) {
+    if (gexec) {
+      cudaGraphLaunch(gexec, strm);
+      prof.total += prof.per_iter_launches;
+      ++graph_iters;
+    } else {
+      one_iteration();
+    }
     int flag = 0;
     cudaMemcpyAsync(&flag, R.conv, sizeof(int), cudaMemcpyDeviceToHost, strm);
     cudaError_t e = cudaStreamSynchronize(strm);
-    if (e != cudaSuccess) { cleanup(); return fail(ACI_ERR_CUDA, std::string("aci sweep: ") + cudaGetErrorString(e)); }
+    if (e != cudaSuccess) {
+      if (gexec) cudaGraphExecDestroy(gexec);
+      cleanup();
+      return fail(ACI_ERR_CUDA, std::string("aci sweep: ") + cudaGetErrorString(e));
+    }
     if (flag) { converged = 1; break; }
   }
   if (it > max_sweeps) it = max_sweeps;
+  if (gexec) cudaGraphExecDestroy(gexec);
+  const int slot = it * 2 * (L - 1);
 
   // ---- results: ranks, flags, log
   std::vector<int> rk(L + 1);
@@ -1189,6 +1254,8 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   auto t_end = std::chrono::steady_clock::now();
   rp.ms = std::chrono::duration<float, std::milli>(t_end - t_start).count();
   rp.n_launches = prof.total;
+  rp.graph_iterations = graph_iters;
+  rp.ms_graph_setup = ms_graph;
   if (o.profile) prof.collect(o.profile);
   if (rep) *rep = rp;
   *out = res;

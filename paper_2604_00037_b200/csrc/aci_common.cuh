@@ -44,17 +44,21 @@ struct LuArgs {
   int *r_out;                 // rank out
   double *eps_out;            // first rejected candidate (R2)
   double *U;                  // optional U rows out (r x n, ld = dims->ldu), U_k = S_k[p,:]/c
-  // grid tier exchange
-  double *colpub;             // 2 x G x colcap
+  // grid tier exchange: every published word carries a tag (epoch << 12 | step + 1) in its
+  // upper 32 bits, so readers validate data without release/acquire fences
+  unsigned long long *colpub; // 2 x G x colcap x 2 words: (tag|lo32, tag|hi32) per element
   int colcap;
-  unsigned *keys;             // 2 x G x 4: published candidate keys (hi, lo, id, pad)
+  unsigned long long *keys;   // 2 x G x 4 words: tag|hi, tag|lo, tag|id, pad
   unsigned int *counter;      // zeroed before launch
+  unsigned int *epoch;        // incremented by every grid-tier launch (tags stay unique)
   long long *dbg;             // development timing (ACI_PRRLU_TIMING builds only)
 };
 
 // ---- launchers (defined in gemm.cu / prrlu.cu / sweep.cu) ----
 void launch_gemm(const GemmDesc *d_descs, int ndesc, int max_m, int max_n, int nin, bool fuse, const FOp &op,
                  unsigned long long *scale_bits, int *nonfinite, cudaStream_t st);
+// Sets kernel attributes (dynamic shared memory) once; call before any stream capture.
+void gemm_init();
 // C = S - A B for every descriptor (blocked triangular solve updates).
 void launch_gemm_sub(const GemmDesc *d_descs, int ndesc, int max_m, int max_n, cudaStream_t st);
 

@@ -169,26 +169,30 @@ __global__ void __launch_bounds__(NT, 2) gemm_dmma_kernel(const GemmDesc *__rest
 template <int NIN, bool FUSE>
 void launch_t(const GemmDesc *d, int ndesc, int max_m, int max_n, const FOp &op, unsigned long long *sb, int *nf,
               cudaStream_t st) {
-  static bool init = false;
   const int smem = (int)sizeof(Smem);
-  if (!init) {
-    cudaFuncSetAttribute(gemm_dmma_kernel<NIN, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    init = true;
-  }
   dim3 grid((max_n + BN - 1) / BN, (max_m + BM - 1) / BM, ndesc);
   gemm_dmma_kernel<NIN, FUSE><<<grid, NT, smem, st>>>(d, op, sb, nf);
 }
 
 }  // namespace
 
+void gemm_init() {
+  // kernel attributes are set once, outside any stream capture
+  static bool done = false;
+  if (done) return;
+  const int smem = (int)sizeof(Smem);
+  cudaFuncSetAttribute(gemm_dmma_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(gemm_dmma_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(gemm_dmma_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(gemm_dmma_kernel<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(gemm_dmma_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(gemm_dmma_kernel<1, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  done = true;
+}
+
 void launch_gemm_sub(const GemmDesc *d, int ndesc, int max_m, int max_n, cudaStream_t st) {
   if (max_m <= 0 || max_n <= 0 || ndesc <= 0) return;
-  static bool init = false;
   const int smem = (int)sizeof(Smem);
-  if (!init) {
-    cudaFuncSetAttribute(gemm_dmma_kernel<1, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    init = true;
-  }
   dim3 grid((max_n + BN - 1) / BN, (max_m + BM - 1) / BM, ndesc);
   FOp op = {};
   gemm_dmma_kernel<1, false, 2><<<grid, NT, smem, st>>>(d, op, nullptr, nullptr);

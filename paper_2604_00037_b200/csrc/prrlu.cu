@@ -11,8 +11,9 @@
 //   rank-1 update, then a branch-free running (value, slot) max per thread
 //   -> warp argmax: 3 x redux.sync on the exact key (|v| bits hi, lo; flat index)
 //   -> CTA argmax: per-warp keys in smem, every warp reduces them itself
-//   -> [grid tier: the owner warp of the CTA candidate publishes key + column, arrives on a
-//       counter (red.release); one poll; every warp reduces the G published keys itself]
+//   -> [grid tier: the owner warp of the CTA candidate publishes key + column as tagged
+//       packets (each 8-byte word carries epoch|step, so no release/acquire fence is needed),
+//       arrives on a counter; one poll; every warp reads the G keys with all loads in flight]
 //   -> pivot column l = S_iq * (1/c) (R4) and pivot row u through smem.
 // The pivot's sign comes from the (published) pivot column, so keys carry only |v|.
 // Row p is zeroed exactly by l_p = 1 (fma(-1, u_j, u_j) = 0); column q by the owner warp.
@@ -46,13 +47,26 @@ constexpr unsigned BAD_ID = 0xffffffffu;
   } while (0)
 #endif
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
   unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void red_release_add(unsigned *p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void red_relaxed_add(unsigned *p, unsigned v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// 16-byte packet = two independently single-copy-atomic 8-byte words, each tagged
+__device__ __forceinline__ void st_pkt(unsigned long long *p, unsigned long long w0, unsigned long long w1) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+}
+__device__ __forceinline__ void ld_pkt(const unsigned long long *p, unsigned long long &w0, unsigned long long &w1) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+}
+__device__ __forceinline__ unsigned long long tagged(unsigned tag, unsigned v) {
+  return ((unsigned long long)tag << 32) | v;
+}
+__device__ __forceinline__ double pkt_double(unsigned long long w0, unsigned long long w1) {
+  return __longlong_as_double((long long)(((w1 & 0xffffffffull) << 32) | (w0 & 0xffffffffull)));
 }
 
 struct Key {
@@ -76,6 +90,9 @@ __device__ __forceinline__ double key_abs(const Key &k) {
   return __longlong_as_double((long long)(((unsigned long long)k.hi << 32) | k.lo));
 }
 
+#ifndef ACI_BIG_EB
+#define ACI_BIG_EB 2  // columns per warp for the 1024-row grid tier (64 CTAs for 1024 columns)
+#endif
 constexpr int kNW = 16;          // warps per CTA (512 threads) for every variant
 constexpr int kMaxRows = 1024;   // 32 * EA_max
 constexpr int kMaxCB = 512;      // NW * EB_max
@@ -85,6 +102,7 @@ struct PrrluSmem {
   double raw[kMaxRows];  // CTA tier: raw pivot column
   double u[kMaxCB];      // pivot row segment
   unsigned hi[32], lo[32], id[32];
+  unsigned win[4];  // grid winner broadcast (ACI_PRRLU_KEYPOLL)
 };
 
 // One factorisation, register tile EA x EB per thread, NW warps per CTA. GRID: G CTAs (this is
@@ -102,6 +120,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   const int c0 = g * CB;
 
   const int m = A.dims->m, n = A.dims->n, ldm = A.dims->ldm, kmax = A.dims->kmax, ldu = A.dims->ldu;
+  const unsigned ep = GRID ? (*A.epoch & 0xfffffu) : 0u;  // read by every CTA before any arrival
   const int mn = m < n ? m : n;
   double thr = A.tol;
   if (A.thr_mode == 0) thr = A.tol * __longlong_as_double((long long)*A.scale_bits);
@@ -181,40 +200,80 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     PHASE(1);
     if (GRID) {
       const int par = k & 1;
-      // the owner warp of the CTA candidate's column publishes column + key and arrives
+      const unsigned tag = (ep << 12) | (unsigned)(k + 1);
+      // the owner warp of the CTA candidate's column publishes the column (tagged packets, no
+      // fence) and lane 0 publishes the key and arrives on the counter
       const int jc = (int)(ck.id % NC) - c0;
-      const int pw = jc % NW;  // the warp that arrives for this CTA
+      const int pw = jc % NW;
       if (w == pw) {
-        {
-          const int bc = jc / NW;
-          double *dst = A.colpub + ((size_t)par * G + g) * A.colcap;
+        const int bc = jc / NW;
+        unsigned long long *dst = A.colpub + (((size_t)par * G + g) * A.colcap) * 2;
 #pragma unroll
-          for (int b = 0; b < EB; ++b)
-            if (b == bc)
+        for (int b = 0; b < EB; ++b)
+          if (b == bc)
 #pragma unroll
-              for (int a = 0; a < EA; ++a)
-                if (rok[a]) __stcg(dst + lane + 32 * a, v[a][b]);
-        }
-        __syncwarp();
+            for (int a = 0; a < EA; ++a)
+              if (rok[a]) {
+                const unsigned long long bits = (unsigned long long)__double_as_longlong(v[a][b]);
+                st_pkt(dst + 2 * (lane + 32 * a), tagged(tag, (unsigned)bits), tagged(tag, (unsigned)(bits >> 32)));
+              }
         if (lane == 0) {
-          __stcg(reinterpret_cast<uint4 *>(A.keys) + par * G + g, make_uint4(ck.hi, ck.lo, ck.id, 0u));
-          red_release_add(A.counter, 1u);
-          const unsigned target = (unsigned)(k + 1) * (unsigned)G;
-          while (ld_acquire_u32(A.counter) < target) {
-          }
+          unsigned long long *kd = A.keys + ((size_t)par * G + g) * 4;
+          st_pkt(kd, tagged(tag, ck.hi), tagged(tag, ck.lo));
+          st_pkt(kd + 2, tagged(tag, ck.id), 0ull);
+          red_relaxed_add(A.counter, 1u);
         }
       }
       PHASE(2);
-      __syncthreads();  // S2: counter passed
+#ifndef ACI_PRRLU_KEYPOLL
+      if (tid == 0) {
+        const unsigned target = (unsigned)(k + 1) * (unsigned)G;
+        while (ld_relaxed_u32(A.counter) < target) {
+        }
+      }
+      __syncthreads();  // S2: every CTA has arrived
+#endif
       PHASE(3);
+      // read all G keys: independent loads in flight, stale packets re-read until their tag is
+      // this step's (with ACI_PRRLU_KEYPOLL only warp 0 does this and the tags are the barrier)
+      constexpr int KPL = (148 + 31) / 32;  // keys per lane
       Key gk{0u, 0u, BAD_ID};
-      const uint4 *keys = reinterpret_cast<const uint4 *>(A.keys) + par * G;
-      for (int t = lane; t < G; t += 32) {
-        const uint4 qk = __ldcg(keys + t);
-        const Key kq{qk.x, qk.y, qk.z};
-        if (better(kq, gk)) gk = kq;
+#ifdef ACI_PRRLU_KEYPOLL
+      if (w == 0) {
+#else
+      {
+#endif
+        unsigned long long kw[KPL][4];
+#pragma unroll
+        for (int t = 0; t < KPL; ++t) {
+          const int s_ = lane + 32 * t;
+          if (s_ < G) {
+            const unsigned long long *kp = A.keys + ((size_t)par * G + s_) * 4;
+            ld_pkt(kp, kw[t][0], kw[t][1]);
+            ld_pkt(kp + 2, kw[t][2], kw[t][3]);
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < KPL; ++t) {
+          const int s_ = lane + 32 * t;
+          if (s_ < G) {
+            const unsigned long long *kp = A.keys + ((size_t)par * G + s_) * 4;
+            while ((unsigned)(kw[t][0] >> 32) != tag || (unsigned)(kw[t][1] >> 32) != tag ||
+                   (unsigned)(kw[t][2] >> 32) != tag) {
+              ld_pkt(kp, kw[t][0], kw[t][1]);
+              ld_pkt(kp + 2, kw[t][2], kw[t][3]);
+            }
+            const Key kq{(unsigned)kw[t][0], (unsigned)kw[t][1], (unsigned)kw[t][2]};
+            if (better(kq, gk)) gk = kq;
+          }
+        }
       }
       win = warp_argmax(gk);
+#ifdef ACI_PRRLU_KEYPOLL
+      if (tid == 0) { S.win[0] = win.hi; S.win[1] = win.lo; S.win[2] = win.id; }
+      __syncthreads();  // S2: the winner, known only after every CTA's key arrived
+      win = Key{S.win[0], S.win[1], S.win[2]};
+#endif
       PHASE(4);
     }
 
@@ -248,10 +307,28 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     }
     double inv;
     if (GRID) {
-      const double *src = A.colpub + ((size_t)(k & 1) * G + q / CB) * A.colcap;
-      inv = 1.0 / __ldcg(src + p);
-#pragma unroll 4
-      for (int i = tid; i < m; i += T) s_l[i] = (i == p) ? 1.0 : __ldcg(src + i) * inv;
+      const unsigned tag = (ep << 12) | (unsigned)(k + 1);
+      const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2;
+      constexpr int PPT = (MROWS + T - 1) / T;  // column packets per thread
+      unsigned long long cw[PPT + 1][2];
+#pragma unroll
+      for (int t = 0; t < PPT; ++t) {
+        const int i = tid + T * t;
+        if (i < m) ld_pkt(src + 2 * i, cw[t][0], cw[t][1]);
+      }
+      ld_pkt(src + 2 * p, cw[PPT][0], cw[PPT][1]);
+      while ((unsigned)(cw[PPT][0] >> 32) != tag || (unsigned)(cw[PPT][1] >> 32) != tag)
+        ld_pkt(src + 2 * p, cw[PPT][0], cw[PPT][1]);
+      inv = 1.0 / pkt_double(cw[PPT][0], cw[PPT][1]);
+#pragma unroll
+      for (int t = 0; t < PPT; ++t) {
+        const int i = tid + T * t;
+        if (i < m) {
+          while ((unsigned)(cw[t][0] >> 32) != tag || (unsigned)(cw[t][1] >> 32) != tag)
+            ld_pkt(src + 2 * i, cw[t][0], cw[t][1]);
+          s_l[i] = (i == p) ? 1.0 : pkt_double(cw[t][0], cw[t][1]) * inv;
+        }
+      }
     } else {
       const int jq = q - c0;
       if ((jq % NW) == w) {
@@ -304,6 +381,9 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   if (g == 0 && tid == 0) {
     *A.r_out = k;
     *A.eps_out = eps;
+    // every CTA read the epoch before its first arrival, and CTA 0 only gets here after the
+    // last exchange, so the increment cannot race with a reader of this launch
+    if (GRID) atomicAdd(A.epoch, 1u);
 #ifdef ACI_PRRLU_TIMING
     for (int t = 0; t < 8; ++t) A.dbg[t] = ph_[t];
 #endif
@@ -311,74 +391,103 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
 }
 
 // Runtime tier selection from the LIVE sizes (device-resident ranks): the launch is sized for
-// the static capacity, and CTAs beyond what the live block needs exit immediately.
-__global__ void __launch_bounds__(kNW * 32) prrlu_kernel(LuArgs A) {
+// the static capacity, and CTAs beyond what the live block needs exit immediately. Two
+// instantiations: 16 warps (static rows <= 512) and 8 warps (static rows <= 1024: 8 columns per
+// CTA and up to 255 registers, so the 32-row-slot tiles do not spill).
+template <int NWT>
+__global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
   __shared__ PrrluSmem S;
   const int m = A.dims->m, n = A.dims->n;
   const int g = blockIdx.x;
 #define ACI_CTA_VARIANT(EA, EB)                                        \
-  if (m <= 32 * (EA) && n <= kNW * (EB)) {                              \
-    if (g == 0) prrlu_body<(EA), (EB), kNW, false>(A, S, 1, 0);        \
+  if (m <= 32 * (EA) && n <= NWT * (EB)) {                              \
+    if (g == 0) prrlu_body<(EA), (EB), NWT, false>(A, S, 1, 0);        \
     return;                                                            \
   }
-#define ACI_GRID_VARIANT(EA)                                           \
+#define ACI_GRID_VARIANT(EA) ACI_GRID_VARIANT2(EA, 1)
+#define ACI_GRID_VARIANT2(EA, EB)                                      \
   if (m <= 32 * (EA)) {                                                \
-    const int Gl = (n + kNW - 1) / kNW;                                \
-    if (g < Gl) prrlu_body<(EA), 1, kNW, true>(A, S, Gl, g);           \
+    const int Gl = (n + NWT * (EB) - 1) / (NWT * (EB));                \
+    if (g < Gl) prrlu_body<(EA), (EB), NWT, true>(A, S, Gl, g);        \
     return;                                                            \
   }
-  ACI_CTA_VARIANT(1, 2)    //   32 x   32
-  ACI_CTA_VARIANT(2, 4)    //   64 x   64
-  ACI_CTA_VARIANT(4, 2)    //  128 x   32
-  ACI_CTA_VARIANT(1, 8)    //   32 x  128
-  ACI_CTA_VARIANT(4, 8)    //  128 x  128
-  ACI_CTA_VARIANT(2, 16)   //   64 x  256
-  ACI_CTA_VARIANT(8, 4)    //  256 x   64
-  ACI_CTA_VARIANT(1, 32)   //   32 x  512
-  ACI_CTA_VARIANT(16, 2)   //  512 x   32
-  ACI_GRID_VARIANT(4)      //  128 x 16 per CTA
-  ACI_GRID_VARIANT(8)      //  256 x 16 per CTA
-  ACI_GRID_VARIANT(16)     //  512 x 16 per CTA
-  ACI_GRID_VARIANT(32)     // 1024 x 16 per CTA
+  if (NWT == 16) {
+    ACI_CTA_VARIANT(1, 2)    //   32 x   32
+    ACI_CTA_VARIANT(2, 4)    //   64 x   64
+    ACI_CTA_VARIANT(4, 2)    //  128 x   32
+    ACI_CTA_VARIANT(1, 8)    //   32 x  128
+    ACI_CTA_VARIANT(4, 8)    //  128 x  128
+    ACI_CTA_VARIANT(2, 16)   //   64 x  256
+    ACI_CTA_VARIANT(8, 4)    //  256 x   64
+    ACI_CTA_VARIANT(1, 32)   //   32 x  512
+    ACI_CTA_VARIANT(16, 2)   //  512 x   32
+    ACI_GRID_VARIANT(4)      //  128 x 16 per CTA
+    ACI_GRID_VARIANT(8)      //  256 x 16 per CTA
+    ACI_GRID_VARIANT(16)     //  512 x 16 per CTA
+  } else {
+    ACI_CTA_VARIANT(1, 4)    //   32 x   32
+    ACI_CTA_VARIANT(2, 8)    //   64 x   64
+    ACI_CTA_VARIANT(4, 4)    //  128 x   32
+    ACI_CTA_VARIANT(1, 16)   //   32 x  128
+    ACI_CTA_VARIANT(4, 16)   //  128 x  128
+    ACI_CTA_VARIANT(8, 8)    //  256 x   64
+    ACI_CTA_VARIANT(2, 32)   //   64 x  256
+    ACI_CTA_VARIANT(32, 2)   // 1024 x   16
+    ACI_GRID_VARIANT(4)      //  128 x 8 per CTA
+    ACI_GRID_VARIANT(8)      //  256 x 8 per CTA
+    ACI_GRID_VARIANT(16)     //  512 x 8 per CTA
+    ACI_GRID_VARIANT2(32, ACI_BIG_EB)  // 1024 x 8*EB per CTA
+  }
 #undef ACI_CTA_VARIANT
 #undef ACI_GRID_VARIANT
+#undef ACI_GRID_VARIANT2
 }
 
 constexpr int kMaxCTAs = 148;
+constexpr int kRowsSmall = 512;  // static rows handled by the 16-warp instantiation
 
-bool fits_one_cta(int m, int n) {
-  const int v[][2] = {{1, 2}, {2, 4}, {4, 2}, {1, 8}, {4, 8}, {2, 16}, {8, 4}, {1, 32}, {16, 2}};
-  for (auto &e : v)
-    if (m <= 32 * e[0] && n <= kNW * e[1]) return true;
+bool fits_one_cta(int m, int n, int nwt) {
+  const int v16[][2] = {{1, 2}, {2, 4}, {4, 2}, {1, 8}, {4, 8}, {2, 16}, {8, 4}, {1, 32}, {16, 2}};
+  const int v8[][2] = {{1, 4}, {2, 8}, {4, 4}, {1, 16}, {4, 16}, {8, 8}, {2, 32}, {32, 2}};
+  if (nwt == 16) {
+    for (auto &e : v16)
+      if (m <= 32 * e[0] && n <= 16 * e[1]) return true;
+  } else {
+    for (auto &e : v8)
+      if (m <= 32 * e[0] && n <= 8 * e[1]) return true;
+  }
   return false;
 }
 
 }  // namespace
 
 bool prrlu_supported(int max_m, int max_n) {
-  if (fits_one_cta(max_m, max_n)) return true;
-  return max_m <= kMaxRows && (max_n + kNW - 1) / kNW <= kMaxCTAs;
+  if (max_m <= kRowsSmall) return fits_one_cta(max_m, max_n, 16) || (max_n + 15) / 16 <= kMaxCTAs;
+  return max_m <= kMaxRows && (fits_one_cta(max_m, max_n, 8) || (max_n + 7) / 8 <= kMaxCTAs);
 }
 
 void prrlu_envelope(int *max_rows, int *max_cols) {
   *max_rows = kMaxRows;
-  *max_cols = kMaxCTAs * kNW;
+  *max_cols = kMaxCTAs * 8;
 }
 
 size_t prrlu_exchange_bytes(int max_m, int max_n) {
   (void)max_n;
   int cap = max_m < kMaxRows ? kMaxRows : max_m;
-  return (size_t)2 * kMaxCTAs * cap * sizeof(double) + 2 * kMaxCTAs * 16 + 256;
+  return (size_t)2 * kMaxCTAs * cap * 16 + 2 * kMaxCTAs * 32 + 256;
 }
 
 void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st) {
-  if (fits_one_cta(max_m, max_n)) {
-    prrlu_kernel<<<1, kNW * 32, 0, st>>>(a);
+  const int nwt = max_m <= kRowsSmall ? 16 : 8;
+  const void *kern = nwt == 16 ? (const void *)prrlu_kernel<16> : (const void *)prrlu_kernel<8>;
+  if (fits_one_cta(max_m, max_n, nwt)) {
+    void *params[] = {const_cast<LuArgs *>(&a)};
+    cudaLaunchKernel(kern, dim3(1), dim3(nwt * 32), params, 0, st);
     return;
   }
   cudaMemsetAsync(a.counter, 0, sizeof(unsigned), st);
-  int G = (max_n + kNW - 1) / kNW;
+  const int G = (max_n + nwt - 1) / nwt;
   LuArgs args = a;
   void *params[] = {&args};
-  cudaLaunchCooperativeKernel((const void *)prrlu_kernel, dim3(G), dim3(kNW * 32), params, 0, st);
+  cudaLaunchCooperativeKernel(kern, dim3(G), dim3(nwt * 32), params, 0, st);
 }

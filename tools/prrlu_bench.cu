@@ -10,20 +10,26 @@
 
 int main(int argc, char **argv) {
   int sizes[][3] = {{64, 64, 64}, {128, 128, 128}, {256, 256, 256}, {512, 512, 512}, {1024, 1024, 512}};
-  double *dM, *dU, *dcol, *deps;
+  double *dM, *dU, *deps;
+  unsigned long long *dcol;
   int *drows, *dcols, *dr;
-  unsigned *dkeys, *dctr;
+  unsigned long long *dkeys;
+  unsigned *dctr, *depoch;
   LuDims *ddims;
   unsigned long long *dscale;
   long long *ddbg;
   cudaMalloc(&dM, sizeof(double) * 1024 * 1024);
   cudaMalloc(&dU, sizeof(double) * 1024 * 1024);
-  cudaMalloc(&dcol, sizeof(double) * 2 * 148 * 1024);
+  cudaMalloc(&dcol, 16 * 2 * 148 * 1024);
+  cudaMemset(dcol, 0, 16 * 2 * 148 * 1024);
+  cudaMalloc(&depoch, 4);
+  cudaMemset(depoch, 0, 4);
   cudaMalloc(&deps, 8);
   cudaMalloc(&drows, 4 * 1024);
   cudaMalloc(&dcols, 4 * 1024);
   cudaMalloc(&dr, 4);
-  cudaMalloc(&dkeys, 16 * 2 * 148);
+  cudaMalloc(&dkeys, 32 * 2 * 148);
+  cudaMemset(dkeys, 0, 32 * 2 * 148);
   cudaMalloc(&dctr, 4);
   cudaMalloc(&ddims, sizeof(LuDims));
   cudaMalloc(&dscale, 8);
@@ -45,7 +51,7 @@ int main(int argc, char **argv) {
     LuArgs a = {};
     a.M = dM; a.dims = ddims; a.tol = 0.0; a.thr_mode = 2; a.scale_bits = dscale;
     a.rows = drows; a.cols = dcols; a.r_out = dr; a.eps_out = deps; a.U = dU;
-    a.colpub = dcol; a.colcap = 1024; a.keys = dkeys; a.counter = dctr; a.dbg = ddbg;
+    a.colpub = dcol; a.colcap = 1024; a.keys = dkeys; a.counter = dctr; a.epoch = depoch; a.dbg = ddbg;
     for (int rep = 0; rep < 3; ++rep) {
       cudaMemset(ddbg, 0, 64);
       cudaEventRecord(e0);

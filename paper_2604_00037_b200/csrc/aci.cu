@@ -746,6 +746,9 @@ static int prepare(aci_op op, const tt_t *const *inputs, int n_inputs, Inputs &I
     for (int u = 0; u < N; ++u)
       if (I.op.expo[t * N + u] > 3 * ACI_MAX_EXPO) return fail(ACI_ERR_INVALID, "aci: merged exponent too large");
   }
+  I.op.monomial_all_ones = I.op.T == 1 ? 1 : 0;
+  for (int u = 0; u < N && I.op.T == 1; ++u)
+    if (I.op.expo[u] != 1) I.op.monomial_all_ones = 0;
   return ACI_OK;
 }
 
@@ -810,9 +813,21 @@ static void bond_update(Run &R, const FOp &op, double tol, int tol_mode, int b, 
   S.ldu = R.nmax[b];
   S.maxrank = R.maxrank;
   S.Pi = R.Pi;
+  // Pi kernel input order: inputs whose inner dimension chi^n_{b+1} is large run the DMMA main
+  // loop (first), tiny ones (e.g. rank-2 inputs) are evaluated in the epilogue; the op's
+  // exponents are permuted to the same order.
+  int order[ACI_GEMM_MAX_IN], nbig = 0, nsmall = 0;
+  for (int n = 0; n < N; ++n)
+    if (R.xr[n][b + 1] > gemm_small_k()) order[nbig++] = n;
+  for (int n = 0; n < N; ++n)
+    if (R.xr[n][b + 1] <= gemm_small_k()) order[nbig + nsmall++] = n;
+  FOp opb = op;
+  for (int t = 0; t < op.T; ++t)
+    for (int k = 0; k < N; ++k) opb.expo[t * N + k] = op.expo[t * N + order[k]];
   int ab_m = 0, ab_n = 0;
-  for (int n = 0; n < N; ++n) {
-    InBond &I = S.in[n];
+  for (int kk = 0; kk < N; ++kk) {
+    const int n = order[kk];
+    InBond &I = S.in[kk];
     I.c0 = R.xr[n][b]; I.c1 = R.xr[n][b + 1]; I.c2 = R.xr[n][b + 2];
     I.Xb = R.xcore0[n] + R.xoff[n][b];
     I.Xb1 = R.xcore0[n] + R.xoff[n][b + 1];
@@ -833,7 +848,7 @@ static void bond_update(Run &R, const FOp &op, double tol, int tol_mode, int b, 
     R.P->end(1);
   }
   R.P->begin(ACI_PROF_GEMM_PI);
-  launch_gemm(R.dPi, 1, R.mmax[b], R.nmax[b], N, true, op, R.scale, R.nonfinite, st);
+  launch_gemm_split(R.dPi, 1, R.mmax[b], R.nmax[b], nbig, nsmall, true, opb, R.scale, R.nonfinite, st);
   R.P->end(1);
   LuArgs a = {};
   a.M = R.Pi; a.dims = R.dLu; a.tol = tol; a.thr_mode = tol_mode == ACI_TOL_RELATIVE ? 0 : 2;

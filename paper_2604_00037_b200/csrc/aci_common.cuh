@@ -24,6 +24,7 @@ struct FOp {
   int T, N;
   double coef[8];
   int expo[8 * ACI_GEMM_MAX_IN];
+  int monomial_all_ones;  // 1: f = coef[0] * x_0 * ... * x_{N-1} (fast epilogue path)
 };
 
 // Live sizes of one prrLU problem, written by the planner on the device.
@@ -57,6 +58,11 @@ struct LuArgs {
 // ---- launchers (defined in gemm.cu / prrlu.cu / sweep.cu) ----
 void launch_gemm(const GemmDesc *d_descs, int ndesc, int max_m, int max_n, int nin, bool fuse, const FOp &op,
                  unsigned long long *scale_bits, int *nonfinite, cudaStream_t st);
+// Pi launch with the inputs split by inner dimension: descriptors 0..nbig-1 run the DMMA main
+// loop, nbig..nbig+nsmall-1 (K <= gemm_small_k()) are evaluated in the epilogue.
+void launch_gemm_split(const GemmDesc *d_descs, int ndesc, int max_m, int max_n, int nbig, int nsmall, bool fuse,
+                       const FOp &op, unsigned long long *scale_bits, int *nonfinite, cudaStream_t st);
+int gemm_small_k();
 // Sets kernel attributes (dynamic shared memory) once; call before any stream capture.
 void gemm_init();
 // C = S - A B for every descriptor (blocked triangular solve updates).

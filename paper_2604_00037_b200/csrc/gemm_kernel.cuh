@@ -1,0 +1,302 @@
+// FP64 tensor-core (DMMA) GEMM templates for the 2-site update (included by gemm.cu; the
+// development benchmark tools/gemm_bench.cu includes it too to sweep tile shapes).
+//   a1/a2: A^n = L^n_{l-1} X^n_l, B^n = X^n_{l+1} R^n_{l+2}     (EPI_STORE)
+//   a3+a4 (Eq. pifromframes, f of P:459-462): Pi = f(A^1 B^1, ..., A^N B^N) (EPI_F)
+//   blocked output-core solve: C = S - A B                                         (EPI_SUB)
+// On sm_100a FP64 matrix math exists only as warp-level mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4
+// (tcgen05 has no f64 kind).
+//
+// Structure: BM x BN CTA tile, WM x WN warp tiles (MI x NI DMMA 8x8 tiles), BK-deep k-tiles in a
+// STAGES-deep cp.async ring. Problem sizes come from device descriptors (live ranks); CTAs whose
+// tile lies outside the live M x N exit at once. In EPI_F the products never reach HBM: f, the
+// NaN check and max|Pi| run on registers. Inputs whose inner dimension K is tiny (<= kSmallK, e.g.
+// the rank-2 input B of configs[1],[3]) are NBIG..NBIG+NSMALL-1 in the descriptor and are
+// evaluated in the epilogue from shared memory instead of a DMMA main loop.
+#pragma once
+#include "aci_common.cuh"
+
+namespace gemmk {
+
+constexpr int kSmallK = 4;
+enum { EPI_STORE = 0, EPI_F = 1, EPI_SUB = 2 };
+
+template <int BM_, int BN_, int WM_, int WN_, int BK_, int ST_, int MINB_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, BK = BK_, STAGES = ST_, MINB = MINB_;
+  static constexpr int WARPS_N = BN / WN, NW = (BM / WM) * (BN / WN), NT = NW * 32;
+  static constexpr int MI = WM / 8, NI = WN / 8;
+  // Both tiles are stored k-permuted: element k of a row sits at (k % 4) * KQ + k / 4 (KQ = BK/4),
+  // so the KQ k-steps a lane (g, c) needs for one fragment (k = c, c+4, ...) are contiguous and
+  // come in KQ/2 LDS.128. B is stored transposed ([col][k]) to use the same access pattern.
+  // Row pitch = BK + 2 doubles: a quarter-warp's 8 16-byte reads hit 8 distinct bank groups.
+  static constexpr int KQ = BK / 4;
+  static constexpr int LDA = BK + 2;
+  static constexpr int LDB = BK + 2;
+  struct Smem {
+    double A[STAGES][BM][LDA];
+    double B[STAGES][BN][LDB];
+  };
+  static_assert(BK % 8 == 0, "two k-steps per LDS.128");
+  static_assert((BM * BK) % NT == 0 && (BK * BN) % NT == 0, "tile loads must divide evenly");
+  static_assert(BM * kSmallK + kSmallK * BN <= STAGES * (BM * LDA + BN * LDB), "small-K staging fits");
+};
+
+__device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <class CF>
+__device__ __forceinline__ void load_stage(typename CF::Smem &sm, int st, const double *A, int lda, const double *B,
+                                           int ldb, int M, int N, int K, int m0, int n0, int k0) {
+  const int t = threadIdx.x;
+  if (m0 + CF::BM <= M && n0 + CF::BN <= N && k0 + CF::BK <= K) {  // interior tile: no bounds checks
+#pragma unroll
+    for (int i = 0; i < (CF::BM * CF::BK) / CF::NT; ++i) {
+      const int e = t + CF::NT * i;
+      const int row = e / CF::BK, kc = e % CF::BK;
+      cp_async8(&sm.A[st][row][(kc & 3) * CF::KQ + (kc >> 2)], A + (size_t)(m0 + row) * lda + (k0 + kc), true);
+    }
+#pragma unroll
+    for (int i = 0; i < (CF::BK * CF::BN) / CF::NT; ++i) {
+      const int e = t + CF::NT * i;
+      const int kr = e / CF::BN, col = e % CF::BN;
+      cp_async8(&sm.B[st][col][(kr & 3) * CF::KQ + (kr >> 2)], B + (size_t)(k0 + kr) * ldb + (n0 + col), true);
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < (CF::BM * CF::BK) / CF::NT; ++i) {
+    const int e = t + CF::NT * i;
+    const int row = e / CF::BK, kc = e % CF::BK;
+    const bool v = (m0 + row < M) && (k0 + kc < K);
+    const double *src = v ? A + (size_t)(m0 + row) * lda + (k0 + kc) : A;
+    cp_async8(&sm.A[st][row][(kc & 3) * CF::KQ + (kc >> 2)], src, v);
+  }
+#pragma unroll
+  for (int i = 0; i < (CF::BK * CF::BN) / CF::NT; ++i) {
+    const int e = t + CF::NT * i;
+    const int kr = e / CF::BN, col = e % CF::BN;
+    const bool v = (k0 + kr < K) && (n0 + col < N);
+    const double *src = v ? B + (size_t)(k0 + kr) * ldb + (n0 + col) : B;
+    cp_async8(&sm.B[st][col][(kr & 3) * CF::KQ + (kr >> 2)], src, v);
+  }
+}
+
+// acc += A (M x K) * B (K x N) on this CTA's tile.
+template <class CF>
+__device__ __forceinline__ void mainloop(typename CF::Smem &sm, double (&acc)[CF::MI][CF::NI][2], const double *A,
+                                         int lda, const double *B, int ldb, int M, int N, int K, int m0, int n0) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, c = lane & 3;
+  const int wm = (w / CF::WARPS_N) * CF::WM, wn = (w % CF::WARPS_N) * CF::WN;
+  const int nk = (K + CF::BK - 1) / CF::BK;
+  __syncthreads();  // shared memory reuse across inputs
+#pragma unroll
+  for (int s = 0; s < CF::STAGES - 1; ++s) {
+    if (s < nk) load_stage<CF>(sm, s, A, lda, B, ldb, M, N, K, m0, n0, s * CF::BK);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<CF::STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = kt + CF::STAGES - 1;
+      if (nxt < nk) load_stage<CF>(sm, nxt % CF::STAGES, A, lda, B, ldb, M, N, K, m0, n0, nxt * CF::BK);
+      cp_async_commit();
+    }
+    const int st = kt % CF::STAGES;
+#pragma unroll
+    for (int kp = 0; kp < CF::KQ / 2; ++kp) {  // two k-steps per LDS.128
+      double2 a[CF::MI], b[CF::NI];
+#pragma unroll
+      for (int mi = 0; mi < CF::MI; ++mi)
+        a[mi] = *reinterpret_cast<const double2 *>(&sm.A[st][wm + mi * 8 + g][c * CF::KQ + 2 * kp]);
+#pragma unroll
+      for (int ni = 0; ni < CF::NI; ++ni)
+        b[ni] = *reinterpret_cast<const double2 *>(&sm.B[st][wn + ni * 8 + g][c * CF::KQ + 2 * kp]);
+#pragma unroll
+      for (int mi = 0; mi < CF::MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < CF::NI; ++ni) dmma(acc[mi][ni], a[mi].x, b[ni].x);
+#pragma unroll
+      for (int mi = 0; mi < CF::MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < CF::NI; ++ni) dmma(acc[mi][ni], a[mi].y, b[ni].y);
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <class CF, int NBIG, int NSMALL, int EPI>
+__global__ void __launch_bounds__(CF::NT, CF::MINB)
+    gemm_kernel(const GemmDesc *__restrict__ descs, FOp op, unsigned long long *scale_bits, int *nonfinite) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto &sm = *reinterpret_cast<typename CF::Smem *>(smem_raw);
+  const GemmDesc &D = descs[blockIdx.z];
+  const int M = D.M, N = D.N;
+  const int m0 = blockIdx.y * CF::BM, n0 = blockIdx.x * CF::BN;
+  if (m0 >= M || n0 >= N) return;
+  constexpr int NB = NBIG > 0 ? NBIG : 1;
+
+  double acc[NB][CF::MI][CF::NI][2];
+#pragma unroll
+  for (int i = 0; i < NB; ++i)
+#pragma unroll
+    for (int mi = 0; mi < CF::MI; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < CF::NI; ++ni) acc[i][mi][ni][0] = acc[i][mi][ni][1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < NBIG; ++i)
+    mainloop<CF>(sm, acc[i], D.A[i], D.lda[i], D.B[i], D.ldb[i], M, N, D.K[i], m0, n0);
+
+  // small-K inputs: stage A_s (BM x K) and B_s (K x BN) in shared memory once
+  double *sA = reinterpret_cast<double *>(smem_raw);
+  double *sB = sA + NSMALL * CF::BM * kSmallK;
+  if (NSMALL > 0) {
+    __syncthreads();
+#pragma unroll
+    for (int s_ = 0; s_ < NSMALL; ++s_) {
+      const int i = NBIG + s_, K = D.K[i];
+      for (int t = threadIdx.x; t < CF::BM * kSmallK; t += CF::NT) {
+        const int row = t / kSmallK, kk = t % kSmallK;
+        sA[s_ * CF::BM * kSmallK + t] =
+            (kk < K && m0 + row < M) ? D.A[i][(size_t)(m0 + row) * D.lda[i] + kk] : 0.0;
+      }
+      for (int t = threadIdx.x; t < kSmallK * CF::BN; t += CF::NT) {
+        const int kk = t / CF::BN, col = t % CF::BN;
+        sB[s_ * kSmallK * CF::BN + t] =
+            (kk < K && n0 + col < N) ? D.B[i][(size_t)kk * D.ldb[i] + n0 + col] : 0.0;
+      }
+    }
+    __syncthreads();
+  }
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, c = lane & 3;
+  const int wm = (w / CF::WARPS_N) * CF::WM, wn = (w % CF::WARPS_N) * CF::WN;
+  double vmax = 0.0;
+  bool bad = false;
+  if (EPI == EPI_F) {
+    // small inputs: this thread's MI rows of A_s and 2*NI columns of B_s in registers
+    constexpr int NS = NSMALL > 0 ? NSMALL : 1;
+    double ra[NS][CF::MI][kSmallK], rb[NS][CF::NI][2][kSmallK];
+    int ks[NS];
+#pragma unroll
+    for (int s_ = 0; s_ < NSMALL; ++s_) {
+      ks[s_] = D.K[NBIG + s_];
+#pragma unroll
+      for (int kk = 0; kk < kSmallK; ++kk) {
+#pragma unroll
+        for (int mi = 0; mi < CF::MI; ++mi)
+          ra[s_][mi][kk] = sA[s_ * CF::BM * kSmallK + (wm + mi * 8 + g) * kSmallK + kk];
+#pragma unroll
+        for (int ni = 0; ni < CF::NI; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) rb[s_][ni][e][kk] = sB[s_ * kSmallK * CF::BN + kk * CF::BN + wn + ni * 8 + 2 * c + e];
+      }
+    }
+    const bool mono = op.monomial_all_ones != 0;
+    const double coef0 = op.coef[0];
+#pragma unroll
+    for (int mi = 0; mi < CF::MI; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < CF::NI; ++ni) {
+        const int row = m0 + wm + mi * 8 + g, col0 = n0 + wn + ni * 8 + 2 * c;
+        double y2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double x[NBIG + NSMALL];
+#pragma unroll
+          for (int i = 0; i < NBIG; ++i) x[i] = acc[i][mi][ni][e];
+#pragma unroll
+          for (int s_ = 0; s_ < NSMALL; ++s_) {
+            double v = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < kSmallK; ++kk)
+              if (kk < ks[s_]) v = fma(ra[s_][mi][kk], rb[s_][ni][e][kk], v);
+            x[NBIG + s_] = v;
+          }
+          double y;
+          if (mono) {
+            // f = coef * prod x_i, multiplied in the oracle's order (apply_f with one term)
+            double p = coef0;
+#pragma unroll
+            for (int i = 0; i < NBIG + NSMALL; ++i) p *= x[i];
+            y = p;
+          } else {
+            y = 0.0;
+            for (int t = 0; t < op.T; ++t) {
+              double p = op.coef[t];
+#pragma unroll
+              for (int i = 0; i < NBIG + NSMALL; ++i)
+                for (int q = 0; q < op.expo[t * op.N + i]; ++q) p *= x[i];
+              y += p;
+            }
+          }
+          bad |= !isfinite(y);
+          vmax = fmax(vmax, fabs(y));
+          y2[e] = y;
+        }
+        if (row < M) {
+          double *dst = D.C + (size_t)row * D.ldc + col0;
+          if (col0 + 1 < N) {
+            dst[0] = y2[0];
+            dst[1] = y2[1];
+          } else if (col0 < N) {
+            dst[0] = y2[0];
+          }
+        }
+      }
+  } else {
+#pragma unroll
+    for (int mi = 0; mi < CF::MI; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < CF::NI; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int row = m0 + wm + mi * 8 + g, col = n0 + wn + ni * 8 + 2 * c + e;
+          if (row < M && col < N) {
+            double y = acc[0][mi][ni][e];
+            if (EPI == EPI_SUB) y = D.S[(size_t)row * D.lds + col] - y;
+            D.C[(size_t)row * D.ldc + col] = y;
+          }
+        }
+  }
+  if (EPI == EPI_F) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+      bad = bad | (__shfl_xor_sync(0xffffffffu, (int)bad, o) != 0);
+    }
+    if (lane == 0) {
+      if (vmax > 0.0) atomicMax(scale_bits, (unsigned long long)__double_as_longlong(vmax));
+      if (bad) atomicOr(nonfinite, 1);
+    }
+  }
+}
+
+template <class CF, int NBIG, int NSMALL, int EPI>
+inline void set_attr() {
+  cudaFuncSetAttribute(gemm_kernel<CF, NBIG, NSMALL, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(typename CF::Smem));
+}
+
+template <class CF, int NBIG, int NSMALL, int EPI>
+inline void launch(const GemmDesc *d, int ndesc, int max_m, int max_n, const FOp &op, unsigned long long *sb,
+                   int *nf, cudaStream_t st) {
+  dim3 grid((max_n + CF::BN - 1) / CF::BN, (max_m + CF::BM - 1) / CF::BM, ndesc);
+  gemm_kernel<CF, NBIG, NSMALL, EPI><<<grid, CF::NT, sizeof(typename CF::Smem), st>>>(d, op, sb, nf);
+}
+
+}  // namespace gemmk

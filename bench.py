@@ -126,6 +126,18 @@ def run_reference(args):
     return 0
 
 
+def reduce_over_ranks(ms, flops, e2e_value, dist, device):
+    """Replica aggregation: the job time is the slowest rank's, the work is summed."""
+    if dist is None:
+        return ms, flops, e2e_value
+    import torch
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    f = torch.tensor([flops, e2e_value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(f, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(f[0].item()), float(f[1].item())
+
+
 def cpu_baseline(chi, sweeps):
     import oracle
     from workloads import make_config
@@ -137,7 +149,7 @@ def cpu_baseline(chi, sweeps):
     res.free()
     return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"configs[3] chi={chi}, first {sweeps} of 4 iterations, single-thread naive C oracle, "
-                      f"{dt:.1f} s"}
+                      f"{dt:.1f} s on {os.cpu_count()} host cores (1 used)"}
 
 
 def main():
@@ -147,7 +159,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--chi", type=int, default=256)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-sweeps", type=int, default=2)
+    ap.add_argument("--ref-sweeps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sweep-chi", action="store_true", help="also print lines for chi=64,128 (stderr)")
     args = ap.parse_args()
@@ -276,18 +288,10 @@ def main():
 
     cf, tot_ms, tot_flops, launches, prof, reps, clocks, e2e = run_chi(args.chi, args.steps, args.warmup,
                                                                        with_e2e=True)
-    # max over ranks for time, sum over ranks for work
-    t_max, f_sum = tot_ms, tot_flops
-    if dist is not None:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
-        f = torch.tensor([tot_flops], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(f, op=dist.ReduceOp.SUM)
-        t_max, f_sum = float(t.item()), float(f.item())
-        if e2e is not None:
-            ev = torch.tensor([e2e["value"]], dtype=torch.float64, device="cuda")
-            dist.all_reduce(ev, op=dist.ReduceOp.SUM)
-            e2e["value"] = float(ev.item())
+    # max over ranks for time, sum over ranks for work (independent replicas)
+    t_max, f_sum, e2e_sum = reduce_over_ranks(tot_ms, tot_flops, e2e["value"] if e2e else 0.0, dist, "cuda")
+    if e2e is not None:
+        e2e["value"] = e2e_sum
     if rank == 0:
         pk = _peaks()
         value = f_sum / t_max / 1e9  # GFLOP/ms -> TFLOP/s

@@ -126,6 +126,23 @@ def run_reference(args):
     return 0
 
 
+def _ncu_traffic():
+    """DRAM bytes per launch (read + write) of the dominant kernels, from the newest committed
+    `ncu --set full` capture summary under profiles/ (None if there is none)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
+    if not files:
+        return {}
+    d = json.load(open(files[-1]))
+    out = {}
+    for k, v in d.items():
+        if isinstance(v, dict) and "dram_bytes_read" in v:
+            key = "prrlu" if k.startswith("prrlu") else "contraction"
+            out[key] = {"bytes": v["dram_bytes_read"] + v["dram_bytes_write"], "source": os.path.basename(files[-1]),
+                        "kernel": v["kernel"]}
+    return out
+
+
 def reduce_over_ranks(ms, flops, e2e_value, dist, device):
     """Replica aggregation: the job time is the slowest rank's, the work is summed."""
     if dist is None:
@@ -316,6 +333,13 @@ def main():
                    "peak": pk["dmma_tflops"], "unit": "TFLOP/s",
                    "frac": pi_flops / ((pi["ms"] + prof["gemm_ab"]["ms"]) * 1e9) / pk["dmma_tflops"],
                    "traffic": None, "note": "FP64 DMMA (mma.sync m8n8k4); peak = measured DMMA microbenchmark"}
+        tr = _ncu_traffic()
+        if "prrlu" in tr:
+            roof_prrlu["traffic"] = tr["prrlu"]["bytes"]
+            roof_prrlu["traffic_source"] = tr["prrlu"]["source"] + ": " + tr["prrlu"]["kernel"]
+        if "contraction" in tr:
+            roof_pi["traffic"] = tr["contraction"]["bytes"]
+            roof_pi["traffic_source"] = tr["contraction"]["source"] + ": " + tr["contraction"]["kernel"]
         roof = roof_prrlu if dom == "prrlu" else roof_pi
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,

@@ -264,3 +264,25 @@ def test_absolute_tolerance_mode(aci):
     ref = oracle.aci(xs, {"coef": [1.0], "expo": [[1, 1]]}, y0, 1e-3, 32, 6, relative=False)
     assert _pivot_agreement(ex, ref) == len(ref.log)
     assert _rel(oracle.tt_dense(out.cores()), oracle.tt_dense(ref.cores)) <= 1e-12
+
+
+def test_caller_workspace_and_stream(aci):
+    """Device memory and the stream come from PyTorch (aci_workspace_query + a torch tensor as
+    the workspace, a torch stream as the call's stream); results equal the default path."""
+    import torch
+    cf = make_config(1, npts=5000)
+    xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+    y0 = aci.TensorTrain.from_cores(cf["y_init"])
+    nbytes = aci.workspace_query(xs, cf["maxrank"], y0)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.Stream()
+    out1, _, rep1, _ = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0,
+                                           workspace=(ws.data_ptr(), nbytes), stream=st.cuda_stream)
+    out2, _, rep2, _ = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0)
+    assert rep1["graph_iterations"] == rep1["iterations"]  # a non-default stream replays one CUDA graph
+    c1, c2 = out1.cores(), out2.cores()
+    assert all(np.array_equal(a, b) for a, b in zip(c1, c2))
+    with pytest.raises(aci.AciError) as e:
+        aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0,
+                            workspace=(ws.data_ptr(), nbytes // 2))
+    assert "OOM" in str(e.value)

@@ -58,6 +58,9 @@ __device__ __forceinline__ void red_relaxed_add(unsigned *p, unsigned v) {
 // Counter poll with NP loads in flight, issued ~kPollGap cycles apart and checked in issue
 // order: completion is seen ~one L2 latency after it lands instead of up to two, which also
 // shrinks the skew between CTAs at the next pivot.
+#ifndef ACI_KEYPOLL_MAXG
+#define ACI_KEYPOLL_MAXG 16
+#endif
 #ifndef ACI_POLL_NP
 #define ACI_POLL_NP 1  // measured: more loads in flight only add contention on the counter line
 #endif
@@ -118,6 +121,17 @@ __device__ __forceinline__ double key_abs(const Key &k) {
   return __longlong_as_double((long long)(((unsigned long long)k.hi << 32) | k.lo));
 }
 
+// columns per warp of the 8-warp grid tiers, measured (tools/prrlu_bench.cu): 16 CTAs with the
+// key-poll barrier beat more CTAs with the counter barrier up to 512 rows
+#ifndef ACI_W8_EB128
+#define ACI_W8_EB128 4
+#endif
+#ifndef ACI_W8_EB256
+#define ACI_W8_EB256 2
+#endif
+#ifndef ACI_W8_EB512
+#define ACI_W8_EB512 4
+#endif
 #ifndef ACI_BIG_EB
 #define ACI_BIG_EB 2  // columns per warp for the 1024-row grid tier (64 CTAs for 1024 columns)
 #endif
@@ -130,7 +144,7 @@ struct PrrluSmem {
   double raw[kMaxRows];  // CTA tier: raw pivot column
   double u[kMaxCB];      // pivot row segment
   unsigned hi[32], lo[32], id[32];
-  unsigned win[4];  // grid winner broadcast (ACI_PRRLU_KEYPOLL)
+  unsigned win[4];  // grid winner broadcast (key-poll mode)
 };
 
 // One factorisation, register tile EA x EB per thread, NW warps per CTA. GRID: G CTAs (this is
@@ -249,24 +263,23 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
           unsigned long long *kd = A.keys + ((size_t)par * G + g) * 4;
           st_pkt(kd, tagged(tag, ck.hi), tagged(tag, ck.lo));
           st_pkt(kd + 2, tagged(tag, ck.id), 0ull);
-          red_relaxed_add(A.counter, 1u);
+          if (G > ACI_KEYPOLL_MAXG) red_relaxed_add(A.counter, 1u);
         }
       }
       PHASE(2);
-#ifndef ACI_PRRLU_KEYPOLL
-      if (tid == 0) poll_counter(A.counter, (unsigned)(k + 1) * (unsigned)G);
-      __syncthreads();  // S2: every CTA has arrived
-#endif
+      // small grids: the tagged keys themselves are the barrier (warp 0 polls them, no counter);
+      // larger grids: one counter poll then every warp reads the keys (measured crossover ~16)
+      const bool keypoll = G <= ACI_KEYPOLL_MAXG;
+      if (!keypoll) {
+        if (tid == 0) poll_counter(A.counter, (unsigned)(k + 1) * (unsigned)G);
+        __syncthreads();  // S2: every CTA has arrived
+      }
       PHASE(3);
       // read all G keys: independent loads in flight, stale packets re-read until their tag is
-      // this step's (with ACI_PRRLU_KEYPOLL only warp 0 does this and the tags are the barrier)
+      // this step's
       constexpr int KPL = (148 + 31) / 32;  // keys per lane
       Key gk{0u, 0u, BAD_ID};
-#ifdef ACI_PRRLU_KEYPOLL
-      if (w == 0) {
-#else
-      {
-#endif
+      if (!keypoll || w == 0) {
         unsigned long long kw[KPL][4];
 #pragma unroll
         for (int t = 0; t < KPL; ++t) {
@@ -293,11 +306,11 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         }
       }
       win = warp_argmax(gk);
-#ifdef ACI_PRRLU_KEYPOLL
-      if (tid == 0) { S.win[0] = win.hi; S.win[1] = win.lo; S.win[2] = win.id; }
-      __syncthreads();  // S2: the winner, known only after every CTA's key arrived
-      win = Key{S.win[0], S.win[1], S.win[2]};
-#endif
+      if (keypoll) {
+        if (tid == 0) { S.win[0] = win.hi; S.win[1] = win.lo; S.win[2] = win.id; }
+        __syncthreads();  // S2: the winner, known only after every CTA's key arrived
+        win = Key{S.win[0], S.win[1], S.win[2]};
+      }
       PHASE(4);
     }
 
@@ -445,9 +458,9 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
     ACI_CTA_VARIANT(8, 4)    //  256 x   64
     ACI_CTA_VARIANT(1, 32)   //   32 x  512
     ACI_CTA_VARIANT(16, 2)   //  512 x   32
-    ACI_GRID_VARIANT(4)      //  128 x 16 per CTA
-    ACI_GRID_VARIANT(8)      //  256 x 16 per CTA
-    ACI_GRID_VARIANT(16)     //  512 x 16 per CTA
+    ACI_GRID_VARIANT2(4, 2)  //  128 x 32 per CTA (key-poll barrier for <= 16 CTAs)
+    ACI_GRID_VARIANT2(8, 2)  //  256 x 32 per CTA
+    ACI_GRID_VARIANT(16)     //  512 x 16 per CTA (counter barrier)
   } else {
     ACI_CTA_VARIANT(1, 4)    //   32 x   32
     ACI_CTA_VARIANT(2, 8)    //   64 x   64
@@ -457,9 +470,9 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
     ACI_CTA_VARIANT(8, 8)    //  256 x   64
     ACI_CTA_VARIANT(2, 32)   //   64 x  256
     ACI_CTA_VARIANT(32, 2)   // 1024 x   16
-    ACI_GRID_VARIANT(4)      //  128 x 8 per CTA
-    ACI_GRID_VARIANT(8)      //  256 x 8 per CTA
-    ACI_GRID_VARIANT(16)     //  512 x 8 per CTA
+    ACI_GRID_VARIANT2(4, ACI_W8_EB128)   //  128 x 8*EB per CTA
+    ACI_GRID_VARIANT2(8, ACI_W8_EB256)   //  256 x 8*EB per CTA
+    ACI_GRID_VARIANT2(16, ACI_W8_EB512)  //  512 x 8*EB per CTA
     ACI_GRID_VARIANT2(32, ACI_BIG_EB)  // 1024 x 8*EB per CTA
   }
 #undef ACI_CTA_VARIANT
@@ -486,8 +499,7 @@ bool fits_one_cta(int m, int n, int nwt) {
 }  // namespace
 
 bool prrlu_supported(int max_m, int max_n) {
-  if (max_m <= kRowsSmall) return fits_one_cta(max_m, max_n, 16) || (max_n + 15) / 16 <= kMaxCTAs;
-  return max_m <= kMaxRows && (fits_one_cta(max_m, max_n, 8) || (max_n + 7) / 8 <= kMaxCTAs);
+  return fits_one_cta(max_m, max_n, 8) || (max_m <= kMaxRows && (max_n + 7) / 8 <= kMaxCTAs);
 }
 
 void prrlu_envelope(int *max_rows, int *max_cols) {
@@ -502,15 +514,16 @@ size_t prrlu_exchange_bytes(int max_m, int max_n) {
 }
 
 void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st) {
-  const int nwt = max_m <= kRowsSmall ? 16 : 8;
-  const void *kern = nwt == 16 ? (const void *)prrlu_kernel<16> : (const void *)prrlu_kernel<8>;
+  // the 8-warp instantiation measured faster than the 16-warp one at every block size
+  constexpr int nwt = 8;
+  const void *kern = (const void *)prrlu_kernel<nwt>;
   if (fits_one_cta(max_m, max_n, nwt)) {
     void *params[] = {const_cast<LuArgs *>(&a)};
     cudaLaunchKernel(kern, dim3(1), dim3(nwt * 32), params, 0, st);
     return;
   }
   cudaMemsetAsync(a.counter, 0, sizeof(unsigned), st);
-  const int G = (max_n + nwt - 1) / nwt;
+  const int G = (max_n + nwt - 1) / nwt;  // enough for every variant the live size may select
   LuArgs args = a;
   void *params[] = {&args};
   cudaLaunchCooperativeKernel(kern, dim3(G), dim3(nwt * 32), params, 0, st);

@@ -9,7 +9,9 @@
 #include <vector>
 
 int main(int argc, char **argv) {
-  int sizes[][3] = {{64, 64, 64}, {128, 128, 128}, {256, 256, 256}, {512, 512, 512}, {1024, 1024, 512}};
+  // {m, n, kmax, static size}: static 1024 exercises the 8-warp instantiation on small live blocks
+  int sizes[][4] = {{64, 64, 64, 0}, {128, 128, 128, 0}, {256, 256, 256, 0}, {512, 512, 512, 0}, {1024, 1024, 512, 0},
+                    {64, 64, 64, 1024}, {128, 128, 128, 1024}, {256, 256, 256, 1024}, {512, 512, 512, 1024}};
   double *dM, *dU, *deps;
   unsigned long long *dcol;
   int *drows, *dcols, *dr;
@@ -44,7 +46,7 @@ int main(int argc, char **argv) {
   cudaEventCreate(&e1);
   int only = argc > 1 ? atoi(argv[1]) : -1;
   for (auto &sz : sizes) {
-    int m = sz[0], n = sz[1], kmax = sz[2];
+    int m = sz[0], n = sz[1], kmax = sz[2], stat = sz[3] ? sz[3] : sz[0];
     if (only > 0 && m != only) continue;
     LuDims D{m, n, n, kmax, n};
     cudaMemcpy(ddims, &D, sizeof(D), cudaMemcpyHostToDevice);
@@ -55,7 +57,7 @@ int main(int argc, char **argv) {
     for (int rep = 0; rep < 3; ++rep) {
       cudaMemset(ddbg, 0, 64);
       cudaEventRecord(e0);
-      launch_prrlu(a, m, n, 0);
+      launch_prrlu(a, stat, stat, 0);
       cudaEventRecord(e1);
       cudaError_t err = cudaEventSynchronize(e1);
       if (err != cudaSuccess) { printf("error %s\n", cudaGetErrorString(err)); return 1; }
@@ -66,7 +68,8 @@ int main(int argc, char **argv) {
       cudaMemcpy(&r, dr, 4, cudaMemcpyDeviceToHost);
       cudaMemcpy(dbg, ddbg, 64, cudaMemcpyDeviceToHost);
       if (rep == 2) {
-        printf("%4dx%4d r=%4d: %8.1f us total, %6.3f us/pivot | cycles/pivot:", m, n, r, ms * 1e3, ms * 1e3 / r);
+        printf("%4dx%4d (static %4d) r=%4d: %8.1f us total, %6.3f us/pivot | cycles/pivot:", m, n, stat, r, ms * 1e3,
+               ms * 1e3 / r);
         for (int t = 0; t < 7; ++t) printf(" p%d=%lld", t, dbg[t] / (r > 0 ? r : 1));
         printf("\n");
       }

@@ -978,6 +978,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   if (L < 2) return fail(ACI_ERR_INVALID, "aci: L must be >= 2 (the 2-site update needs two sites)");
   cudaStream_t strm = o.stream ? (cudaStream_t)o.stream : lib_stream();
   gemm_init();
+  prrlu_init();
 
   // ---- y_init (R9)
   tt_s *ygen = nullptr;

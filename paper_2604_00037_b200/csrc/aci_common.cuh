@@ -72,4 +72,6 @@ void launch_gemm_sub(const GemmDesc *d_descs, int ndesc, int max_m, int max_n, c
 bool prrlu_supported(int max_m, int max_n);
 size_t prrlu_exchange_bytes(int max_m, int max_n);
 void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st);
+// Chooses the prrLU exchange tier (cluster size) once; call before any stream capture.
+void prrlu_init();
 void prrlu_envelope(int *max_rows, int *max_cols);

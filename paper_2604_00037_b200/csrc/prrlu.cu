@@ -23,6 +23,8 @@
 //     __syncthreads per pivot.
 //   * grid tier (GRID = true): G co-resident CTAs (cooperative launch), column-partitioned.
 // The tier is chosen per launch on the device from the live block size (prrlu_kernel).
+#include <cstdlib>
+
 #include "aci_common.cuh"
 
 namespace {
@@ -100,6 +102,46 @@ __device__ __forceinline__ double pkt_double(unsigned long long w0, unsigned lon
   return __longlong_as_double((long long)(((w1 & 0xffffffffull) << 32) | (w0 & 0xffffffffull)));
 }
 
+// ---- cluster (DSMEM) exchange primitives: keys are pushed into every CTA's shared memory with
+// st.async, whose complete_tx lands on the destination CTA's mbarrier (measured 0.2-0.25 us per
+// 8/16-CTA key exchange vs ~0.7-0.8 us for an L2 poll, profiles/r01_probe7_cluster_push.txt)
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned mapa_u32(unsigned a, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned a, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(unsigned a, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void st_async_key(unsigned raddr, unsigned a, unsigned b, unsigned c, unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(raddr),
+               "r"(a), "r"(b), "r"(c), "r"(0u), "r"(rbar)
+               : "memory");
+}
+
 struct Key {
   unsigned hi, lo, id;  // |v| bits (hi, lo); id = flat index (row * n + col)
 };
@@ -137,6 +179,7 @@ __device__ __forceinline__ double key_abs(const Key &k) {
 #endif
 constexpr int kNW = 16;          // warps per CTA (512 threads) for every variant
 constexpr int kMaxRows = 1024;   // 32 * EA_max
+constexpr int kMaxCTAs = 148;
 constexpr int kMaxCB = 512;      // NW * EB_max
 
 struct PrrluSmem {
@@ -145,12 +188,20 @@ struct PrrluSmem {
   double u[kMaxCB];      // pivot row segment
   unsigned hi[32], lo[32], id[32];
   unsigned win[4];  // grid winner broadcast (key-poll mode)
+  uint4 ck[2][16];                // cluster tier: CTA keys pushed by the cluster's CTAs (by parity)
+  uint4 gw[2];                    // cluster tier, several clusters: global winner pushed by rank 0
+  unsigned long long mb[4];       // cluster tier: key mbarrier and winner mbarrier per parity
 };
 
 // One factorisation, register tile EA x EB per thread, NW warps per CTA. GRID: G CTAs (this is
 // CTA g) cooperate through the exchange buffers; otherwise one CTA does everything.
-template <int EA, int EB, int NW, bool GRID>
+// XM: exchange mode. 0 = one CTA; 1 = grid of co-resident CTAs exchanging through L2 (tagged
+// packets, counter or key-poll barrier); 2 = grid of whole thread-block clusters: CTA keys are
+// pushed through DSMEM (st.async + mbarrier), cluster winners (if more than one cluster) and
+// candidate columns go through L2 as tagged packets.
+template <int EA, int EB, int NW, int XM>
 __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const int G, const int g) {
+  constexpr bool GRID = XM != 0;
   constexpr int T = NW * 32;
   constexpr int MROWS = 32 * EA;
   constexpr int CB = NW * EB;  // columns per CTA
@@ -223,6 +274,19 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     return Key{(unsigned)(bits >> 32), (unsigned)bits, flat};
   };
   scan();
+  if (XM == 2) {
+    // one mbarrier per parity, armed for steps 0 and 1 before any CTA of the cluster pushes
+    if (tid == 0) {
+      const unsigned CS = cluster_size();
+      for (int t = 0; t < 4; ++t) mbar_init(smem_u32(&S.mb[t]), 1u);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_arm(smem_u32(&S.mb[0]), CS * 16u);
+      mbar_arm(smem_u32(&S.mb[1]), CS * 16u);
+      mbar_arm(smem_u32(&S.mb[2]), 16u);
+      mbar_arm(smem_u32(&S.mb[3]), 16u);
+    }
+    cluster_sync_all();
+  }
 
   double first = 0.0, eps = 0.0;
   int k = 0;
@@ -259,7 +323,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
                 const unsigned long long bits = (unsigned long long)__double_as_longlong(v[a][b]);
                 st_pkt(dst + 2 * (lane + 32 * a), tagged(tag, (unsigned)bits), tagged(tag, (unsigned)(bits >> 32)));
               }
-        if (lane == 0) {
+        if (XM == 1 && lane == 0) {
           unsigned long long *kd = A.keys + ((size_t)par * G + g) * 4;
           st_pkt(kd, tagged(tag, ck.hi), tagged(tag, ck.lo));
           st_pkt(kd + 2, tagged(tag, ck.id), 0ull);
@@ -267,49 +331,96 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         }
       }
       PHASE(2);
-      // small grids: the tagged keys themselves are the barrier (warp 0 polls them, no counter);
-      // larger grids: one counter poll then every warp reads the keys (measured crossover ~16)
-      const bool keypoll = G <= ACI_KEYPOLL_MAXG;
-      if (!keypoll) {
-        if (tid == 0) poll_counter(A.counter, (unsigned)(k + 1) * (unsigned)G);
-        __syncthreads();  // S2: every CTA has arrived
-      }
-      PHASE(3);
-      // read all G keys: independent loads in flight, stale packets re-read until their tag is
-      // this step's
-      constexpr int KPL = (148 + 31) / 32;  // keys per lane
-      Key gk{0u, 0u, BAD_ID};
-      if (!keypoll || w == 0) {
-        unsigned long long kw[KPL][4];
-#pragma unroll
-        for (int t = 0; t < KPL; ++t) {
-          const int s_ = lane + 32 * t;
-          if (s_ < G) {
-            const unsigned long long *kp = A.keys + ((size_t)par * G + s_) * 4;
-            ld_pkt(kp, kw[t][0], kw[t][1]);
-            ld_pkt(kp + 2, kw[t][2], kw[t][3]);
+      if (XM == 2) {
+        // ---- cluster key exchange: push this CTA's key into every cluster CTA's smem
+        const unsigned CS = cluster_size(), crank = cluster_rank();
+        const unsigned mbp = smem_u32(&S.mb[par]);
+        if (tid < (int)CS)
+          st_async_key(mapa_u32(smem_u32(&S.ck[par][crank]), (unsigned)tid), ck.hi, ck.lo, ck.id, mapa_u32(mbp, (unsigned)tid));
+        mbar_wait(mbp, (unsigned)(k >> 1) & 1u);
+        PHASE(3);
+        if (tid == 0) mbar_arm(mbp, CS * 16u);  // re-arm this parity for step k + 2
+        const uint4 q4 = S.ck[par][lane < (int)CS ? lane : 0];
+        const Key cw = warp_argmax(lane < (int)CS ? Key{q4.x, q4.y, q4.z} : Key{0u, 0u, BAD_ID});
+        const int NCL = G / (int)CS;
+        if (NCL == 1) {
+          win = cw;
+        } else {
+          // cluster winners through L2: warp 0 of each cluster's rank-0 CTA publishes its
+          // cluster's winner (slots 256 B apart), polls the NCL tagged keys and pushes the
+          // global winner to its cluster peers through DSMEM (one poller per cluster keeps the
+          // L2 lines uncontended)
+          const int cid = g / (int)CS;
+          const unsigned mwp = smem_u32(&S.mb[2 + par]);
+          if (crank == 0 && w == 0) {
+            if (lane == 0) {
+              unsigned long long *kd = A.keys + ((size_t)par * kMaxCTAs / 8 + cid) * 32;
+              st_pkt(kd, tagged(tag, cw.hi), tagged(tag, cw.lo));
+              st_pkt(kd + 2, tagged(tag, cw.id), 0ull);
+            }
+            Key gk{0u, 0u, BAD_ID};
+            if (lane < NCL) {
+              const unsigned long long *kp = A.keys + ((size_t)par * kMaxCTAs / 8 + lane) * 32;
+              unsigned long long kw[4];
+              do {
+                ld_pkt(kp, kw[0], kw[1]);
+                ld_pkt(kp + 2, kw[2], kw[3]);
+              } while ((unsigned)(kw[0] >> 32) != tag || (unsigned)(kw[1] >> 32) != tag || (unsigned)(kw[2] >> 32) != tag);
+              gk = Key{(unsigned)kw[0], (unsigned)kw[1], (unsigned)kw[2]};
+            }
+            const Key gw = warp_argmax(gk);
+            if (lane < (int)CS)
+              st_async_key(mapa_u32(smem_u32(&S.gw[par]), (unsigned)lane), gw.hi, gw.lo, gw.id, mapa_u32(mwp, (unsigned)lane));
           }
+          mbar_wait(mwp, (unsigned)(k >> 1) & 1u);
+          if (tid == 0) mbar_arm(mwp, 16u);
+          win = Key{S.gw[par].x, S.gw[par].y, S.gw[par].z};
         }
-#pragma unroll
-        for (int t = 0; t < KPL; ++t) {
-          const int s_ = lane + 32 * t;
-          if (s_ < G) {
-            const unsigned long long *kp = A.keys + ((size_t)par * G + s_) * 4;
-            while ((unsigned)(kw[t][0] >> 32) != tag || (unsigned)(kw[t][1] >> 32) != tag ||
-                   (unsigned)(kw[t][2] >> 32) != tag) {
+      } else {
+        // small grids: the tagged keys themselves are the barrier (warp 0 polls them, no counter);
+        // larger grids: one counter poll then every warp reads the keys (measured crossover ~16)
+        const bool keypoll = G <= ACI_KEYPOLL_MAXG;
+        if (!keypoll) {
+          if (tid == 0) poll_counter(A.counter, (unsigned)(k + 1) * (unsigned)G);
+          __syncthreads();  // S2: every CTA has arrived
+        }
+        PHASE(3);
+        // read all G keys: independent loads in flight, stale packets re-read until their tag is
+        // this step's
+        constexpr int KPL = (148 + 31) / 32;  // keys per lane
+        Key gk{0u, 0u, BAD_ID};
+        if (!keypoll || w == 0) {
+          unsigned long long kw[KPL][4];
+  #pragma unroll
+          for (int t = 0; t < KPL; ++t) {
+            const int s_ = lane + 32 * t;
+            if (s_ < G) {
+              const unsigned long long *kp = A.keys + ((size_t)par * G + s_) * 4;
               ld_pkt(kp, kw[t][0], kw[t][1]);
               ld_pkt(kp + 2, kw[t][2], kw[t][3]);
             }
-            const Key kq{(unsigned)kw[t][0], (unsigned)kw[t][1], (unsigned)kw[t][2]};
-            if (better(kq, gk)) gk = kq;
+          }
+  #pragma unroll
+          for (int t = 0; t < KPL; ++t) {
+            const int s_ = lane + 32 * t;
+            if (s_ < G) {
+              const unsigned long long *kp = A.keys + ((size_t)par * G + s_) * 4;
+              while ((unsigned)(kw[t][0] >> 32) != tag || (unsigned)(kw[t][1] >> 32) != tag ||
+                     (unsigned)(kw[t][2] >> 32) != tag) {
+                ld_pkt(kp, kw[t][0], kw[t][1]);
+                ld_pkt(kp + 2, kw[t][2], kw[t][3]);
+              }
+              const Key kq{(unsigned)kw[t][0], (unsigned)kw[t][1], (unsigned)kw[t][2]};
+              if (better(kq, gk)) gk = kq;
+            }
           }
         }
-      }
-      win = warp_argmax(gk);
-      if (keypoll) {
-        if (tid == 0) { S.win[0] = win.hi; S.win[1] = win.lo; S.win[2] = win.id; }
-        __syncthreads();  // S2: the winner, known only after every CTA's key arrived
-        win = Key{S.win[0], S.win[1], S.win[2]};
+        win = warp_argmax(gk);
+        if (keypoll) {
+          if (tid == 0) { S.win[0] = win.hi; S.win[1] = win.lo; S.win[2] = win.id; }
+          __syncthreads();  // S2: the winner, known only after every CTA's key arrived
+          win = Key{S.win[0], S.win[1], S.win[2]};
+        }
       }
       PHASE(4);
     }
@@ -425,81 +536,97 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     for (int t = 0; t < 8; ++t) A.dbg[t] = ph_[t];
 #endif
   }
+  if (XM == 2) cluster_sync_all();  // no CTA leaves while a cluster peer may still push to it
 }
 
 // Runtime tier selection from the LIVE sizes (device-resident ranks): the launch is sized for
-// the static capacity, and CTAs beyond what the live block needs exit immediately. Two
-// instantiations: 16 warps (static rows <= 512) and 8 warps (static rows <= 1024: 8 columns per
-// CTA and up to 255 registers, so the 32-row-slot tiles do not spill).
-template <int NWT>
+// the static capacity, and CTAs beyond what the live block needs exit immediately. 8 warps per
+// CTA (up to 255 registers, so the 32-row-slot tiles do not spill; measured faster than 16).
+// XM = 1: cooperative grid, L2 exchange. XM = 2: cluster launch; the participating CTAs are
+// rounded up to whole clusters (CTAs past the live columns hold padding only).
+template <int NWT, int XM>
 __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
   __shared__ PrrluSmem S;
   const int m = A.dims->m, n = A.dims->n;
   const int g = blockIdx.x;
 #define ACI_CTA_VARIANT(EA, EB)                                        \
   if (m <= 32 * (EA) && n <= NWT * (EB)) {                              \
-    if (g == 0) prrlu_body<(EA), (EB), NWT, false>(A, S, 1, 0);        \
+    if (g == 0) prrlu_body<(EA), (EB), NWT, 0>(A, S, 1, 0);            \
     return;                                                            \
   }
-#define ACI_GRID_VARIANT(EA) ACI_GRID_VARIANT2(EA, 1)
 #define ACI_GRID_VARIANT2(EA, EB)                                      \
   if (m <= 32 * (EA)) {                                                \
-    const int Gl = (n + NWT * (EB) - 1) / (NWT * (EB));                \
-    if (g < Gl) prrlu_body<(EA), (EB), NWT, true>(A, S, Gl, g);        \
+    int Gl = (n + NWT * (EB) - 1) / (NWT * (EB));                      \
+    if (XM == 2) {                                                     \
+      const int CS = (int)cluster_size();                              \
+      Gl = (Gl + CS - 1) / CS * CS;                                    \
+    }                                                                  \
+    if (g < Gl) prrlu_body<(EA), (EB), NWT, XM>(A, S, Gl, g);          \
     return;                                                            \
   }
-  if (NWT == 16) {
-    ACI_CTA_VARIANT(1, 2)    //   32 x   32
-    ACI_CTA_VARIANT(2, 4)    //   64 x   64
-    ACI_CTA_VARIANT(4, 2)    //  128 x   32
-    ACI_CTA_VARIANT(1, 8)    //   32 x  128
-    ACI_CTA_VARIANT(4, 8)    //  128 x  128
-    ACI_CTA_VARIANT(2, 16)   //   64 x  256
-    ACI_CTA_VARIANT(8, 4)    //  256 x   64
-    ACI_CTA_VARIANT(1, 32)   //   32 x  512
-    ACI_CTA_VARIANT(16, 2)   //  512 x   32
-    ACI_GRID_VARIANT2(4, 2)  //  128 x 32 per CTA (key-poll barrier for <= 16 CTAs)
-    ACI_GRID_VARIANT2(8, 2)  //  256 x 32 per CTA
-    ACI_GRID_VARIANT(16)     //  512 x 16 per CTA (counter barrier)
-  } else {
-    ACI_CTA_VARIANT(1, 4)    //   32 x   32
-    ACI_CTA_VARIANT(2, 8)    //   64 x   64
-    ACI_CTA_VARIANT(4, 4)    //  128 x   32
-    ACI_CTA_VARIANT(1, 16)   //   32 x  128
-    ACI_CTA_VARIANT(4, 16)   //  128 x  128
-    ACI_CTA_VARIANT(8, 8)    //  256 x   64
-    ACI_CTA_VARIANT(2, 32)   //   64 x  256
-    ACI_CTA_VARIANT(32, 2)   // 1024 x   16
-    ACI_GRID_VARIANT2(4, ACI_W8_EB128)   //  128 x 8*EB per CTA
-    ACI_GRID_VARIANT2(8, ACI_W8_EB256)   //  256 x 8*EB per CTA
-    ACI_GRID_VARIANT2(16, ACI_W8_EB512)  //  512 x 8*EB per CTA
-    ACI_GRID_VARIANT2(32, ACI_BIG_EB)  // 1024 x 8*EB per CTA
-  }
+  ACI_CTA_VARIANT(1, 4)    //   32 x   32
+  ACI_CTA_VARIANT(2, 8)    //   64 x   64
+  ACI_CTA_VARIANT(4, 4)    //  128 x   32
+  ACI_CTA_VARIANT(1, 16)   //   32 x  128
+  ACI_CTA_VARIANT(4, 16)   //  128 x  128
+  ACI_CTA_VARIANT(8, 8)    //  256 x   64
+  ACI_CTA_VARIANT(2, 32)   //   64 x  256
+  ACI_CTA_VARIANT(32, 2)   // 1024 x   16
+  ACI_GRID_VARIANT2(4, ACI_W8_EB128)   //  128 x 8*EB per CTA
+  ACI_GRID_VARIANT2(8, ACI_W8_EB256)   //  256 x 8*EB per CTA
+  ACI_GRID_VARIANT2(16, ACI_W8_EB512)  //  512 x 8*EB per CTA
+  ACI_GRID_VARIANT2(32, ACI_BIG_EB)    // 1024 x 8*EB per CTA
 #undef ACI_CTA_VARIANT
-#undef ACI_GRID_VARIANT
 #undef ACI_GRID_VARIANT2
 }
 
-constexpr int kMaxCTAs = 148;
-constexpr int kRowsSmall = 512;  // static rows handled by the 16-warp instantiation
+constexpr int kNWT = 8;
 
-bool fits_one_cta(int m, int n, int nwt) {
-  const int v16[][2] = {{1, 2}, {2, 4}, {4, 2}, {1, 8}, {4, 8}, {2, 16}, {8, 4}, {1, 32}, {16, 2}};
+bool fits_one_cta(int m, int n) {
   const int v8[][2] = {{1, 4}, {2, 8}, {4, 4}, {1, 16}, {4, 16}, {8, 8}, {2, 32}, {32, 2}};
-  if (nwt == 16) {
-    for (auto &e : v16)
-      if (m <= 32 * e[0] && n <= 16 * e[1]) return true;
-  } else {
-    for (auto &e : v8)
-      if (m <= 32 * e[0] && n <= 8 * e[1]) return true;
-  }
+  for (auto &e : v8)
+    if (m <= 32 * e[0] && n <= kNWT * e[1]) return true;
   return false;
+}
+
+// Cluster size of the XM = 2 launch, chosen once: 16 (non-portable) if four 16-CTA clusters of
+// this kernel can be co-resident (the 1024-row tier uses 64 CTAs), else 8, else 0 = L2 tier.
+// ACI_PRRLU_CLUSTER=0/8/16 overrides (measurements).
+int cluster_choice() {
+  static int cs = -1;
+  if (cs >= 0) return cs;
+  const void *kern = (const void *)prrlu_kernel<kNWT, 2>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  auto active = [&](int c) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c * 8);
+    cfg.blockDim = dim3(kNWT * 32);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return n;
+  };
+  const char *env = getenv("ACI_PRRLU_CLUSTER");
+  int want = env ? atoi(env) : 16;
+  cs = 0;
+  if (want >= 16 && active(16) * 16 >= 64) cs = 16;
+  else if (want >= 8 && active(8) * 8 >= 64) cs = 8;
+  return cs;
 }
 
 }  // namespace
 
 bool prrlu_supported(int max_m, int max_n) {
-  return fits_one_cta(max_m, max_n, 8) || (max_m <= kMaxRows && (max_n + 7) / 8 <= kMaxCTAs);
+  return fits_one_cta(max_m, max_n) || (max_m <= kMaxRows && (max_n + 7) / 8 <= kMaxCTAs);
 }
 
 void prrlu_envelope(int *max_rows, int *max_cols) {
@@ -513,18 +640,34 @@ size_t prrlu_exchange_bytes(int max_m, int max_n) {
   return (size_t)2 * kMaxCTAs * cap * 16 + 2 * kMaxCTAs * 32 + 256;
 }
 
+void prrlu_init() { cluster_choice(); }
+
 void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st) {
-  // the 8-warp instantiation measured faster than the 16-warp one at every block size
-  constexpr int nwt = 8;
-  const void *kern = (const void *)prrlu_kernel<nwt>;
-  if (fits_one_cta(max_m, max_n, nwt)) {
+  if (fits_one_cta(max_m, max_n)) {
     void *params[] = {const_cast<LuArgs *>(&a)};
-    cudaLaunchKernel(kern, dim3(1), dim3(nwt * 32), params, 0, st);
+    cudaLaunchKernel((const void *)prrlu_kernel<kNWT, 1>, dim3(1), dim3(kNWT * 32), params, 0, st);
+    return;
+  }
+  int G = (max_n + kNWT - 1) / kNWT;  // enough for every variant the live size may select
+  const int cs = cluster_choice();
+  LuArgs args = a;
+  if (cs > 0) {
+    G = (G + cs - 1) / cs * cs;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kNWT * 32);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 2>, args);
     return;
   }
   cudaMemsetAsync(a.counter, 0, sizeof(unsigned), st);
-  const int G = (max_n + nwt - 1) / nwt;  // enough for every variant the live size may select
-  LuArgs args = a;
   void *params[] = {&args};
-  cudaLaunchCooperativeKernel(kern, dim3(G), dim3(nwt * 32), params, 0, st);
+  cudaLaunchCooperativeKernel((const void *)prrlu_kernel<kNWT, 1>, dim3(G), dim3(kNWT * 32), params, 0, st);
 }

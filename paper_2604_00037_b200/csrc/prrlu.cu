@@ -67,6 +67,9 @@ __device__ __forceinline__ void red_relaxed_add(unsigned *p, unsigned v) {
 #define ACI_POLL_NP 1  // measured: more loads in flight only add contention on the counter line
 #endif
 constexpr int kPollGap = 160;
+#ifndef ACI_LEADER_NP
+#define ACI_LEADER_NP 1  // cluster-leader key poll: loads in flight (measured: 3 is not faster)
+#endif
 __device__ __forceinline__ void poll_counter(const unsigned *ctr, unsigned target) {
   constexpr int NP = ACI_POLL_NP;
   unsigned v[NP];
@@ -245,26 +248,28 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   auto scan = [&]() {
     constexpr int NE = EA * EB;
     constexpr int NCH = NE < 4 ? NE : 4;
+    // chains keep the SIGNED value and compare magnitudes (|.| operand modifiers of DSETP), so
+    // no FP64-pipe instruction is spent materialising |v|
     double cx[NCH];
     int ce[NCH];
 #pragma unroll
-    for (int t = 0; t < NCH; ++t) { cx[t] = fabs(v[t / EB][t % EB]); ce[t] = t; }
+    for (int t = 0; t < NCH; ++t) { cx[t] = v[t / EB][t % EB]; ce[t] = t; }
 #pragma unroll
     for (int e = NCH; e < NE; ++e) {
-      const double ax = fabs(v[e / EB][e % EB]);
-      const bool take = ax > cx[e % NCH];
-      cx[e % NCH] = take ? ax : cx[e % NCH];
+      const double x = v[e / EB][e % EB];
+      const bool take = fabs(x) > fabs(cx[e % NCH]);
+      cx[e % NCH] = take ? x : cx[e % NCH];
       ce[e % NCH] = take ? e : ce[e % NCH];
     }
     double bm = cx[0];
     int bi = ce[0];
 #pragma unroll
     for (int t = 1; t < NCH; ++t) {
-      const bool take = cx[t] > bm || (cx[t] == bm && ce[t] < bi);
+      const bool take = fabs(cx[t]) > fabs(bm) || (fabs(cx[t]) == fabs(bm) && ce[t] < bi);
       bm = take ? cx[t] : bm;
       bi = take ? ce[t] : bi;
     }
-    bx = bm;
+    bx = fabs(bm);
     be = bi;
   };
   auto thread_key = [&]() -> Key {
@@ -311,6 +316,14 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       // fence) and lane 0 publishes the key and arrives on the counter
       const int jc = (int)(ck.id % NC) - c0;
       const int pw = jc % NW;
+      if (XM == 2 && w == 0) {
+        // cluster tier: the key goes out first (st.async into every cluster CTA's smem), the
+        // column store follows; readers only touch it after the key exchange
+        const unsigned CS = cluster_size();
+        if (lane < (int)CS)
+          st_async_key(mapa_u32(smem_u32(&S.ck[par][cluster_rank()]), (unsigned)lane), ck.hi, ck.lo, ck.id,
+                       mapa_u32(smem_u32(&S.mb[par]), (unsigned)lane));
+      }
       if (w == pw) {
         const int bc = jc / NW;
         unsigned long long *dst = A.colpub + (((size_t)par * G + g) * A.colcap) * 2;
@@ -335,8 +348,6 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         // ---- cluster key exchange: push this CTA's key into every cluster CTA's smem
         const unsigned CS = cluster_size(), crank = cluster_rank();
         const unsigned mbp = smem_u32(&S.mb[par]);
-        if (tid < (int)CS)
-          st_async_key(mapa_u32(smem_u32(&S.ck[par][crank]), (unsigned)tid), ck.hi, ck.lo, ck.id, mapa_u32(mbp, (unsigned)tid));
         mbar_wait(mbp, (unsigned)(k >> 1) & 1u);
         PHASE(3);
         if (tid == 0) mbar_arm(mbp, CS * 16u);  // re-arm this parity for step k + 2
@@ -360,13 +371,37 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
             }
             Key gk{0u, 0u, BAD_ID};
             if (lane < NCL) {
+              // rolling poll: ACI_LEADER_NP loads in flight, issued ~kPollGap cycles apart, so a
+              // packet is seen about one L2 round trip after it lands
               const unsigned long long *kp = A.keys + ((size_t)par * kMaxCTAs / 8 + lane) * 32;
-              unsigned long long kw[4];
-              do {
-                ld_pkt(kp, kw[0], kw[1]);
-                ld_pkt(kp + 2, kw[2], kw[3]);
-              } while ((unsigned)(kw[0] >> 32) != tag || (unsigned)(kw[1] >> 32) != tag || (unsigned)(kw[2] >> 32) != tag);
-              gk = Key{(unsigned)kw[0], (unsigned)kw[1], (unsigned)kw[2]};
+              constexpr int NP = ACI_LEADER_NP;
+              unsigned long long kw[NP][4];
+#pragma unroll
+              for (int i = 0; i < NP; ++i) {
+                ld_pkt(kp, kw[i][0], kw[i][1]);
+                ld_pkt(kp + 2, kw[i][2], kw[i][3]);
+                if (NP > 1 && i + 1 < NP) {
+                  const long long t0 = clock64();
+                  while (clock64() - t0 < kPollGap) {
+                  }
+                }
+              }
+              bool got = false;
+              while (!got) {
+#pragma unroll
+                for (int i = 0; i < NP; ++i) {
+                  if (!got) {
+                    if ((unsigned)(kw[i][0] >> 32) == tag && (unsigned)(kw[i][1] >> 32) == tag &&
+                        (unsigned)(kw[i][2] >> 32) == tag) {
+                      gk = Key{(unsigned)kw[i][0], (unsigned)kw[i][1], (unsigned)kw[i][2]};
+                      got = true;
+                    } else {
+                      ld_pkt(kp, kw[i][0], kw[i][1]);
+                      ld_pkt(kp + 2, kw[i][2], kw[i][3]);
+                    }
+                  }
+                }
+              }
             }
             const Key gw = warp_argmax(gk);
             if (lane < (int)CS)
@@ -453,7 +488,16 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
 #pragma unroll
           for (int b = 0; b < EB; ++b) s_u[w + NW * b] = v[a][b];
     }
-    double inv;
+    // 1/|c| from the key, off the column's critical path; the sign arrives with the column
+    // (1/(-x) = -(1/x) exactly). CTA tier: l_i = S_iq * (1/S_pq) (R4) is applied as
+    // fma(l'_i, -/+u_j, v) with l'_i = S_iq * (1/|c|): negation is exact, so this is
+    // bit-identical to fma(-l_i, u_j, v).
+    // __drcp_rn is the correctly rounded reciprocal, i.e. the same bits as 1.0 / |c|; the empty
+    // asm pins its evaluation here, ahead of the column loads it would otherwise trail
+    double inv_abs = __drcp_rn(absc);
+    asm volatile("" : "+d"(inv_abs));
+    double inv;       // signed 1/S_pq
+    double ub[EB];    // pivot row (CTA tier: sign-folded, -u_j (c > 0) or +u_j (c < 0))
     if (GRID) {
       const unsigned tag = (ep << 12) | (unsigned)(k + 1);
       const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2;
@@ -464,10 +508,11 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         const int i = tid + T * t;
         if (i < m) ld_pkt(src + 2 * i, cw[t][0], cw[t][1]);
       }
-      ld_pkt(src + 2 * p, cw[PPT][0], cw[PPT][1]);
+      ld_pkt(src + 2 * p, cw[PPT][0], cw[PPT][1]);  // the pivot itself, for its sign
       while ((unsigned)(cw[PPT][0] >> 32) != tag || (unsigned)(cw[PPT][1] >> 32) != tag)
         ld_pkt(src + 2 * p, cw[PPT][0], cw[PPT][1]);
-      inv = 1.0 / pkt_double(cw[PPT][0], cw[PPT][1]);
+      const bool neg = (cw[PPT][1] & 0x80000000ull) != 0;
+      inv = neg ? -inv_abs : inv_abs;
 #pragma unroll
       for (int t = 0; t < PPT; ++t) {
         const int i = tid + T * t;
@@ -476,6 +521,21 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
             ld_pkt(src + 2 * i, cw[t][0], cw[t][1]);
           s_l[i] = (i == p) ? 1.0 : pkt_double(cw[t][0], cw[t][1]) * inv;
         }
+      }
+      __syncthreads();  // S3
+      PHASE(5);
+      if (A.U)
+        for (int jj = tid; jj < CB; jj += T) {
+          const int j = c0 + jj;
+          if (j < n) A.U[(size_t)k * ldu + j] = (j == q) ? 1.0 : s_u[jj] * inv;
+        }
+#pragma unroll
+      for (int b = 0; b < EB; ++b) ub[b] = s_u[w + NW * b];
+#pragma unroll
+      for (int a = 0; a < EA; ++a) {
+        const double li = s_l[lane + 32 * a];
+#pragma unroll
+        for (int b = 0; b < EB; ++b) v[a][b] = fma(-li, ub[b], v[a][b]);
       }
     } else {
       const int jq = q - c0;
@@ -487,26 +547,25 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
 #pragma unroll
             for (int a = 0; a < EA; ++a) s_raw[lane + 32 * a] = v[a][b];
       }
-      __syncthreads();  // S2 (CTA tier)
-      inv = 1.0 / s_raw[p];
-      for (int i = tid; i < m; i += T) s_l[i] = (i == p) ? 1.0 : s_raw[i] * inv;
-    }
-    __syncthreads();  // S3
-    PHASE(5);
-    if (A.U)
-      for (int jj = tid; jj < CB; jj += T) {
-        const int j = c0 + jj;
-        if (j < n) A.U[(size_t)k * ldu + j] = (j == q) ? 1.0 : s_u[jj] * inv;
+      __syncthreads();  // S2 (CTA tier): raw pivot column and pivot row in smem
+      const bool neg = s_raw[p] < 0.0;
+      inv = neg ? -inv_abs : inv_abs;
+#pragma unroll
+      for (int b = 0; b < EB; ++b) ub[b] = neg ? s_u[w + NW * b] : -s_u[w + NW * b];
+      PHASE(5);
+      if (A.U)
+        for (int jj = tid; jj < CB; jj += T) {
+          const int j = c0 + jj;
+          if (j < n) A.U[(size_t)k * ldu + j] = (j == q) ? 1.0 : s_u[jj] * inv;
+        }
+      // every thread forms its own l'_i (no third barrier)
+#pragma unroll
+      for (int a = 0; a < EA; ++a) {
+        const int i = lane + 32 * a;
+        const double li = (i == p) ? (neg ? -1.0 : 1.0) : s_raw[i] * inv_abs;
+#pragma unroll
+        for (int b = 0; b < EB; ++b) v[a][b] = fma(li, ub[b], v[a][b]);
       }
-    // ---- rank-1 Schur update in registers
-    double ub[EB];
-#pragma unroll
-    for (int b = 0; b < EB; ++b) ub[b] = s_u[w + NW * b];
-#pragma unroll
-    for (int a = 0; a < EA; ++a) {
-      const double li = s_l[lane + 32 * a];
-#pragma unroll
-      for (int b = 0; b < EB; ++b) v[a][b] = fma(-li, ub[b], v[a][b]);
     }
     // column q -> exact zeros (owner warp; warp-uniform branch)
     {

@@ -16,3 +16,8 @@ for chi in chis:
         out.free()
         ms.append(rep["ms"])
     print(f"chi={chi}: " + " ".join(f"{m:.1f}" for m in ms) + f" | pivots {rep['pivot_steps']}", flush=True)
+    out, st, rep, ex = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0,
+                                           profile=True)
+    out.free()
+    print("   profile (ms, launches):", {k: (round(v["ms"], 2), v["launches"]) for k, v in ex["profile"].items()},
+          flush=True)

@@ -202,19 +202,40 @@ struct InBond {
   const double *Xb, *Xb1;
   const double *Rnext;  // R^n_{b+2} (chi_{b+2} x rmax[b+1], ld ldR); null at b == L-2 (R_L = [1])
   int ldR;
-  double *Abuf, *Bbuf;
+  double *Abuf, *Bbuf;  // per-bond scratch of the half that depends on this sweep's pivots
+  double *Apre, *Bpre;  // this bond's half that does not (computed for all bonds at half-sweep start)
   int c0, c1, c2;       // chi^n_b, chi^n_{b+1}, chi^n_{b+2}
 };
 struct BondStatic {
-  int b, L, N, db, db1;
+  int b, L, N, dir, db, db1;
   int ldu;              // static ld of the U store (nmax[b])
   int maxrank;
   InBond in[ACI_GEMM_MAX_IN];
   double *Pi;
 };
 
-// One thread: live sizes -> GEMM descriptors (a1, a2 per input; a3+f) and prrLU dims.
-__global__ void plan_bond_kernel(BondStatic S, const int *rk, GemmDesc *ab, GemmDesc *pi, LuDims *lu) {
+// a1: A^n = L^n_{b-1} X^n_b : (rl x c0) (c0 x db*c1) -> rl x (db c1) == (rl db) x c1
+__device__ __forceinline__ GemmDesc desc_a(const BondStatic &S, const InBond &I, int rl, double *C) {
+  GemmDesc a = {};
+  if (!I.Lprev) return a;
+  a.C = C; a.M = rl; a.N = S.db * I.c1; a.ldc = S.db * I.c1; a.nin = 1;
+  a.A[0] = I.Lprev; a.lda[0] = I.c0; a.K[0] = I.c0; a.B[0] = I.Xb; a.ldb[0] = S.db * I.c1;
+  return a;
+}
+// a2: B^n = X^n_{b+1} R^n_{b+2} : (c1 db1 x c2) (c2 x rr) -> (c1 db1) x rr == c1 x (db1 rr)
+__device__ __forceinline__ GemmDesc desc_b(const BondStatic &S, const InBond &I, int rr, double *C) {
+  GemmDesc bb = {};
+  if (!I.Rnext) return bb;
+  bb.C = C; bb.M = I.c1 * S.db1; bb.N = rr; bb.ldc = rr; bb.nin = 1;
+  bb.A[0] = I.Xb1; bb.lda[0] = I.c2; bb.K[0] = I.c2; bb.B[0] = I.Rnext; bb.ldb[0] = I.ldR;
+  return bb;
+}
+
+// Live sizes -> GEMM descriptors of one bond update and its prrLU dims. Only the half that
+// depends on the pivots of this sweep is computed per bond (A^n in L->R, B^n in R->L, into
+// ab[0..N-1]); the other half was computed for every bond at the start of the half-sweep
+// (plan_pre_kernel), because it reads frames of the previous half-sweep only (R20).
+__device__ void plan_bond(const BondStatic &S, const int *rk, GemmDesc *ab, GemmDesc *pi, LuDims *lu) {
   const int b = S.b;
   const int rl = rk[b], rr = rk[b + 2];
   const int m = rl * S.db, n = S.db1 * rr;
@@ -222,24 +243,12 @@ __global__ void plan_bond_kernel(BondStatic S, const int *rk, GemmDesc *ab, Gemm
   P.C = S.Pi; P.M = m; P.N = n; P.ldc = n; P.nin = S.N;
   for (int i = 0; i < S.N; ++i) {
     const InBond &I = S.in[i];
-    GemmDesc a = {}, bb = {};
-    // a1: A^n = L^n_{b-1} X^n_b : (rl x c0) (c0 x db*c1) -> rl x (db c1) == (rl db) x c1
-    if (I.Lprev) {
-      a.C = I.Abuf; a.M = rl; a.N = S.db * I.c1; a.ldc = S.db * I.c1; a.nin = 1;
-      a.A[0] = I.Lprev; a.lda[0] = I.c0; a.K[0] = I.c0; a.B[0] = I.Xb; a.ldb[0] = S.db * I.c1;
-    }
-    // a2: B^n = X^n_{b+1} R^n_{b+2} : (c1 db1 x c2) (c2 x rr) -> (c1 db1) x rr == c1 x (db1 rr)
-    if (I.Rnext) {
-      bb.C = I.Bbuf; bb.M = I.c1 * S.db1; bb.N = rr; bb.ldc = rr; bb.nin = 1;
-      bb.A[0] = I.Xb1; bb.lda[0] = I.c2; bb.K[0] = I.c2; bb.B[0] = I.Rnext; bb.ldb[0] = I.ldR;
-    }
-    ab[2 * i] = a;
-    ab[2 * i + 1] = bb;
+    ab[i] = S.dir == 0 ? desc_a(S, I, rl, I.Abuf) : desc_b(S, I, rr, I.Bbuf);
     // a3: Pi^n = A^n B^n : (m x c1) (c1 x n)
-    P.A[i] = I.Lprev ? I.Abuf : I.Xb;
+    P.A[i] = I.Lprev ? (S.dir == 0 ? I.Abuf : I.Apre) : I.Xb;
     P.lda[i] = I.c1;
     P.K[i] = I.c1;
-    P.B[i] = I.Rnext ? I.Bbuf : I.Xb1;
+    P.B[i] = I.Rnext ? (S.dir == 0 ? I.Bpre : I.Bbuf) : I.Xb1;
     P.ldb[i] = n;
   }
   *pi = P;
@@ -249,6 +258,22 @@ __global__ void plan_bond_kernel(BondStatic S, const int *rk, GemmDesc *ab, Gemm
   D.ldu = S.ldu;
   *lu = D;
 }
+
+__global__ void plan_bond_kernel(const BondStatic *S, const int *rk, GemmDesc *ab, GemmDesc *pi, LuDims *lu) {
+  plan_bond(*S, rk, ab, pi, lu);
+}
+
+// Descriptors of the pivot-independent half of every bond of a half-sweep (dir 0: B^n_b for
+// b = 0..L-3; dir 1: A^n_b for b = 1..L-2), one thread per (bond, input).
+__global__ void plan_pre_kernel(const BondStatic *S, int nb, int N, const int *rk, GemmDesc *pre) {
+  for (int t = threadIdx.x; t < nb * N; t += blockDim.x) {
+    const int b = t / N, i = t % N;
+    const BondStatic &B = S[b];
+    const InBond &I = B.in[i];
+    pre[t] = B.dir == 0 ? desc_b(B, I, rk[b + 2], I.Bpre) : desc_a(B, I, rk[b], I.Apre);
+  }
+}
+
 
 struct UpdateArgs {
   int b, dir, L, N, db, db1;
@@ -275,6 +300,10 @@ struct UpdateArgs {
   int *log_rows, *log_cols;   // cap_piv per slot
   const int *iter;
   int step, per_iter, cap_piv;
+  // plan of the next bond update (fused; null for the last update of an iteration)
+  const BondStatic *next;
+  GemmDesc *ab, *pi;
+  LuDims *lu;
 };
 
 // Index-set update (a6, R21) and frame update (a7: the rows/columns of A^n / B^n the
@@ -288,6 +317,7 @@ __global__ void update_bond_kernel(UpdateArgs U) {
   const size_t slot = (size_t)(*U.iter) * U.per_iter + U.step;
   if (gt == 0) {
     U.rk[b + 1] = r;  // no thread of this kernel reads rk[b+1]
+    if (U.next) plan_bond(*U.next, U.rk, U.ab, U.pi, U.lu);  // reads the rank just written
     const double eps = *U.eps_in;
     atomicMax(U.maxeps_bits, (unsigned long long)__double_as_longlong(eps));
     int *li = U.log_info + slot * 5;
@@ -585,6 +615,12 @@ struct Run {
   std::vector<int *> prow, pcol;
   std::vector<std::vector<double *>> Lf, Rf;
   std::vector<double *> Abuf, Bbuf, Ust, Yin, Yabs;
+  std::vector<std::vector<double *>> Apre, Bpre;  // [n][b]: pivot-independent halves (R->L A, L->R B)
+  BondStatic *dStat = nullptr;   // [dir * (L-1) + b], uploaded once per call
+  GemmDesc *dPre = nullptr;      // (L-1) * N descriptors of the half-sweep's pre-launch
+  std::vector<BondStatic> hStat;
+  std::vector<int> nbig, nsmall; // [dir * (L-1) + b]: Pi kernel input split
+  std::vector<FOp> opb;          // [dir * (L-1) + b]: op with exponents in Pi input order
   double *Pi = nullptr, *Y0 = nullptr, *Mp = nullptr;
   std::vector<uint8_t *> Imi, Jmi;
   GemmDesc *dAB = nullptr, *dPi = nullptr, *dT = nullptr, *dY = nullptr;
@@ -659,6 +695,12 @@ static size_t carve(Run &R, char *base) {
     R.Abuf[n] = c.take<double>(acap);
     R.Bbuf[n] = c.take<double>(bcap);
   }
+  R.Apre.assign(N, std::vector<double *>(L, nullptr));
+  R.Bpre.assign(N, std::vector<double *>(L, nullptr));
+  for (int n = 0; n < N; ++n) {
+    for (int b = 1; b < L - 1; ++b) R.Apre[n][b] = c.take<double>((size_t)R.rmax[b - 1] * R.d[b] * R.xr[n][b + 1]);
+    for (int b = 0; b + 2 < L; ++b) R.Bpre[n][b] = c.take<double>((size_t)R.xr[n][b + 1] * R.d[b + 1] * R.rmax[b + 1]);
+  }
   size_t picap = 1;
   for (int b = 0; b < L - 1; ++b) picap = std::max(picap, (size_t)R.mmax[b] * R.nmax[b]);
   R.Pi = c.take<double>(picap);
@@ -679,6 +721,8 @@ static size_t carve(Run &R, char *base) {
   }
   R.Mp = c.take<double>(mpcap);
   R.dAB = c.take<GemmDesc>(2 * ACI_GEMM_MAX_IN);
+  R.dStat = c.take<BondStatic>(2 * std::max(L - 1, 1));
+  R.dPre = c.take<GemmDesc>((size_t)std::max(L - 1, 1) * N);
   R.dPi = c.take<GemmDesc>(1);
   R.dT = c.take<GemmDesc>(ACI_GEMM_MAX_IN);
   R.dY = c.take<GemmDesc>(1);
@@ -770,8 +814,9 @@ static double normal_at(uint64_t seed, uint64_t i) {
 // ============================================================================ host: the sweep
 namespace {
 
-static void launch_update(Run &R, int b, int dir, int logslot, cudaStream_t st) {
+static void launch_update(Run &R, int b, int dir, int logslot, const BondStatic *next, cudaStream_t st) {
   UpdateArgs U = {};
+  U.next = next; U.ab = R.dAB; U.pi = R.dPi; U.lu = R.dLu;
   U.b = b; U.dir = dir; U.L = R.L; U.N = R.N; U.db = R.d[b]; U.db1 = R.d[b + 1];
   U.rows = R.prow[b]; U.cols = R.pcol[b]; U.r_in = R.rout + b; U.eps_in = R.epsb + b;
   U.rk = R.rk;
@@ -805,50 +850,94 @@ static void launch_update(Run &R, int b, int dir, int logslot, cudaStream_t st) 
   update_bond_kernel<<<blocks, 256, 0, st>>>(U);
 }
 
-static void bond_update(Run &R, const FOp &op, double tol, int tol_mode, int b, int dir, int logslot,
-                        cudaStream_t st) {
+// Static description of every bond update (both directions), built once per call on the host
+// and uploaded to the workspace: the planner kernels read it together with the live ranks.
+static void build_statics(Run &R, const FOp &op) {
+  const int L = R.L, N = R.N, nb = L - 1;
+  R.hStat.assign(2 * nb, BondStatic{});
+  R.nbig.assign(2 * nb, 0);
+  R.nsmall.assign(2 * nb, 0);
+  R.opb.assign(2 * nb, op);
+  for (int dir = 0; dir < 2; ++dir)
+    for (int b = 0; b < nb; ++b) {
+      BondStatic &S = R.hStat[dir * nb + b];
+      S.b = b; S.L = L; S.N = N; S.dir = dir; S.db = R.d[b]; S.db1 = R.d[b + 1];
+      S.ldu = R.nmax[b];
+      S.maxrank = R.maxrank;
+      S.Pi = R.Pi;
+      // Pi kernel input order: inputs whose inner dimension chi^n_{b+1} is large run the DMMA
+      // main loop (first), tiny ones (e.g. rank-2 inputs) are evaluated in the epilogue; the op's
+      // exponents are permuted to the same order.
+      int order[ACI_GEMM_MAX_IN], nbig = 0, nsmall = 0;
+      for (int n = 0; n < N; ++n)
+        if (R.xr[n][b + 1] > gemm_small_k()) order[nbig++] = n;
+      for (int n = 0; n < N; ++n)
+        if (R.xr[n][b + 1] <= gemm_small_k()) order[nbig + nsmall++] = n;
+      R.nbig[dir * nb + b] = nbig;
+      R.nsmall[dir * nb + b] = nsmall;
+      FOp &ob = R.opb[dir * nb + b];
+      for (int t = 0; t < op.T; ++t)
+        for (int k = 0; k < N; ++k) ob.expo[t * N + k] = op.expo[t * N + order[k]];
+      for (int kk = 0; kk < N; ++kk) {
+        const int n = order[kk];
+        InBond &I = S.in[kk];
+        I.c0 = R.xr[n][b]; I.c1 = R.xr[n][b + 1]; I.c2 = R.xr[n][b + 2];
+        I.Xb = R.xcore0[n] + R.xoff[n][b];
+        I.Xb1 = R.xcore0[n] + R.xoff[n][b + 1];
+        I.Lprev = b > 0 ? R.Lf[n][b - 1] : nullptr;
+        I.Rnext = b + 2 < L ? R.Rf[n][b + 2] : nullptr;
+        I.ldR = b + 2 < L ? R.rmax[b + 1] : 1;
+        I.Abuf = R.Abuf[n];
+        I.Bbuf = R.Bbuf[n];
+        I.Apre = R.Apre[n][b];
+        I.Bpre = R.Bpre[n][b];
+      }
+    }
+}
+
+static const BondStatic *dstat(const Run &R, int dir, int b) { return R.dStat + dir * (R.L - 1) + b; }
+
+// Pivot-independent halves of every bond of one half-sweep in one launch (R20: an L->R bond
+// reads the previous sweep's R frames, an R->L bond the previous sweep's L frames).
+static void pre_launch(Run &R, int dir, cudaStream_t st) {
   const int L = R.L, N = R.N;
-  BondStatic S = {};
-  S.b = b; S.L = L; S.N = N; S.db = R.d[b]; S.db1 = R.d[b + 1];
-  S.ldu = R.nmax[b];
-  S.maxrank = R.maxrank;
-  S.Pi = R.Pi;
-  // Pi kernel input order: inputs whose inner dimension chi^n_{b+1} is large run the DMMA main
-  // loop (first), tiny ones (e.g. rank-2 inputs) are evaluated in the epilogue; the op's
-  // exponents are permuted to the same order.
-  int order[ACI_GEMM_MAX_IN], nbig = 0, nsmall = 0;
-  for (int n = 0; n < N; ++n)
-    if (R.xr[n][b + 1] > gemm_small_k()) order[nbig++] = n;
-  for (int n = 0; n < N; ++n)
-    if (R.xr[n][b + 1] <= gemm_small_k()) order[nbig + nsmall++] = n;
-  FOp opb = op;
-  for (int t = 0; t < op.T; ++t)
-    for (int k = 0; k < N; ++k) opb.expo[t * N + k] = op.expo[t * N + order[k]];
+  int pm = 0, pn = 0;
+  for (int b = 0; b < L - 1; ++b)
+    for (int n = 0; n < N; ++n) {
+      if (dir == 0 && b + 2 < L) { pm = std::max(pm, R.xr[n][b + 1] * R.d[b + 1]); pn = std::max(pn, R.rmax[b + 1]); }
+      if (dir == 1 && b > 0) { pm = std::max(pm, R.rmax[b - 1]); pn = std::max(pn, R.d[b] * R.xr[n][b + 1]); }
+    }
+  if (pm == 0) return;
+  R.P->begin(ACI_PROF_GEMM_AB);
+  plan_pre_kernel<<<1, 256, 0, st>>>(dstat(R, dir, 0), L - 1, N, R.rk, R.dPre);
+  FOp dummy = {};
+  launch_gemm(R.dPre, (L - 1) * N, pm, pn, 1, false, dummy, nullptr, nullptr, st);
+  R.P->end(2);
+}
+
+// One 2-site update (Alg. 1): [plan] -> dependent half of a1/a2 -> a3+a4 -> a5 ->
+// a6/a7 (+ the plan of the next bond, fused into the update kernel when `next` is given).
+static void bond_update(Run &R, double tol, int tol_mode, int b, int dir, int logslot, bool plan_here,
+                        const BondStatic *next, cudaStream_t st) {
+  const int L = R.L, N = R.N, k = dir * (L - 1) + b;
   int ab_m = 0, ab_n = 0;
-  for (int kk = 0; kk < N; ++kk) {
-    const int n = order[kk];
-    InBond &I = S.in[kk];
-    I.c0 = R.xr[n][b]; I.c1 = R.xr[n][b + 1]; I.c2 = R.xr[n][b + 2];
-    I.Xb = R.xcore0[n] + R.xoff[n][b];
-    I.Xb1 = R.xcore0[n] + R.xoff[n][b + 1];
-    I.Lprev = b > 0 ? R.Lf[n][b - 1] : nullptr;
-    I.Rnext = b + 2 < L ? R.Rf[n][b + 2] : nullptr;
-    I.ldR = b + 2 < L ? R.rmax[b + 1] : 1;
-    I.Abuf = R.Abuf[n];
-    I.Bbuf = R.Bbuf[n];
-    if (I.Lprev) { ab_m = std::max(ab_m, R.rmax[b - 1]); ab_n = std::max(ab_n, S.db * I.c1); }
-    if (I.Rnext) { ab_m = std::max(ab_m, I.c1 * S.db1); ab_n = std::max(ab_n, R.rmax[b + 1]); }
+  for (int n = 0; n < N; ++n) {
+    if (dir == 0 && b > 0) { ab_m = std::max(ab_m, R.rmax[b - 1]); ab_n = std::max(ab_n, R.d[b] * R.xr[n][b + 1]); }
+    if (dir == 1 && b + 2 < L) { ab_m = std::max(ab_m, R.xr[n][b + 1] * R.d[b + 1]); ab_n = std::max(ab_n, R.rmax[b + 1]); }
   }
-  R.P->begin(ACI_PROF_UPDATE);
-  plan_bond_kernel<<<1, 1, 0, st>>>(S, R.rk, R.dAB, R.dPi, R.dLu);
-  R.P->end(1);
+  if (plan_here) {
+    R.P->begin(ACI_PROF_UPDATE);
+    plan_bond_kernel<<<1, 1, 0, st>>>(dstat(R, dir, b), R.rk, R.dAB, R.dPi, R.dLu);
+    R.P->end(1);
+  }
   if (ab_m > 0) {
     R.P->begin(ACI_PROF_GEMM_AB);
-    launch_gemm(R.dAB, 2 * N, ab_m, ab_n, 1, false, op, nullptr, nullptr, st);
+    FOp dummy = {};
+    launch_gemm(R.dAB, N, ab_m, ab_n, 1, false, dummy, nullptr, nullptr, st);
     R.P->end(1);
   }
   R.P->begin(ACI_PROF_GEMM_PI);
-  launch_gemm_split(R.dPi, 1, R.mmax[b], R.nmax[b], nbig, nsmall, true, opb, R.scale, R.nonfinite, st);
+  launch_gemm_split(R.dPi, 1, R.mmax[b], R.nmax[b], R.nbig[k], R.nsmall[k], true, R.opb[k], R.scale, R.nonfinite, st);
   R.P->end(1);
   LuArgs a = {};
   a.M = R.Pi; a.dims = R.dLu; a.tol = tol; a.thr_mode = tol_mode == ACI_TOL_RELATIVE ? 0 : 2;
@@ -860,7 +949,7 @@ static void bond_update(Run &R, const FOp &op, double tol, int tol_mode, int b, 
   launch_prrlu(a, R.mmax[b], R.nmax[b], st);
   R.P->end(1);
   R.P->begin(ACI_PROF_UPDATE);
-  launch_update(R, b, dir, logslot, st);
+  launch_update(R, b, dir, logslot, next, st);
   R.P->end(1);
 }
 
@@ -1048,8 +1137,11 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   {
     std::vector<int> rk0(L + 1, 0);
     rk0[0] = 1; rk0[L] = 1;
-    // the only host->device copy of state: boundary ranks (pageable; tiny)
+    // host->device copies of state: boundary ranks and the static bond table (pointers and
+    // input ranks of every bond update; no data)
     cudaMemcpyAsync(R.rk, rk0.data(), sizeof(int) * (L + 1), cudaMemcpyHostToDevice, strm);
+    build_statics(R, I.op);
+    cudaMemcpyAsync(R.dStat, R.hStat.data(), sizeof(BondStatic) * R.hStat.size(), cudaMemcpyHostToDevice, strm);
     cudaStreamSynchronize(strm);
   }
   cudaMemsetAsync(R.scale, 0, sizeof(unsigned long long), strm);
@@ -1075,8 +1167,12 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   // once as a CUDA graph and replayed; only the convergence flag comes back to the host.
   auto one_iteration = [&]() {
     int step = 0;
-    for (int b = 0; b < L - 1; ++b) bond_update(R, I.op, tol, o.tol_mode, b, 0, step++, strm);
-    for (int b = L - 2; b >= 0; --b) bond_update(R, I.op, tol, o.tol_mode, b, 1, step++, strm);
+    pre_launch(R, 0, strm);
+    for (int b = 0; b < L - 1; ++b)
+      bond_update(R, tol, o.tol_mode, b, 0, step++, b == 0, b + 1 < L - 1 ? dstat(R, 0, b + 1) : dstat(R, 1, L - 2), strm);
+    pre_launch(R, 1, strm);
+    for (int b = L - 2; b >= 0; --b)
+      bond_update(R, tol, o.tol_mode, b, 1, step++, false, b > 0 ? dstat(R, 1, b - 1) : nullptr, strm);
     prof.begin(ACI_PROF_CONV);
     converge_kernel<<<1, 32, 0, strm>>>(R.rk, R.prev, L, R.maxeps, R.scale, tol, o.tol_mode, R.conv, R.err,
                                         R.iter);

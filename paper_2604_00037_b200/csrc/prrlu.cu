@@ -180,7 +180,6 @@ __device__ __forceinline__ double key_abs(const Key &k) {
 #ifndef ACI_BIG_EB
 #define ACI_BIG_EB 2  // columns per warp for the 1024-row grid tier (64 CTAs for 1024 columns)
 #endif
-constexpr int kNW = 16;          // warps per CTA (512 threads) for every variant
 constexpr int kMaxRows = 1024;   // 32 * EA_max
 constexpr int kMaxCTAs = 148;
 constexpr int kMaxCB = 512;      // NW * EB_max

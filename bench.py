@@ -136,7 +136,7 @@ def _ncu_traffic():
     d = json.load(open(files[-1]))
     out = {}
     for k, v in d.items():
-        if isinstance(v, dict) and "dram_bytes_read" in v:
+        if isinstance(v, dict) and "dram_bytes_read" in v and (k.startswith("prrlu") or k.startswith("gemmpi")):
             key = "prrlu" if k.startswith("prrlu") else "contraction"
             out[key] = {"bytes": v["dram_bytes_read"] + v["dram_bytes_write"], "source": os.path.basename(files[-1]),
                         "kernel": v["kernel"]}

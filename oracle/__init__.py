@@ -10,6 +10,8 @@ Contents
 --------
 * ``aci``      — Alg. 1-5 as naive C loops (``aci_oracle.c``),
                  readings R1-R22 of DESIGN.md §2.
+* ``aci_z``, ``ldu_z`` — the same for complex values (f: C^N -> C, P:84;
+                 ``aci_oracle_z.c``), complex-arithmetic readings RZ1-RZ6.
 * ``ldu``, ``ci_right``, ``assemble_pi`` — the sub-steps (Alg. 2, Alg. 3,
                  Eq. pifromframes), exported for the pin tests.
 * ``tt_evaluate``, ``tt_dense`` — the plain definition of a TT.
@@ -34,6 +36,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "aci_oracle.c")
+_SRCZ = os.path.join(_HERE, "aci_oracle_z.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
@@ -42,9 +45,10 @@ STATUS = {0: "ok", -1: "invalid", -3: "nonfinite", -4: "oom"}
 
 def build(force: bool = False) -> str:
     """Compile the C oracle with gcc (no fast-math, no FP contraction)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if (force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC)
+            or os.path.getmtime(_LIB) < os.path.getmtime(_SRCZ)):
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC",
-                               "-o", _LIB, _SRC, "-lm"])
+                               "-o", _LIB, _SRC, _SRCZ, "-lm"])
     return _LIB
 
 
@@ -78,6 +82,18 @@ def _load():
                                         C.c_int, dp]
         lib.oracle_assemble_pi.argtypes = [C.c_int, ip, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(dp),
                                            C.POINTER(dp), C.POINTER(dp), C.POINTER(dp), C.c_int, dp, ip, dp]
+        lib.oraclez_aci.restype = vp
+        lib.oraclez_aci.argtypes = lib.oracle_aci.argtypes
+        lib.oraclez_free.argtypes = [vp]
+        lib.oraclez_report.argtypes = lib.oracle_report.argtypes
+        lib.oraclez_out_ranks.argtypes = [vp, ip]
+        lib.oraclez_out_core.argtypes = [vp, C.c_int, dp]
+        lib.oraclez_log_count.argtypes = [vp]
+        lib.oraclez_log_entry.argtypes = [vp, C.c_int, ip, dp, ip, ip]
+        lib.oraclez_canon_jn.argtypes = [vp, C.c_int]
+        lib.oraclez_canon_cols.argtypes = [vp, C.c_int, ip]
+        lib.oraclez_ldu.argtypes = [C.c_int, C.c_int, dp, C.c_double, C.c_int, C.c_int, ip, ip, ip, dp, dp,
+                                    C.c_int, dp]
         _lib = lib
     return _lib
 
@@ -293,18 +309,131 @@ def aci(inputs, op, y_init, tol, maxrank, max_sweeps, relative=True) -> AciResul
 
 
 # --------------------------------------------------------------------------
+# Complex values (f: C^N -> C): aci_oracle_z.c, readings RZ1-RZ6
+# --------------------------------------------------------------------------
+def _zptr(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def ldu_z(M, thr: float, maxrank: int, relative_to_own_max: bool = False) -> dict:
+    """Alg. 2 on a complex matrix (RZ1-RZ4). Returns rows, cols, D, U (r x n), eps."""
+    lib = _load()
+    M = np.ascontiguousarray(M, dtype=np.complex128)
+    m, n = M.shape
+    maxr = max(1, min(m, n, maxrank))
+    r, eps = C.c_int(), C.c_double()
+    rows = np.zeros(maxr, np.int32)
+    cols = np.zeros(maxr, np.int32)
+    D = np.zeros(maxr, np.complex128)
+    U = np.zeros((maxr, n), np.complex128)
+    st = lib.oraclez_ldu(m, n, _zptr(M), thr, 1 if relative_to_own_max else 0, maxrank, C.byref(r), _iptr(rows),
+                         _iptr(cols), _zptr(D), _zptr(U), maxr, C.byref(eps))
+    if st != 0:
+        raise ValueError(f"oraclez_ldu: {STATUS.get(st, st)}")
+    k = r.value
+    return {"r": k, "rows": rows[:k].copy(), "cols": cols[:k].copy(), "D": D[:k].copy(), "U": U[:k].copy(),
+            "eps": eps.value}
+
+
+class AciResultZ:
+    """Handle on a complex oracle ACI run (cores complex128)."""
+
+    def __init__(self, h, L, N, d):
+        self._h = h
+        self.L, self.N, self.d = L, N, d
+        lib = _load()
+        sc, err, fc, fp = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+        it, cv = C.c_int(), C.c_int()
+        pv = C.c_longlong()
+        lib.oraclez_report(h, C.byref(sc), C.byref(err), C.byref(it), C.byref(cv), C.byref(fc), C.byref(fp),
+                           C.byref(pv))
+        self.report = {"scale": sc.value, "error_estimate": err.value, "iterations": it.value,
+                       "converged": bool(cv.value), "flops_contraction": fc.value, "flops_prrlu": fp.value,
+                       "pivot_steps": pv.value}
+        ranks = np.zeros(L + 1, np.int32)
+        lib.oraclez_out_ranks(h, _iptr(ranks))
+        self.ranks = [int(x) for x in ranks]
+        self.cores = []
+        for s in range(L):
+            c = np.zeros((self.ranks[s], d[s], self.ranks[s + 1]), np.complex128)
+            lib.oraclez_out_core(h, s, _zptr(c))
+            self.cores.append(c)
+        self.log = []
+        for u in range(lib.oraclez_log_count(h)):
+            info = np.zeros(5, np.int32)
+            es = np.zeros(2)
+            lib.oraclez_log_entry(h, u, _iptr(info), _dptr(es), None, None)
+            rows = np.zeros(info[4], np.int32)
+            cols = np.zeros(info[4], np.int32)
+            lib.oraclez_log_entry(h, u, _iptr(info), _dptr(es), _iptr(rows), _iptr(cols))
+            self.log.append({"bond": int(info[0]), "dir": int(info[1]), "rl": int(info[2]), "rr": int(info[3]),
+                             "r": int(info[4]), "eps": float(es[0]), "scale": float(es[1]), "rows": rows,
+                             "cols": cols})
+
+    def canon_cols(self, s):
+        n = _load().oraclez_canon_jn(self._h, s)
+        out = np.zeros(n, np.int32)
+        _load().oraclez_canon_cols(self._h, s, _iptr(out))
+        return out
+
+    def free(self):
+        if self._h:
+            _load().oraclez_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def aci_z(inputs, op, y_init, tol, maxrank, max_sweeps, relative=True) -> AciResultZ:
+    """Complex Alg. 1 with RZ1-RZ6; inputs and y_init complex TTs."""
+    lib = _load()
+    ins = [_cores_of(x) for x in inputs]
+    N, L = len(ins), len(ins[0])
+    d = [int(c.shape[1]) for c in ins[0]]
+    xr = np.array([[int(c[0].shape[0])] + [int(cc.shape[2]) for cc in c] for c in ins], np.int32)
+    keep = []
+    cp = (C.POINTER(C.c_double) * (N * L))()
+    for n in range(N):
+        for s in range(L):
+            a = np.ascontiguousarray(ins[n][s], dtype=np.complex128)
+            keep.append(a)
+            cp[n * L + s] = _zptr(a)
+    yc = _cores_of(y_init)
+    yr = np.array([int(yc[0].shape[0])] + [int(c.shape[2]) for c in yc], np.int32)
+    yp = (C.POINTER(C.c_double) * L)()
+    for s in range(L):
+        a = np.ascontiguousarray(yc[s], dtype=np.complex128)
+        keep.append(a)
+        yp[s] = _zptr(a)
+    coef = np.ascontiguousarray(op["coef"], dtype=np.float64)
+    expo = np.ascontiguousarray(op["expo"], dtype=np.int32)
+    dd = np.array(d, np.int32)
+    st = C.c_int()
+    h = lib.oraclez_aci(L, _iptr(dd), N, _iptr(xr), cp, len(coef), _dptr(coef), _iptr(expo), _iptr(yr), yp,
+                        float(tol), 0 if relative else 1, int(maxrank), int(max_sweeps), C.byref(st))
+    if not h:
+        raise ValueError(f"oraclez_aci: {STATUS.get(st.value, st.value)}")
+    return AciResultZ(h, L, N, d)
+
+
+# --------------------------------------------------------------------------
 # Plain definitions (numpy): TT evaluation, dense tensor, exact product
 # --------------------------------------------------------------------------
 def tt_evaluate(cores, idx, chunk: int = 4096) -> np.ndarray:
     """x_sigma = X_1[sigma_1] X_2[sigma_2] ... X_L[sigma_L], per point."""
     cores = _cores_of(cores)
     idx = np.asarray(idx)
-    out = np.empty(idx.shape[0])
+    dt = np.result_type(*cores)
+    out = np.empty(idx.shape[0], dt)
     for p0 in range(0, idx.shape[0], chunk):
         sl = idx[p0:p0 + chunk]
-        v = np.ones((sl.shape[0], 1))
+        v = np.ones((sl.shape[0], 1), dt)
         for s, c in enumerate(cores):
-            nv = np.empty((sl.shape[0], c.shape[2]))
+            nv = np.empty((sl.shape[0], c.shape[2]), dt)
             for sg in range(c.shape[1]):
                 sel = sl[:, s] == sg
                 if np.any(sel):
@@ -362,7 +491,7 @@ def exact_product(inputs, op) -> list:
         else:
             rl = sum(p.shape[0] for p in parts)
             rr = sum(p.shape[2] for p in parts)
-            c = np.zeros((rl, parts[0].shape[1], rr))
+            c = np.zeros((rl, parts[0].shape[1], rr), np.result_type(*parts))
             i = j = 0
             for p in parts:
                 c[i:i + p.shape[0], :, j:j + p.shape[2]] = p
@@ -376,7 +505,7 @@ def tt_round(cores, tol: float) -> list:
     """Textbook TT-SVD rounding: left-to-right QR, then right-to-left truncated SVD with
     per-bond Frobenius budget tol*||C||_F/sqrt(L-1) (the step the paper leaves to the
     MPO-MPS baseline)."""
-    cores = [np.array(c, dtype=np.float64) for c in _cores_of(cores)]
+    cores = [np.array(c, dtype=np.result_type(c, np.float64)) for c in _cores_of(cores)]
     L = len(cores)
     for s in range(L - 1):
         r0, d, r1 = cores[s].shape
@@ -412,7 +541,7 @@ def tt_axpby(alpha, a, beta, b) -> list:
         elif s == L - 1:
             out.append(np.concatenate([x, y], axis=0))
         else:
-            c = np.zeros((x.shape[0] + y.shape[0], x.shape[1], x.shape[2] + y.shape[2]))
+            c = np.zeros((x.shape[0] + y.shape[0], x.shape[1], x.shape[2] + y.shape[2]), np.result_type(x, y))
             c[:x.shape[0], :, :x.shape[2]] = x
             c[x.shape[0]:, :, x.shape[2]:] = y
             out.append(c)
@@ -422,7 +551,7 @@ def tt_axpby(alpha, a, beta, b) -> list:
 def tt_norm(cores) -> float:
     """Frobenius norm by left-orthogonalisation (QR sweep): no cancellation, accurate even when
     the TT is a small difference of two large ones."""
-    cores = [np.array(c, dtype=np.float64) for c in _cores_of(cores)]
+    cores = [np.array(c, dtype=np.result_type(c, np.float64)) for c in _cores_of(cores)]
     R = np.ones((1, 1))
     for c in cores:
         c = np.einsum("ab,bsc->asc", R, c)

@@ -21,6 +21,7 @@ CONFIG_NAMES = {
     2: "cfg2_psi3_gaussians_L30",
     3: "cfg3_randomTT_L40_chi{chi}",
     4: "cfg4_planewave_L20_d4",
+    5: "cfg5_fourier_complex_L30_K{chi}",
 }
 
 
@@ -63,7 +64,7 @@ def _block_sum(tts: list) -> TT:
         else:
             rl = sum(p.shape[0] for p in parts)
             rr = sum(p.shape[2] for p in parts)
-            c = np.zeros((rl, d, rr))
+            c = np.zeros((rl, d, rr), np.result_type(*parts))
             i0 = j0 = 0
             for p in parts:
                 c[i0:i0 + p.shape[0], :, j0:j0 + p.shape[2]] = p
@@ -175,6 +176,63 @@ def gaussian3d_tt(nbits: int, cs, sigmas, amps, cutoff=1e-12) -> TT:
     return tt
 
 
+def _tt_compress(cores: list, cutoff: float) -> list:
+    """Input-construction rounding: left-to-right QR, right-to-left SVD keeping singular values
+    s_k > cutoff * s_1 per bond (the R14 cutoff rule, on complex or real cores)."""
+    cores = [c.copy() for c in cores]
+    L = len(cores)
+    for s in range(L - 1):
+        r0, d, r1 = cores[s].shape
+        Q, R = np.linalg.qr(cores[s].reshape(r0 * d, r1))
+        cores[s] = Q.reshape(r0, d, Q.shape[1])
+        nxt = cores[s + 1]
+        cores[s + 1] = (R @ nxt.reshape(nxt.shape[0], -1)).reshape(R.shape[0], nxt.shape[1], nxt.shape[2])
+    for s in range(L - 1, 0, -1):
+        r0, d, r1 = cores[s].shape
+        U, S, Vt = np.linalg.svd(cores[s].reshape(r0, d * r1), full_matrices=False)
+        keep = max(1, int(np.sum(S > cutoff * S[0])))
+        cores[s] = Vt[:keep].reshape(keep, d, r1)
+        prv = cores[s - 1]
+        cores[s - 1] = (prv.reshape(-1, prv.shape[2]) @ (U[:, :keep] * S[:keep])).reshape(prv.shape[0], prv.shape[1],
+                                                                                           keep)
+    return cores
+
+
+def fourier_tt(L: int, coefs, cutoff: float = 1e-12, chunk: int = 256) -> TT:
+    """Complex QTT of g(x) = sum_{k=0..K} coefs[k] e^{i k x} on x = sum_l 2^-l sigma_l in [0, 1)
+    (P:289-293). Each e^{ikx} = prod_l e^{i k 2^-l sigma_l} is rank 1; the terms are block-summed
+    in chunks of `chunk` frequencies and rounded after each chunk (cutoff rule of R14), so the
+    rank stays at the numerical rank O(sqrt K)."""
+    coefs = np.asarray(coefs, dtype=np.complex128)
+    K = len(coefs) - 1
+    acc = None
+    for k0 in range(0, K + 1, chunk):
+        ks = np.arange(k0, min(K + 1, k0 + chunk))
+        n = len(ks)
+        cores = []
+        for s in range(L):
+            ph = np.exp(1j * ks * 2.0 ** -(s + 1))
+            if s == 0:
+                c = np.zeros((1, 2, n), np.complex128)
+                c[0, 0, :] = coefs[ks]
+                c[0, 1, :] = coefs[ks] * ph
+            elif s == L - 1:
+                c = np.zeros((n, 2, 1), np.complex128)
+                c[:, 0, 0] = 1.0
+                c[:, 1, 0] = ph
+            else:
+                c = np.zeros((n, 2, n), np.complex128)
+                i = np.arange(n)
+                c[i, 0, i] = 1.0
+                c[i, 1, i] = ph
+            cores.append(c)
+        part = TT(cores)
+        acc = part if acc is None else _block_sum([acc, part])
+        acc = TT(_tt_compress(acc.cores, cutoff))
+    acc.meta = {"kind": "fourier", "coefs": coefs}
+    return acc
+
+
 def _bond_bound(d: list, s: int) -> int:
     """Largest possible rank of bond s-1|s of any tensor: min(prod d[:s], prod d[s:])."""
     left = int(np.prod([float(x) for x in d[:s]]))
@@ -184,11 +242,19 @@ def _bond_bound(d: list, s: int) -> int:
 
 def random_init(inputs: list, maxrank: int, rng: np.random.Generator) -> TT:
     """y_init: bond ranks min_n chi^n_l capped at maxrank and at the full-tensor bound
-    min(prod d_left, prod d_right) (R9'), iid N(0,1) entries (R9)."""
+    min(prod d_left, prod d_right) (R9'), iid N(0,1) entries (R9); complex inputs get
+    iid N(0,1) real and imaginary parts."""
     L = inputs[0].L
     d = inputs[0].d
     ranks = [1] + [min(min(t.ranks[s] for t in inputs), maxrank, _bond_bound(d, s)) for s in range(1, L)] + [1]
-    cores = [rng.standard_normal((ranks[s], d[s], ranks[s + 1])) for s in range(L)]
+    cplx = any(np.iscomplexobj(c) for t in inputs for c in t.cores)
+    cores = []
+    for s in range(L):
+        shp = (ranks[s], d[s], ranks[s + 1])
+        c = rng.standard_normal(shp)
+        if cplx:
+            c = c + 1j * rng.standard_normal(shp)
+        cores.append(c)
     return TT(cores, {"kind": "y_init"})
 
 
@@ -242,6 +308,18 @@ def make_config(cfg: int, chi: int = 0, npts: int = 100_000) -> dict:
             tts.append(plane_wave_tt(L, kx, ky, ph, [(m + 1) ** -2.0 for m in range(64)]))
         op = {"coef": [1.0, 1.0], "expo": [[1, 1], [2, 0]]}
         tol, maxrank, sweeps = 1e-8, 256, 8
+    elif cfg == 5:
+        # the paper's random Fourier series: two series with K+1 complex coefficients,
+        # Re and Im iid U[0,1], normalised to sum |g_k|^2 = 1, L = 30 quantics, tau = 1e-8;
+        # `chi` carries K here
+        K = chi if chi > 0 else 100
+        tts = []
+        for stream in (0, 1):
+            r = _rng(5, stream, K)
+            c = r.uniform(0, 1, K + 1) + 1j * r.uniform(0, 1, K + 1)
+            tts.append(fourier_tt(30, c / np.linalg.norm(c)))
+        op = {"coef": [1.0], "expo": [[1, 1]]}
+        tol, maxrank, sweeps = 1e-8, 256, 20
     else:
         raise ValueError(cfg)
     y_init = random_init(tts, maxrank, _rng(cfg, 2, chi))

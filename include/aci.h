@@ -53,20 +53,36 @@ int tt_create(int L, const int *d, const int *ranks, const double *const *cores,
  * (device pointer). The data are copied device -> device. */
 int tt_create_device(int L, const int *d, const int *ranks, const double *dev_cores, void *stream, tt_t **out);
 
+/* Complex TTs (f: C^N -> C; the random Fourier series of P:289-296). Arguments as
+ * tt_create / tt_create_device, but every core entry is a complex number stored as two
+ * consecutive doubles (re, im) (C99 double complex / numpy complex128 layout): core s holds
+ * 2*ranks[s]*d[s]*ranks[s+1] doubles. Every other call accepts complex handles: tt_get_cores and
+ * tt_evaluate(_device) then read/write 2 doubles per entry / per point, and aci_elementwise(_ex)
+ * requires all inputs (and y_init) to be complex and returns a complex TT (readings RZ1-RZ6 of
+ * pivots by |z|^2 = re^2 + im^2, complex Schur updates). Complex 2-site blocks
+ * are limited to 512 rows (aci_elementwise returns ACI_ERR_UNSUPPORTED beyond). */
+int tt_create_z(int L, const int *d, const int *ranks, const double *const *cores, tt_t **out);
+int tt_create_device_z(int L, const int *d, const int *ranks, const double *dev_cores, void *stream, tt_t **out);
+
+/* 1 if tt holds complex cores, else 0 (NULL: 0). */
+int tt_is_complex(const tt_t *tt);
+
 /* Free a TT (device memory included). NULL is a no-op. Returns ACI_OK. */
 int tt_destroy(tt_t *tt);
 
 /* Shape query: *L, and if non-NULL d[L], ranks[L+1]. */
 int tt_shape(const tt_t *tt, int *L, int *d, int *ranks);
 
-/* Copy the cores to host buffers host_cores[s] (each ranks[s]*d[s]*ranks[s+1] doubles). */
+/* Copy the cores to host buffers host_cores[s] (each ranks[s]*d[s]*ranks[s+1] doubles; twice
+ * that, interleaved (re, im), for a complex TT). */
 int tt_get_cores(const tt_t *tt, double *const *host_cores);
 
 /* Device pointer to the contiguous core storage (core s at offset sum_{t<s} r_t d_t r_{t+1}). */
 const double *tt_device_cores(const tt_t *tt);
 
 /* Evaluate x at npts full multi-indices (O(L chi^2) per point).
- * idx: host, npts*L uint8 (row-major, point-major), out: host, npts doubles.
+ * idx: host, npts*L uint8 (row-major, point-major), out: host, npts doubles (2*npts,
+ * interleaved (re, im), for a complex TT).
  * Errors: ACI_ERR_INVALID (index >= d_s, null), ACI_ERR_CUDA. */
 int tt_evaluate(const tt_t *tt, int64_t npts, const uint8_t *idx, double *out);
 

@@ -90,6 +90,7 @@ def _load():
         lib.oraclez_out_core.argtypes = [vp, C.c_int, dp]
         lib.oraclez_log_count.argtypes = [vp]
         lib.oraclez_log_entry.argtypes = [vp, C.c_int, ip, dp, ip, ip]
+        lib.oraclez_log_gaps.argtypes = [vp, C.c_int, dp]
         lib.oraclez_canon_jn.argtypes = [vp, C.c_int]
         lib.oraclez_canon_cols.argtypes = [vp, C.c_int, ip]
         lib.oraclez_ldu.argtypes = [C.c_int, C.c_int, dp, C.c_double, C.c_int, C.c_int, ip, ip, ip, dp, dp,
@@ -366,9 +367,11 @@ class AciResultZ:
             rows = np.zeros(info[4], np.int32)
             cols = np.zeros(info[4], np.int32)
             lib.oraclez_log_entry(h, u, _iptr(info), _dptr(es), _iptr(rows), _iptr(cols))
+            gap = np.zeros(info[4])
+            lib.oraclez_log_gaps(h, u, _dptr(gap))
             self.log.append({"bond": int(info[0]), "dir": int(info[1]), "rl": int(info[2]), "rr": int(info[3]),
                              "r": int(info[4]), "eps": float(es[0]), "scale": float(es[1]), "rows": rows,
-                             "cols": cols})
+                             "cols": cols, "gap": gap})
 
     def canon_cols(self, s):
         n = _load().oraclez_canon_jn(self._h, s)

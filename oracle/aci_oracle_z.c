@@ -67,10 +67,12 @@ typedef struct {
   cz *U;       /* r x n, U_k = S_k[p,:] * inv, U_k[q] = 1 */
   double eps;  /* |c| of the first rejected candidate (R2) */
   double first;
+  double *gap; /* per accepted pivot: (w1 - w2) / w1, w1 >= w2 the two largest candidate |z|^2
+                * (diagnostic for ties within roundoff; 1 if there is a single candidate) */
 } zldu_t;
 
 static void zldu_free(zldu_t *f) {
-  free(f->rows); free(f->cols); free(f->D); free(f->U);
+  free(f->rows); free(f->cols); free(f->D); free(f->U); free(f->gap);
   memset(f, 0, sizeof(*f));
 }
 
@@ -86,22 +88,25 @@ static int zldu(int m, int n, const cz *M, double thr, int thr_mode, int maxrank
   out->cols = (int *)malloc(sizeof(int) * (kcap + 1));
   out->D = (cz *)malloc(sizeof(cz) * (kcap + 1));
   out->U = (cz *)calloc((size_t)(kcap + 1) * n, sizeof(cz));
-  if (!S || !rowdone || !coldone || !out->rows || !out->U) return ORC_ERR_OOM;
+  out->gap = (double *)calloc(kcap + 1, sizeof(double));
+  if (!S || !rowdone || !coldone || !out->rows || !out->U || !out->gap) return ORC_ERR_OOM;
   memcpy(S, M, sizeof(cz) * (size_t)m * n);
   int mn = m < n ? m : n;
   int k = 0;
   for (;;) {
     if (k == mn) { out->eps = 0.0; break; }
     int p = -1, q = -1;
-    double best = -1.0;
+    double best = -1.0, second = -1.0;
     for (int i = 0; i < m; ++i) {
       if (rowdone[i]) continue;
       for (int j = 0; j < n; ++j) {
         if (coldone[j]) continue;
         double w = cz_w(S[(size_t)i * n + j]);
-        if (w > best) { best = w; p = i; q = j; } /* strict '>' keeps the smallest (row, col) (R3) */
+        if (w > best) { second = best; best = w; p = i; q = j; } /* strict '>': smallest (row, col) (R3) */
+        else if (w > second) second = w;
       }
     }
+    out->gap[k] = (best > 0 && second >= 0) ? (best - second) / best : 1.0;
     cz c = S[(size_t)p * n + q];
     double w = cz_w(c);
     double absc = sqrt(w);
@@ -202,6 +207,7 @@ typedef struct {
   int b, dir, rl, rr, r;
   double eps, scale;
   int *rows, *cols;
+  double *gap;
 } zlogent_t;
 
 typedef struct {
@@ -235,6 +241,8 @@ static void zlog_push(zaci_t *S, int b, int dir, int rl, int rr, const zldu_t *f
   e->cols = (int *)malloc(sizeof(int) * f->r);
   memcpy(e->rows, f->rows, sizeof(int) * f->r);
   memcpy(e->cols, f->cols, sizeof(int) * f->r);
+  e->gap = (double *)malloc(sizeof(double) * f->r);
+  memcpy(e->gap, f->gap, sizeof(double) * f->r);
 }
 
 /* Alg. 5 Leftframe */
@@ -321,7 +329,7 @@ static void zaci_free(zaci_t *S) {
   free(S->I); free(S->J);
   for (int s = 0; s < S->L; ++s) if (S->Y) free(S->Y[s]);
   free(S->Y); free(S->yr);
-  for (int i = 0; i < S->nlog; ++i) { free(S->log[i].rows); free(S->log[i].cols); }
+  for (int i = 0; i < S->nlog; ++i) { free(S->log[i].rows); free(S->log[i].cols); free(S->log[i].gap); }
   free(S->log);
   for (int s = 0; s <= S->L; ++s) if (S->canon_cols_log) free(S->canon_cols_log[s]);
   free(S->canon_cols_log); free(S->canon_Jn);
@@ -503,6 +511,10 @@ void oraclez_log_entry(void *h, int u, int *info, double *eps_scale, int *rows, 
   eps_scale[0] = e->eps; eps_scale[1] = e->scale;
   if (rows) memcpy(rows, e->rows, sizeof(int) * e->r);
   if (cols) memcpy(cols, e->cols, sizeof(int) * e->r);
+}
+void oraclez_log_gaps(void *h, int u, double *gap) {
+  zlogent_t *e = &((zaci_t *)h)->log[u];
+  memcpy(gap, e->gap, sizeof(double) * e->r);
 }
 int oraclez_canon_jn(void *h, int s) { return ((zaci_t *)h)->canon_Jn[s]; }
 void oraclez_canon_cols(void *h, int s, int *dst) {

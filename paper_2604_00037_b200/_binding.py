@@ -19,9 +19,9 @@ TOL_RELATIVE, TOL_ABSOLUTE = 0, 1
 MAX_INPUTS, MAX_TERMS, MAX_EXPO = 4, 8, 4
 
 # every symbol include/aci.h declares (tests check the library exports all of them)
-EXPORTS = ["tt_create", "tt_create_device", "tt_destroy", "tt_shape", "tt_get_cores", "tt_device_cores",
-           "tt_evaluate", "tt_evaluate_device", "aci_elementwise", "aci_elementwise_ex", "aci_workspace_query",
-           "aci_limits", "aci_last_error", "aci_version"]
+EXPORTS = ["tt_create", "tt_create_z", "tt_create_device", "tt_create_device_z", "tt_is_complex", "tt_destroy",
+           "tt_shape", "tt_get_cores", "tt_device_cores", "tt_evaluate", "tt_evaluate_device", "aci_elementwise",
+           "aci_elementwise_ex", "aci_workspace_query", "aci_limits", "aci_last_error", "aci_version"]
 
 
 class AciError(RuntimeError):
@@ -81,7 +81,10 @@ def load(path: str = LIB_PATH):
     lib = C.CDLL(path)
     vp, ip, dp = C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double)
     lib.tt_create.argtypes = [C.c_int, ip, ip, C.POINTER(dp), C.POINTER(vp)]
+    lib.tt_create_z.argtypes = [C.c_int, ip, ip, C.POINTER(dp), C.POINTER(vp)]
     lib.tt_create_device.argtypes = [C.c_int, ip, ip, C.c_void_p, C.c_void_p, C.POINTER(vp)]
+    lib.tt_create_device_z.argtypes = [C.c_int, ip, ip, C.c_void_p, C.c_void_p, C.POINTER(vp)]
+    lib.tt_is_complex.argtypes = [vp]
     lib.tt_destroy.argtypes = [vp]
     lib.tt_shape.argtypes = [vp, ip, ip, ip]
     lib.tt_get_cores.argtypes = [vp, C.POINTER(dp)]
@@ -119,14 +122,18 @@ class TensorTrain:
 
     @classmethod
     def from_cores(cls, cores) -> "TensorTrain":
-        cores = [np.ascontiguousarray(c, dtype=np.float64) for c in (cores.cores if hasattr(cores, "cores") else cores)]
+        """Real cores -> tt_create; complex cores (numpy complex128, interleaved) -> tt_create_z."""
+        cores = list(cores.cores if hasattr(cores, "cores") else cores)
+        cplx = any(np.iscomplexobj(c) for c in cores)
+        dt = np.complex128 if cplx else np.float64
+        cores = [np.ascontiguousarray(c, dtype=dt) for c in cores]
         L = len(cores)
         d = np.array([c.shape[1] for c in cores], np.int32)
         r = np.array([cores[0].shape[0]] + [c.shape[2] for c in cores], np.int32)
         ptrs = (C.POINTER(C.c_double) * L)(*[_dptr(c) for c in cores])
         h = C.c_void_p()
-        _check(load().tt_create(L, d.ctypes.data_as(C.POINTER(C.c_int)), r.ctypes.data_as(C.POINTER(C.c_int)),
-                                ptrs, C.byref(h)))
+        fn = load().tt_create_z if cplx else load().tt_create
+        _check(fn(L, d.ctypes.data_as(C.POINTER(C.c_int)), r.ctypes.data_as(C.POINTER(C.c_int)), ptrs, C.byref(h)))
         return cls(h)
 
     @classmethod
@@ -152,9 +159,14 @@ class TensorTrain:
                                r.ctypes.data_as(C.POINTER(C.c_int))))
         return [int(x) for x in d], [int(x) for x in r]
 
+    @property
+    def is_complex(self) -> bool:
+        return bool(load().tt_is_complex(self._h))
+
     def cores(self):
         d, r = self.shape()
-        out = [np.zeros((r[s], d[s], r[s + 1])) for s in range(len(d))]
+        dt = np.complex128 if self.is_complex else np.float64
+        out = [np.zeros((r[s], d[s], r[s + 1]), dt) for s in range(len(d))]
         ptrs = (C.POINTER(C.c_double) * len(d))(*[_dptr(c) for c in out])
         _check(load().tt_get_cores(self._h, ptrs))
         return out
@@ -164,7 +176,7 @@ class TensorTrain:
 
     def evaluate(self, idx) -> np.ndarray:
         idx = np.ascontiguousarray(idx, dtype=np.uint8)
-        out = np.zeros(idx.shape[0])
+        out = np.zeros(idx.shape[0], np.complex128 if self.is_complex else np.float64)
         _check(load().tt_evaluate(self._h, idx.shape[0], idx.ctypes.data, _dptr(out)))
         return out
 

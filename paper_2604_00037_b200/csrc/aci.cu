@@ -35,8 +35,9 @@ extern "C" const char *aci_version(void) { return "aci-b200 0.1 (sm_100a, FP64 D
 // ============================================================================ TT objects
 struct tt_s {
   int L = 0;
+  int cplx = 0;             // 1: complex cores, interleaved (re, im) doubles
   std::vector<int> d, ranks;
-  std::vector<size_t> off;  // L+1 offsets (doubles)
+  std::vector<size_t> off;  // L+1 offsets (doubles; 2 per complex entry)
   double *dcores = nullptr;
   size_t total = 0;
 };
@@ -69,28 +70,30 @@ static int validate_shape(int L, const int *d, const int *ranks) {
   return ACI_OK;
 }
 
-static tt_s *tt_alloc_shape(int L, const int *d, const int *ranks) {
+static tt_s *tt_alloc_shape(int L, const int *d, const int *ranks, int cplx = 0) {
   tt_s *t = new tt_s;
   t->L = L;
+  t->cplx = cplx;
   t->d.assign(d, d + L);
   t->ranks.assign(ranks, ranks + L + 1);
   t->off.resize(L + 1);
   size_t o = 0;
   for (int s = 0; s < L; ++s) {
     t->off[s] = o;
-    o += (size_t)ranks[s] * d[s] * ranks[s + 1];
+    o += (size_t)ranks[s] * d[s] * ranks[s + 1] * (cplx ? 2 : 1);
   }
   t->off[L] = o;
   t->total = o;
   return t;
 }
 
-extern "C" int tt_create(int L, const int *d, const int *ranks, const double *const *cores, tt_t **out) {
+static int tt_create_impl(int L, const int *d, const int *ranks, const double *const *cores, int cplx,
+                          tt_t **out) {
   if (!out || !cores) return fail(ACI_ERR_INVALID, "tt_create: null argument");
   int st = validate_shape(L, d, ranks);
   if (st) return st;
   if ((st = check_device())) return st;
-  tt_s *t = tt_alloc_shape(L, d, ranks);
+  tt_s *t = tt_alloc_shape(L, d, ranks, cplx);
   for (int s = 0; s < L; ++s) {
     if (!cores[s]) { delete t; return fail(ACI_ERR_INVALID, "tt_create: null core"); }
     size_t sz = t->off[s + 1] - t->off[s];
@@ -114,13 +117,23 @@ extern "C" int tt_create(int L, const int *d, const int *ranks, const double *co
   return ACI_OK;
 }
 
-extern "C" int tt_create_device(int L, const int *d, const int *ranks, const double *dev_cores, void *stream,
-                                tt_t **out) {
+extern "C" int tt_create(int L, const int *d, const int *ranks, const double *const *cores, tt_t **out) {
+  return tt_create_impl(L, d, ranks, cores, 0, out);
+}
+
+extern "C" int tt_create_z(int L, const int *d, const int *ranks, const double *const *cores, tt_t **out) {
+  return tt_create_impl(L, d, ranks, cores, 1, out);
+}
+
+extern "C" int tt_is_complex(const tt_t *t) { return t ? t->cplx : 0; }
+
+static int tt_create_device_impl(int L, const int *d, const int *ranks, const double *dev_cores, void *stream,
+                                 int cplx, tt_t **out) {
   if (!out || !dev_cores) return fail(ACI_ERR_INVALID, "tt_create_device: null argument");
   int st = validate_shape(L, d, ranks);
   if (st) return st;
   if ((st = check_device())) return st;
-  tt_s *t = tt_alloc_shape(L, d, ranks);
+  tt_s *t = tt_alloc_shape(L, d, ranks, cplx);
   if (cudaMalloc(&t->dcores, sizeof(double) * std::max<size_t>(t->total, 1)) != cudaSuccess) {
     delete t;
     return fail(ACI_ERR_OOM, "tt_create_device: cudaMalloc failed");
@@ -135,6 +148,16 @@ extern "C" int tt_create_device(int L, const int *d, const int *ranks, const dou
   }
   *out = t;
   return ACI_OK;
+}
+
+extern "C" int tt_create_device(int L, const int *d, const int *ranks, const double *dev_cores, void *stream,
+                                tt_t **out) {
+  return tt_create_device_impl(L, d, ranks, dev_cores, stream, 0, out);
+}
+
+extern "C" int tt_create_device_z(int L, const int *d, const int *ranks, const double *dev_cores, void *stream,
+                                  tt_t **out) {
+  return tt_create_device_impl(L, d, ranks, dev_cores, stream, 1, out);
 }
 
 extern "C" int tt_destroy(tt_t *t) {
@@ -205,30 +228,40 @@ struct InBond {
   int ldR;
   double *Abuf, *Bbuf;  // per-bond scratch of the half that depends on this sweep's pivots
   double *Apre, *Bpre;  // this bond's half that does not (computed for all bonds at half-sweep start)
+  const double *Xeb, *Xeb1;  // complex runs: expanded cores of sites b, b+1 (right operands)
   int c0, c1, c2;       // chi^n_b, chi^n_{b+1}, chi^n_{b+2}
 };
 struct BondStatic {
   int b, L, N, dir, db, db1;
+  int Z;                // 1 real, 2 complex (interleaved left operands, expanded right operands)
   int ldu;              // static ld of the U store (nmax[b])
   int maxrank;
   InBond in[ACI_GEMM_MAX_IN];
   double *Pi;
 };
 
+// Complex runs (S.Z = 2) use the same real GEMMs: a complex left operand (M x K) is read as the
+// real M x 2K matrix of its interleaved storage, a right operand is stored 2x2-block expanded
+// (2K x 2N), so K and N double; a2's result is written expanded (EPI_STORE_X, xd = d_{b+1}).
 // a1: A^n = L^n_{b-1} X^n_b : (rl x c0) (c0 x db*c1) -> rl x (db c1) == (rl db) x c1
 __device__ __forceinline__ GemmDesc desc_a(const BondStatic &S, const InBond &I, int rl, double *C) {
   GemmDesc a = {};
   if (!I.Lprev) return a;
-  a.C = C; a.M = rl; a.N = S.db * I.c1; a.ldc = S.db * I.c1; a.nin = 1;
-  a.A[0] = I.Lprev; a.lda[0] = I.c0; a.K[0] = I.c0; a.B[0] = I.Xb; a.ldb[0] = S.db * I.c1;
+  const int z = S.Z;
+  a.C = C; a.M = rl; a.N = z * S.db * I.c1; a.ldc = z * S.db * I.c1; a.nin = 1;
+  a.A[0] = I.Lprev; a.lda[0] = z * I.c0; a.K[0] = z * I.c0;
+  a.B[0] = z == 2 ? I.Xeb : I.Xb; a.ldb[0] = z * S.db * I.c1;
   return a;
 }
 // a2: B^n = X^n_{b+1} R^n_{b+2} : (c1 db1 x c2) (c2 x rr) -> (c1 db1) x rr == c1 x (db1 rr)
 __device__ __forceinline__ GemmDesc desc_b(const BondStatic &S, const InBond &I, int rr, double *C) {
   GemmDesc bb = {};
   if (!I.Rnext) return bb;
-  bb.C = C; bb.M = I.c1 * S.db1; bb.N = rr; bb.ldc = rr; bb.nin = 1;
-  bb.A[0] = I.Xb1; bb.lda[0] = I.c2; bb.K[0] = I.c2; bb.B[0] = I.Rnext; bb.ldb[0] = I.ldR;
+  const int z = S.Z;
+  bb.C = C; bb.M = I.c1 * S.db1; bb.N = z * rr; bb.nin = 1;
+  bb.ldc = z == 2 ? 2 * S.db1 * rr : rr;  // expanded c1 x (db1 rr) block matrix
+  bb.xd = S.db1;
+  bb.A[0] = I.Xb1; bb.lda[0] = z * I.c2; bb.K[0] = z * I.c2; bb.B[0] = I.Rnext; bb.ldb[0] = z * I.ldR;
   return bb;
 }
 
@@ -240,17 +273,18 @@ __device__ void plan_bond(const BondStatic &S, const int *rk, GemmDesc *ab, Gemm
   const int b = S.b;
   const int rl = rk[b], rr = rk[b + 2];
   const int m = rl * S.db, n = S.db1 * rr;
+  const int z = S.Z;
   GemmDesc P = {};
-  P.C = S.Pi; P.M = m; P.N = n; P.ldc = n; P.nin = S.N;
+  P.C = S.Pi; P.M = m; P.N = z * n; P.ldc = z * n; P.nin = S.N;
   for (int i = 0; i < S.N; ++i) {
     const InBond &I = S.in[i];
     ab[i] = S.dir == 0 ? desc_a(S, I, rl, I.Abuf) : desc_b(S, I, rr, I.Bbuf);
     // a3: Pi^n = A^n B^n : (m x c1) (c1 x n)
     P.A[i] = I.Lprev ? (S.dir == 0 ? I.Abuf : I.Apre) : I.Xb;
-    P.lda[i] = I.c1;
-    P.K[i] = I.c1;
-    P.B[i] = I.Rnext ? (S.dir == 0 ? I.Bpre : I.Bbuf) : I.Xb1;
-    P.ldb[i] = n;
+    P.lda[i] = z * I.c1;
+    P.K[i] = z * I.c1;
+    P.B[i] = I.Rnext ? (S.dir == 0 ? I.Bpre : I.Bbuf) : (z == 2 ? I.Xeb1 : I.Xb1);
+    P.ldb[i] = z * n;
   }
   *pi = P;
   LuDims D;
@@ -301,6 +335,7 @@ struct UpdateArgs {
   int *log_rows, *log_cols;   // cap_piv per slot
   const int *iter;
   int step, per_iter, cap_piv;
+  int Z;                      // 2: complex (L frames / A^n interleaved, R frames / B^n expanded)
   // plan of the next bond update (fused; null for the last update of an iteration)
   const BondStatic *next;
   GemmDesc *ab, *pi;
@@ -345,13 +380,13 @@ __global__ void update_bond_kernel(UpdateArgs U) {
   if (U.dir == 0) {
     for (int i = 0; i < U.N; ++i) {
       if (!U.Lnew[i]) continue;
-      const int c1 = U.c1[i];
+      const int c1 = U.c1[i] * U.Z;  // complex rows are 2 c1 doubles (interleaved)
       for (int t = gt; t < r * c1; t += gs) {
         const int k = t / c1, bb = t % c1;
         U.Lnew[i][t] = U.A[i][(size_t)U.rows[k] * c1 + bb];
       }
     }
-  } else {
+  } else if (U.Z == 1) {
     for (int i = 0; i < U.N; ++i) {
       if (!U.Rnew[i]) continue;
       const int c1 = U.c1[i];
@@ -365,6 +400,27 @@ __global__ void update_bond_kernel(UpdateArgs U) {
       for (int t = gt; t < m * r; t += gs) {
         const int ii = t / r, k = t % r;
         U.Y0[t] = U.Pi[(size_t)ii * n + U.cols[k]];
+      }
+    }
+  } else {
+    // complex: B^n and R frames are expanded (2 c1 x 2 n, ld 2 n / 2 ldRnew): copy the 2x2 blocks
+    for (int i = 0; i < U.N; ++i) {
+      if (!U.Rnew[i]) continue;
+      const int c1 = U.c1[i];
+      for (int t = gt; t < 2 * c1 * r; t += gs) {
+        const int a2 = t / r, k = t % r;
+        const double *src = U.B[i] + (size_t)a2 * 2 * n + 2 * U.cols[k];
+        double *dst = U.Rnew[i] + (size_t)a2 * 2 * U.ldRnew + 2 * k;
+        dst[0] = src[0];
+        dst[1] = src[1];
+      }
+    }
+    if (b == 0) {
+      const int m = rl * U.db;
+      for (int t = gt; t < m * r; t += gs) {
+        const int ii = t / r, k = t % r;
+        U.Y0[2 * t] = U.Pi[((size_t)ii * n + U.cols[k]) * 2];
+        U.Y0[2 * t + 1] = U.Pi[((size_t)ii * n + U.cols[k]) * 2 + 1];
       }
     }
   }
@@ -404,6 +460,7 @@ struct CanonArgs {
   double *Tbuf[ACI_GEMM_MAX_IN];
   int c0[ACI_GEMM_MAX_IN], c1[ACI_GEMM_MAX_IN];
   GemmDesc *tdesc;                // N descriptors
+  int Z;                          // 2: complex (R frames expanded, T interleaved)
 };
 
 __global__ void plan_canon_kernel(CanonArgs C, const int *rk) {
@@ -416,9 +473,9 @@ __global__ void plan_canon_kernel(CanonArgs C, const int *rk) {
   for (int i = 0; i < C.N; ++i) {
     GemmDesc g = {};
     if (C.Rnext[i]) {
-      g.C = C.Tbuf[i]; g.M = C.c0[i] * C.ds; g.N = jn; g.ldc = jn; g.nin = 1;
-      g.A[0] = C.Xs[i]; g.lda[0] = C.c1[i]; g.K[0] = C.c1[i];
-      g.B[0] = C.Rnext[i]; g.ldb[0] = C.ldR;
+      g.C = C.Tbuf[i]; g.M = C.c0[i] * C.ds; g.N = C.Z * jn; g.ldc = C.Z * jn; g.nin = 1;
+      g.A[0] = C.Xs[i]; g.lda[0] = C.Z * C.c1[i]; g.K[0] = C.Z * C.c1[i];
+      g.B[0] = C.Rnext[i]; g.ldb[0] = C.Z * C.ldR;
     }
     C.tdesc[i] = g;
   }
@@ -440,6 +497,7 @@ struct CanonUpd {
   GemmDesc *ydesc;
   int *canon_n;                          // log
   int *canon_cols;
+  int Z;                                 // 2: complex (Mp and R frames written expanded)
 };
 
 __global__ void canon_update_kernel(CanonUpd U) {
@@ -452,9 +510,9 @@ __global__ void canon_update_kernel(CanonUpd U) {
     U.rk[s] = r;  // |J_s| = rank of bond s-1; this kernel only reads rk[s+1]
     *U.canon_n = r;
     GemmDesc g = {};
-    g.C = U.Yabs_prev; g.M = U.yr_prev_rows; g.N = r; g.ldc = r; g.nin = 1;
-    g.A[0] = U.Yin_prev; g.lda[0] = U.yr_s; g.K[0] = U.yr_s;
-    g.B[0] = U.Mp; g.ldb[0] = r;
+    g.C = U.Yabs_prev; g.M = U.yr_prev_rows; g.N = U.Z * r; g.ldc = U.Z * r; g.nin = 1;
+    g.A[0] = U.Yin_prev; g.lda[0] = U.Z * U.yr_s; g.K[0] = U.Z * U.yr_s;
+    g.B[0] = U.Mp; g.ldb[0] = U.Z * r;
     *U.ydesc = g;
   }
   for (int k = gt; k < r; k += gs) U.canon_cols[k] = U.cols[k];
@@ -464,15 +522,38 @@ __global__ void canon_update_kernel(CanonUpd U) {
     const int col = U.cols[k];
     U.Jnew[t] = pos == 0 ? (uint8_t)(col / jn) : U.Jnext[(col % jn) * (wJ - 1) + pos - 1];
   }
+  if (U.Z == 1) {
+    for (int t = gt; t < U.yr_s * r; t += gs) {
+      const int a = t / r, k = t % r;
+      U.Mp[t] = U.M[(size_t)a * n + U.cols[k]];
+    }
+    for (int i = 0; i < U.N; ++i) {
+      const int c0 = U.c0[i];
+      for (int t = gt; t < c0 * r; t += gs) {
+        const int a = t / r, k = t % r;
+        U.Rnew[i][(size_t)a * U.ldRnew + k] = U.T[i][(size_t)a * n + U.cols[k]];
+      }
+    }
+    return;
+  }
+  // complex: gathered entries (re, im) written as 2x2 blocks [[re, im], [-im, re]]
+  auto put = [](double *E, size_t ld, int a, int k, double re, double im) {
+    E[(size_t)(2 * a) * ld + 2 * k] = re;
+    E[(size_t)(2 * a) * ld + 2 * k + 1] = im;
+    E[(size_t)(2 * a + 1) * ld + 2 * k] = -im;
+    E[(size_t)(2 * a + 1) * ld + 2 * k + 1] = re;
+  };
   for (int t = gt; t < U.yr_s * r; t += gs) {
     const int a = t / r, k = t % r;
-    U.Mp[t] = U.M[(size_t)a * n + U.cols[k]];
+    const double *x = U.M + ((size_t)a * n + U.cols[k]) * 2;
+    put(U.Mp, 2 * (size_t)r, a, k, x[0], x[1]);
   }
   for (int i = 0; i < U.N; ++i) {
     const int c0 = U.c0[i];
     for (int t = gt; t < c0 * r; t += gs) {
       const int a = t / r, k = t % r;
-      U.Rnew[i][(size_t)a * U.ldRnew + k] = U.T[i][(size_t)a * n + U.cols[k]];
+      const double *x = U.T[i] + ((size_t)a * n + U.cols[k]) * 2;
+      put(U.Rnew[i], 2 * (size_t)U.ldRnew, a, k, x[0], x[1]);
     }
   }
 }
@@ -534,6 +615,70 @@ __global__ void __launch_bounds__(64) tri_block_kernel(const TriArgs *args) {
 
 __global__ void copy_prev_kernel(const int *rk, int *prev, int L) {
   for (int b = threadIdx.x; b < L - 1; b += blockDim.x) prev[b] = rk[b + 1];
+}
+
+// ---- complex output cores: Y_{b+1} = U_J^{-1} U (Alg. 3 right branch, R5; products
+// as RZ5). One launch for every bond: a CTA owns 16 columns of one bond and keeps them in shared
+// memory; 8 lanes share each column's dot products (shuffle reduction), one barrier per row.
+struct ZTrsmArgs {
+  const double *U;  // complex U store (r x n, ld ldu complex)
+  int ldu;
+  const int *cols;
+  double *out;      // complex output core (r x n)
+  int r, n;
+};
+constexpr int kZTrsmCols = 16;
+__global__ void __launch_bounds__(128) ztrsm_kernel(const ZTrsmArgs *args) {
+  extern __shared__ double zb[];  // [r][kZTrsmCols][2]
+  const ZTrsmArgs A = args[blockIdx.y];
+  const int j0 = blockIdx.x * kZTrsmCols;
+  if (j0 >= A.n) return;
+  const int c = threadIdx.x >> 3, t = threadIdx.x & 7;
+  const int j = j0 + c;
+  for (int e = threadIdx.x; e < A.r * kZTrsmCols; e += blockDim.x) {
+    const int i = e / kZTrsmCols, cc = e % kZTrsmCols;
+    const bool ok = j0 + cc < A.n;
+    zb[2 * e] = ok ? A.U[((size_t)i * A.ldu + j0 + cc) * 2] : 0.0;
+    zb[2 * e + 1] = ok ? A.U[((size_t)i * A.ldu + j0 + cc) * 2 + 1] : 0.0;
+  }
+  __syncthreads();
+  for (int k = A.r - 1; k >= 0; --k) {
+    double sr = 0.0, si = 0.0;
+    for (int i = k + 1 + t; i < A.r; i += 8) {
+      const double *u = A.U + ((size_t)k * A.ldu + A.cols[i]) * 2;
+      const double br = zb[2 * (i * kZTrsmCols + c)], bi = zb[2 * (i * kZTrsmCols + c) + 1];
+      sr += u[0] * br - u[1] * bi;
+      si += u[0] * bi + u[1] * br;
+    }
+#pragma unroll
+    for (int o = 4; o; o >>= 1) {
+      sr += __shfl_xor_sync(0xffffffffu, sr, o);
+      si += __shfl_xor_sync(0xffffffffu, si, o);
+    }
+    if (t == 0) {
+      zb[2 * (k * kZTrsmCols + c)] -= sr;
+      zb[2 * (k * kZTrsmCols + c) + 1] -= si;
+    }
+    __syncthreads();
+  }
+  if (j < A.n)
+    for (int k = t; k < A.r; k += 8) {
+      A.out[((size_t)k * A.n + j) * 2] = zb[2 * (k * kZTrsmCols + c)];
+      A.out[((size_t)k * A.n + j) * 2 + 1] = zb[2 * (k * kZTrsmCols + c) + 1];
+    }
+}
+
+// 2x2-block expansion of a complex (rows x cols) matrix for use as a right GEMM operand.
+__global__ void expand_kernel(const double *X, double *E, int rows, int cols) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < rows * cols; t += gridDim.x * blockDim.x) {
+    const int a = t / cols, k = t % cols;
+    const double re = X[2 * (size_t)t], im = X[2 * (size_t)t + 1];
+    const size_t ld = 2 * (size_t)cols;
+    E[(2 * a) * ld + 2 * k] = re;
+    E[(2 * a) * ld + 2 * k + 1] = im;
+    E[(2 * a + 1) * ld + 2 * k] = -im;
+    E[(2 * a + 1) * ld + 2 * k + 1] = re;
+  }
 }
 
 // ============================================================================ host: workspace
@@ -603,11 +748,13 @@ struct Prof {
 
 struct Run {
   Prof *P = nullptr;
+  int cplx = 0, Z = 1, ZE = 1;  // complex run: Z = 2 doubles per entry, ZE = 4 for expanded operands
   int L = 0, N = 0, maxrank = 0, max_sweeps = 0, log_cap_upd = 0, log_cap_piv = 0, colcap = 0;
   std::vector<int> d, yr;
   std::vector<std::vector<int>> xr;      // [n][s], s = 0..L
   std::vector<const double *> xcore0;    // device base of input n
   std::vector<std::vector<size_t>> xoff; // [n][s]
+  std::vector<std::vector<double *>> Xe; // [n][s]: complex runs, 2x2-block expanded cores (GemmDesc::xd)
   std::vector<int> rmax, mmax, nmax;     // per bond
   // device
   int *rk = nullptr, *prev = nullptr, *rout = nullptr, *nonfinite = nullptr, *conv = nullptr, *iter = nullptr;
@@ -687,27 +834,35 @@ static size_t carve(Run &R, char *base) {
   R.Bbuf.assign(N, nullptr);
   for (int n = 0; n < N; ++n) {
     size_t acap = 1, bcap = 1;
+    // complex: left operands (L frames, A^n) interleaved (x Z), right operands (R frames, B^n)
+    // in 2x2-block expanded form (x ZE)
     for (int b = 0; b < L - 1; ++b) {
-      R.Lf[n][b] = c.take<double>((size_t)R.rmax[b] * R.xr[n][b + 1]);
+      R.Lf[n][b] = c.take<double>((size_t)R.rmax[b] * R.xr[n][b + 1] * R.Z);
       acap = std::max(acap, (size_t)R.mmax[b] * R.xr[n][b + 1]);
       bcap = std::max(bcap, (size_t)R.xr[n][b + 1] * R.nmax[b]);
     }
-    for (int s = 1; s < L; ++s) R.Rf[n][s] = c.take<double>((size_t)R.xr[n][s] * R.rmax[s - 1]);
-    R.Abuf[n] = c.take<double>(acap);
-    R.Bbuf[n] = c.take<double>(bcap);
+    for (int s = 1; s < L; ++s) R.Rf[n][s] = c.take<double>((size_t)R.xr[n][s] * R.rmax[s - 1] * R.ZE);
+    R.Abuf[n] = c.take<double>(acap * R.Z);
+    R.Bbuf[n] = c.take<double>(bcap * R.ZE);
   }
   R.Apre.assign(N, std::vector<double *>(L, nullptr));
   R.Bpre.assign(N, std::vector<double *>(L, nullptr));
   for (int n = 0; n < N; ++n) {
-    for (int b = 1; b < L - 1; ++b) R.Apre[n][b] = c.take<double>((size_t)R.rmax[b - 1] * R.d[b] * R.xr[n][b + 1]);
-    for (int b = 0; b + 2 < L; ++b) R.Bpre[n][b] = c.take<double>((size_t)R.xr[n][b + 1] * R.d[b + 1] * R.rmax[b + 1]);
+    for (int b = 1; b < L - 1; ++b)
+      R.Apre[n][b] = c.take<double>((size_t)R.rmax[b - 1] * R.d[b] * R.xr[n][b + 1] * R.Z);
+    for (int b = 0; b + 2 < L; ++b)
+      R.Bpre[n][b] = c.take<double>((size_t)R.xr[n][b + 1] * R.d[b + 1] * R.rmax[b + 1] * R.ZE);
+  }
+  R.Xe.assign(N, std::vector<double *>(L, nullptr));
+  for (int n = 0; n < N && R.cplx; ++n) {
+    for (int s = 0; s < L; ++s) R.Xe[n][s] = c.take<double>((size_t)R.xr[n][s] * R.d[s] * R.xr[n][s + 1] * 4);
   }
   size_t picap = 1;
   for (int b = 0; b < L - 1; ++b) picap = std::max(picap, (size_t)R.mmax[b] * R.nmax[b]);
-  R.Pi = c.take<double>(picap);
+  R.Pi = c.take<double>(picap * R.Z);
   R.Ust.assign(L, nullptr);
-  for (int b = 0; b < L - 1; ++b) R.Ust[b] = c.take<double>((size_t)R.rmax[b] * R.nmax[b]);
-  R.Y0 = c.take<double>(L > 1 ? (size_t)R.mmax[0] * R.rmax[0] : 1);
+  for (int b = 0; b < L - 1; ++b) R.Ust[b] = c.take<double>((size_t)R.rmax[b] * R.nmax[b] * R.Z);
+  R.Y0 = c.take<double>(L > 1 ? (size_t)R.mmax[0] * R.rmax[0] * R.Z : 1);
   R.Imi.assign(L, nullptr);
   R.Jmi.assign(L + 1, nullptr);
   for (int b = 0; b < L - 1; ++b) R.Imi[b] = c.take<uint8_t>((size_t)R.rmax[b] * (b + 1));
@@ -716,11 +871,11 @@ static size_t carve(Run &R, char *base) {
   R.Yabs.assign(L, nullptr);
   size_t mpcap = 1;
   for (int s = 0; s < L; ++s) {
-    R.Yin[s] = c.take<double>((size_t)R.yr[s] * R.d[s] * R.yr[s + 1]);
-    if (s < L - 1) R.Yabs[s] = c.take<double>((size_t)R.yr[s] * R.d[s] * R.rmax[s]);
+    R.Yin[s] = c.take<double>((size_t)R.yr[s] * R.d[s] * R.yr[s + 1] * R.Z);
+    if (s < L - 1) R.Yabs[s] = c.take<double>((size_t)R.yr[s] * R.d[s] * R.rmax[s] * R.Z);
     if (s >= 1) mpcap = std::max(mpcap, (size_t)R.yr[s] * R.rmax[s - 1]);
   }
-  R.Mp = c.take<double>(mpcap);
+  R.Mp = c.take<double>(mpcap * R.ZE);
   R.dAB = c.take<GemmDesc>(2 * ACI_GEMM_MAX_IN);
   R.dStat = c.take<BondStatic>(2 * std::max(L - 1, 1));
   R.dPre = c.take<GemmDesc>((size_t)std::max(L - 1, 1) * N);
@@ -742,7 +897,7 @@ static size_t carve(Run &R, char *base) {
   R.UJ.assign(L, nullptr);
   size_t nblk = 0;
   for (int b = 0; b < L - 1; ++b) {
-    R.UJ[b] = c.take<double>((size_t)R.rmax[b] * R.rmax[b]);
+    R.UJ[b] = c.take<double>((size_t)R.rmax[b] * R.rmax[b] * R.Z);
     nblk += (R.rmax[b] + 63) / 64;
   }
   R.dtgemm = c.take<GemmDesc>(nblk);
@@ -776,6 +931,7 @@ static int prepare(aci_op op, const tt_t *const *inputs, int n_inputs, Inputs &I
   const tt_s *t0 = I.tts[0];
   for (int j = 1; j < N; ++j) {
     if (I.tts[j]->L != t0->L || I.tts[j]->d != t0->d) return fail(ACI_ERR_SHAPE, "aci: inputs differ in L or d (S:253)");
+    if (I.tts[j]->cplx != t0->cplx) return fail(ACI_ERR_SHAPE, "aci: inputs mix real and complex TTs");
   }
   std::memset(&I.op, 0, sizeof(I.op));
   I.op.T = op.n_terms;
@@ -865,7 +1021,7 @@ static std::vector<uint64_t> graph_key(const Run &R, const FOp &op, double tol, 
     u(b);
   };
   u((uint64_t)(uintptr_t)ws); u(need); u((uint64_t)(uintptr_t)st);
-  u(R.L); u(R.N); u(R.maxrank); u(R.log_cap_upd); u(R.log_cap_piv); u(R.colcap);
+  u(R.L); u(R.N); u(R.maxrank); u(R.log_cap_upd); u(R.log_cap_piv); u(R.colcap); u(R.cplx);
   dbl(tol); u(tol_mode);
   for (int x : R.d) u(x);
   for (int x : R.yr) u(x);
@@ -896,11 +1052,12 @@ static void launch_update(Run &R, int b, int dir, int logslot, const BondStatic 
     const bool has_L = b > 0, has_R = b + 2 < R.L;
     U.A[n] = has_L ? R.Abuf[n] : R.xcore0[n] + R.xoff[n][b];
     U.Lnew[n] = R.Lf[n][b];
-    U.B[n] = has_R ? R.Bbuf[n] : R.xcore0[n] + R.xoff[n][b + 1];
+    U.B[n] = has_R ? R.Bbuf[n] : (R.cplx ? R.Xe[n][b + 1] : R.xcore0[n] + R.xoff[n][b + 1]);
     U.Rnew[n] = R.Rf[n][b + 1];
     U.c1[n] = R.xr[n][b + 1];
   }
   U.ldRnew = R.rmax[b];
+  U.Z = R.Z;
   U.Pi = R.Pi;
   U.Y0 = R.Y0;
   U.maxeps_bits = R.maxeps;
@@ -930,6 +1087,7 @@ static void build_statics(Run &R, const FOp &op) {
     for (int b = 0; b < nb; ++b) {
       BondStatic &S = R.hStat[dir * nb + b];
       S.b = b; S.L = L; S.N = N; S.dir = dir; S.db = R.d[b]; S.db1 = R.d[b + 1];
+      S.Z = R.Z;
       S.ldu = R.nmax[b];
       S.maxrank = R.maxrank;
       S.Pi = R.Pi;
@@ -937,10 +1095,11 @@ static void build_statics(Run &R, const FOp &op) {
       // main loop (first), tiny ones (e.g. rank-2 inputs) are evaluated in the epilogue; the op's
       // exponents are permuted to the same order.
       int order[ACI_GEMM_MAX_IN], nbig = 0, nsmall = 0;
+      // (complex runs: every input through the DMMA main loop)
       for (int n = 0; n < N; ++n)
-        if (R.xr[n][b + 1] > gemm_small_k()) order[nbig++] = n;
+        if (R.cplx || R.xr[n][b + 1] > gemm_small_k()) order[nbig++] = n;
       for (int n = 0; n < N; ++n)
-        if (R.xr[n][b + 1] <= gemm_small_k()) order[nbig + nsmall++] = n;
+        if (!R.cplx && R.xr[n][b + 1] <= gemm_small_k()) order[nbig + nsmall++] = n;
       R.nbig[dir * nb + b] = nbig;
       R.nsmall[dir * nb + b] = nsmall;
       FOp &ob = R.opb[dir * nb + b];
@@ -959,6 +1118,8 @@ static void build_statics(Run &R, const FOp &op) {
         I.Bbuf = R.Bbuf[n];
         I.Apre = R.Apre[n][b];
         I.Bpre = R.Bpre[n][b];
+        I.Xeb = R.Xe[n][b];
+        I.Xeb1 = R.Xe[n][b + 1];
       }
     }
 }
@@ -979,7 +1140,10 @@ static void pre_launch(Run &R, int dir, cudaStream_t st) {
   R.P->begin(ACI_PROF_GEMM_AB);
   plan_pre_kernel<<<1, 256, 0, st>>>(dstat(R, dir, 0), L - 1, N, R.rk, R.dPre);
   FOp dummy = {};
-  launch_gemm(R.dPre, (L - 1) * N, pm, pn, 1, false, dummy, nullptr, nullptr, st);
+  if (R.cplx)
+    launch_gemm_z(R.dPre, (L - 1) * N, pm, 2 * pn, dir == 0 ? 1 : 0, 1, dummy, nullptr, nullptr, st);
+  else
+    launch_gemm(R.dPre, (L - 1) * N, pm, pn, 1, false, dummy, nullptr, nullptr, st);
   R.P->end(2);
 }
 
@@ -1001,11 +1165,18 @@ static void bond_update(Run &R, double tol, int tol_mode, int b, int dir, int lo
   if (ab_m > 0) {
     R.P->begin(ACI_PROF_GEMM_AB);
     FOp dummy = {};
-    launch_gemm(R.dAB, N, ab_m, ab_n, 1, false, dummy, nullptr, nullptr, st);
+    if (R.cplx)
+      launch_gemm_z(R.dAB, N, ab_m, 2 * ab_n, dir == 0 ? 0 : 1, 1, dummy, nullptr, nullptr, st);
+    else
+      launch_gemm(R.dAB, N, ab_m, ab_n, 1, false, dummy, nullptr, nullptr, st);
     R.P->end(1);
   }
   R.P->begin(ACI_PROF_GEMM_PI);
-  launch_gemm_split(R.dPi, 1, R.mmax[b], R.nmax[b], R.nbig[k], R.nsmall[k], true, R.opb[k], R.scale, R.nonfinite, st);
+  if (R.cplx)
+    launch_gemm_z(R.dPi, 1, R.mmax[b], 2 * R.nmax[b], 2, N, R.opb[k], R.scale, R.nonfinite, st);
+  else
+    launch_gemm_split(R.dPi, 1, R.mmax[b], R.nmax[b], R.nbig[k], R.nsmall[k], true, R.opb[k], R.scale, R.nonfinite,
+                      st);
   R.P->end(1);
   LuArgs a = {};
   a.M = R.Pi; a.dims = R.dLu; a.tol = tol; a.thr_mode = tol_mode == ACI_TOL_RELATIVE ? 0 : 2;
@@ -1014,7 +1185,7 @@ static void bond_update(Run &R, double tol, int tol_mode, int b, int dir, int lo
   a.U = dir == 1 ? R.Ust[b] : nullptr;
   a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter; a.epoch = R.epoch;
   R.P->begin(ACI_PROF_PRRLU);
-  launch_prrlu(a, R.mmax[b], R.nmax[b], st);
+  launch_prrlu(a, R.mmax[b], R.nmax[b], st, R.cplx != 0);
   R.P->end(1);
   R.P->begin(ACI_PROF_UPDATE);
   launch_update(R, b, dir, logslot, next, st);
@@ -1030,6 +1201,7 @@ static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st)
   C.maxrank = R.rmax[s - 1];  // R9': canonical J_s never exceeds the full-tensor bond bound
   C.ldR = s + 1 < L ? R.rmax[s] : 1;
   C.tdesc = R.dT;
+  C.Z = R.Z;
   int tm = 0, tn = 0;
   for (int n = 0; n < N; ++n) {
     C.Xs[n] = R.xcore0[n] + R.xoff[n][s];
@@ -1042,7 +1214,10 @@ static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st)
   R.P->begin(ACI_PROF_CANON);
   plan_canon_kernel<<<1, 1, 0, st>>>(C, R.rk);
   FOp dummy = {};
-  if (tm > 0) launch_gemm(R.dT, N, tm, tn, 1, false, dummy, nullptr, nullptr, st);
+  if (tm > 0) {
+    if (R.cplx) launch_gemm_z(R.dT, N, tm, 2 * tn, 0, 1, dummy, nullptr, nullptr, st);
+    else launch_gemm(R.dT, N, tm, tn, 1, false, dummy, nullptr, nullptr, st);
+  }
   const int max_m = R.yr[s], max_n = R.nmax[s - 1];
   LuArgs a = {};
   a.M = C.M; a.dims = R.dLu; a.tol = tol; a.thr_mode = tol_mode == ACI_TOL_RELATIVE ? 1 : 2;
@@ -1050,7 +1225,7 @@ static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st)
   a.rows = R.prow[s - 1]; a.cols = R.pcol[s - 1]; a.r_out = R.rout + (s - 1); a.eps_out = R.epsb + (s - 1);
   a.U = nullptr;
   a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter; a.epoch = R.epoch;
-  launch_prrlu(a, max_m, max_n, st);
+  launch_prrlu(a, max_m, max_n, st, R.cplx != 0);
   CanonUpd U = {};
   U.s = s; U.L = L; U.N = N; U.ds = R.d[s]; U.yr_s = R.yr[s]; U.yr_prev_rows = R.yr[s - 1] * R.d[s - 1];
   U.cols = R.pcol[s - 1]; U.r_in = R.rout + (s - 1);
@@ -1070,8 +1245,12 @@ static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st)
   U.ydesc = R.dY;
   U.canon_n = R.canon_n + s;
   U.canon_cols = R.canon_cols + (size_t)s * R.log_cap_piv;
+  U.Z = R.Z;
   canon_update_kernel<<<64, 256, 0, st>>>(U);
-  launch_gemm(R.dY, 1, R.yr[s - 1] * R.d[s - 1], R.rmax[s - 1], 1, false, dummy, nullptr, nullptr, st);
+  if (R.cplx)
+    launch_gemm_z(R.dY, 1, R.yr[s - 1] * R.d[s - 1], 2 * R.rmax[s - 1], 0, 1, dummy, nullptr, nullptr, st);
+  else
+    launch_gemm(R.dY, 1, R.yr[s - 1] * R.d[s - 1], R.rmax[s - 1], 1, false, dummy, nullptr, nullptr, st);
   R.P->end(4 + (tm > 0 ? 1 : 0));
 }
 
@@ -1099,6 +1278,9 @@ static int build_run(const Inputs &I, const tt_s *y, int maxrank, int max_sweeps
     R.xoff[n] = I.tts[n]->off;
   }
   R.yr = y->ranks;
+  R.cplx = t0->cplx;
+  R.Z = R.cplx ? 2 : 1;
+  R.ZE = R.cplx ? 4 : 1;
   plan_capacities(R);
   R.log_cap_upd = 2 * std::max(R.L - 1, 1) * max_sweeps;
   R.log_cap_piv = 1;
@@ -1106,13 +1288,14 @@ static int build_run(const Inputs &I, const tt_s *y, int maxrank, int max_sweeps
   R.colcap = 32;
   for (int b = 0; b < R.L - 1; ++b) R.colcap = std::max(R.colcap, R.mmax[b]);
   for (int s = 0; s < R.L; ++s) R.colcap = std::max(R.colcap, R.yr[s]);
+  R.colcap *= R.Z;
   // envelope
   for (int b = 0; b < R.L - 1; ++b)
-    if (!prrlu_supported(R.mmax[b], R.nmax[b]))
+    if (!prrlu_supported(R.mmax[b], R.nmax[b], R.cplx != 0))
       return fail(ACI_ERR_UNSUPPORTED, "aci: 2-site block " + std::to_string(R.mmax[b]) + "x" +
                                            std::to_string(R.nmax[b]) + " exceeds the prrLU envelope");
   for (int s = 1; s < R.L; ++s)
-    if (!prrlu_supported(R.yr[s], R.nmax[s - 1]))
+    if (!prrlu_supported(R.yr[s], R.nmax[s - 1], R.cplx != 0))
       return fail(ACI_ERR_UNSUPPORTED, "aci: y_init bond too large for the prrLU envelope");
   return ACI_OK;
 }
@@ -1142,6 +1325,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   const tt_s *y = o.y_init;
   if (y) {
     if (y->L != L || y->d != t0->d) return fail(ACI_ERR_SHAPE, "aci: y_init shape differs from the inputs");
+    if (y->cplx != t0->cplx) return fail(ACI_ERR_SHAPE, "aci: y_init must be complex iff the inputs are");
   } else {
     std::vector<int> yr(L + 1, 1);
     for (int s = 1; s < L; ++s) {
@@ -1153,11 +1337,12 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
     std::vector<const double *> ptr(L);
     uint64_t cnt = 0;
     for (int s = 0; s < L; ++s) {
-      cores[s].resize((size_t)yr[s] * t0->d[s] * yr[s + 1]);
+      cores[s].resize((size_t)yr[s] * t0->d[s] * yr[s + 1] * (t0->cplx ? 2 : 1));
       for (auto &x : cores[s]) x = normal_at(o.seed, cnt++);
       ptr[s] = cores[s].data();
     }
-    st = tt_create(L, t0->d.data(), yr.data(), ptr.data(), &ygen);
+    st = t0->cplx ? tt_create_z(L, t0->d.data(), yr.data(), ptr.data(), &ygen)
+                  : tt_create(L, t0->d.data(), yr.data(), ptr.data(), &ygen);
     if (st) return st;
     y = ygen;
   }
@@ -1223,6 +1408,14 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   for (int s = 0; s < L; ++s)
     cudaMemcpyAsync(R.Yin[s], y->dcores + y->off[s], sizeof(double) * (y->off[s + 1] - y->off[s]),
                     cudaMemcpyDeviceToDevice, strm);
+  if (R.cplx) {
+    // right-operand copies of the input cores (core s viewed chi_s x (d_s chi_{s+1}))
+    prof.begin(ACI_PROF_CANON);
+    for (int n = 0; n < R.N; ++n)
+      for (int s = 0; s < L; ++s)
+        expand_kernel<<<64, 256, 0, strm>>>(R.xcore0[n] + R.xoff[n][s], R.Xe[n][s], R.xr[n][s], R.d[s] * R.xr[n][s + 1]);
+    prof.end(R.N * L);
+  }
 
   // ---- a0: CI-canonicalise y_init, right-to-left
   for (int s = L - 1; s >= 1; --s) canon_step(R, tol, o.tol_mode, s, strm);
@@ -1308,14 +1501,35 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   if (nonfinite) { cleanup(); return fail(ACI_ERR_NONFINITE, "aci: f produced NaN/Inf (S:255)"); }
 
   // ---- a8: output cores from the last right-to-left half-sweep (R5)
-  tt_s *res = tt_alloc_shape(L, t0->d.data(), rk.data());
+  tt_s *res = tt_alloc_shape(L, t0->d.data(), rk.data(), R.cplx);
   if (cudaMalloc(&res->dcores, sizeof(double) * std::max<size_t>(res->total, 1)) != cudaSuccess) {
     delete res;
     cleanup();
     return fail(ACI_ERR_OOM, "aci: output allocation failed");
   }
   cudaMemcpyAsync(res->dcores, R.Y0, sizeof(double) * (res->off[1] - res->off[0]), cudaMemcpyDeviceToDevice, strm);
-  {
+  if (R.cplx) {
+    std::vector<ZTrsmArgs> za(L - 1);
+    int nmx = 1, rmx = 1;
+    for (int b = 0; b < L - 1; ++b) {
+      za[b] = ZTrsmArgs{R.Ust[b], R.nmax[b], R.pcol[b], res->dcores + res->off[b + 1], rk[b + 1], R.d[b + 1] * rk[b + 2]};
+      nmx = std::max(nmx, za[b].n);
+      rmx = std::max(rmx, za[b].r);
+    }
+    cudaMemcpyAsync(R.dtrsm, za.data(), sizeof(ZTrsmArgs) * za.size(), cudaMemcpyHostToDevice, strm);
+    const int smem = rmx * kZTrsmCols * 2 * (int)sizeof(double);
+    cudaFuncSetAttribute(ztrsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    prof.begin(ACI_PROF_TRSM);
+    ztrsm_kernel<<<dim3((nmx + kZTrsmCols - 1) / kZTrsmCols, L - 1), 128, smem, strm>>>(
+        reinterpret_cast<const ZTrsmArgs *>(R.dtrsm));
+    prof.end(1);
+    e = cudaStreamSynchronize(strm);
+    if (e != cudaSuccess) {
+      tt_destroy(res);
+      cleanup();
+      return fail(ACI_ERR_CUDA, std::string("aci output: ") + cudaGetErrorString(e));
+    }
+  } else {
     // Blocked back substitution B = U_J^{-1} U (64-row blocks from the bottom): per step one
     // batched DMMA GEMM B[R] = U[R] - U_J[R, below] B[below] over all bonds, then the diagonal
     // block solve. The final ranks are known on the host here, so descriptors are built here.
@@ -1395,14 +1609,16 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
     const int m = rl * R.d[b], n = R.d[b + 1] * rr;
     for (int i = 0; i < R.N; ++i) {
       const double c0 = R.xr[i][b], c1 = R.xr[i][b + 1], c2 = R.xr[i][b + 2];
-      rp.flops_contraction += 2.0 * rl * c0 * R.d[b] * c1 + 2.0 * c1 * R.d[b + 1] * c2 * rr + 2.0 * m * c1 * n;
+      // complex: 4 real products per complex product (RZ5)
+      rp.flops_contraction +=
+          R.ZE * (2.0 * rl * c0 * R.d[b] * c1 + 2.0 * c1 * R.d[b + 1] * c2 * rr + 2.0 * m * c1 * n);
     }
-    for (int k = 0; k < r; ++k) rp.flops_prrlu += 2.0 * (m - k - 1) * (double)(n - k - 1);
+    for (int k = 0; k < r; ++k) rp.flops_prrlu += R.ZE * 2.0 * (m - k - 1) * (double)(n - k - 1);
     rp.pivot_steps += r;
   }
   for (int b = 0; b < L - 1; ++b) {
     const double r = rk[b + 1], n = R.d[b + 1] * rk[b + 2];
-    rp.flops_trsm += r * r * (n - r);
+    rp.flops_trsm += R.ZE * r * r * (n - r);
   }
   if (o.log) {
     aci_pivot_log *lg = o.log;
@@ -1489,34 +1705,47 @@ extern "C" int tt_evaluate_device(const tt_t *t, int64_t npts, const uint8_t *de
   if (npts == 0) return ACI_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const int L = t->L;
+  // complex TTs: the same real pipeline on interleaved vectors (ranks x 2) against 2x2-block
+  // expanded cores
+  const int z = t->cplx ? 2 : 1;
   int rmx = 1, wmx = 1;
+  size_t emx = 1;
   for (int s = 0; s < L; ++s) {
-    rmx = std::max(rmx, t->ranks[s + 1]);
-    wmx = std::max(wmx, t->d[s] * t->ranks[s + 1]);
+    rmx = std::max(rmx, z * t->ranks[s + 1]);
+    wmx = std::max(wmx, z * t->d[s] * t->ranks[s + 1]);
+    emx = std::max(emx, (size_t)4 * t->ranks[s] * t->d[s] * t->ranks[s + 1]);
   }
   const int64_t P = 8192;
-  double *V = nullptr, *W = nullptr;
+  double *V = nullptr, *W = nullptr, *E = nullptr;
   GemmDesc *desc = nullptr;
   if (cudaMallocAsync((void **)&V, sizeof(double) * P * rmx, st) != cudaSuccess ||
       cudaMallocAsync((void **)&W, sizeof(double) * P * wmx, st) != cudaSuccess ||
-      cudaMallocAsync((void **)&desc, sizeof(GemmDesc), st) != cudaSuccess)
+      cudaMallocAsync((void **)&desc, sizeof(GemmDesc), st) != cudaSuccess ||
+      (t->cplx && cudaMallocAsync((void **)&E, sizeof(double) * emx * L, st) != cudaSuccess))
     return fail(ACI_ERR_OOM, "tt_evaluate: workspace");
+  std::vector<size_t> eoff(L + 1, 0);
+  for (int s = 0; s < L; ++s) eoff[s + 1] = eoff[s] + (t->cplx ? (size_t)4 * t->ranks[s] * t->d[s] * t->ranks[s + 1] : 0);
+  if (t->cplx)
+    for (int s = 1; s < L; ++s)
+      expand_kernel<<<64, 256, 0, st>>>(t->dcores + t->off[s], E + eoff[s], t->ranks[s], t->d[s] * t->ranks[s + 1]);
   FOp dummy = {};
   for (int64_t p0 = 0; p0 < npts; p0 += P) {
     const int np = (int)std::min<int64_t>(P, npts - p0);
     const uint8_t *ix = dev_idx + p0 * L;
-    eval_first_kernel<<<296, 256, 0, st>>>(t->dcores, V, ix, L, t->ranks[1], np);
+    eval_first_kernel<<<296, 256, 0, st>>>(t->dcores, V, ix, L, z * t->ranks[1], np);
     for (int s = 1; s < L; ++s) {
       const int r0 = t->ranks[s], r1 = t->ranks[s + 1];
-      eval_desc_kernel<<<1, 1, 0, st>>>(desc, V, t->dcores + t->off[s], W, np, r0, t->d[s] * r1);
-      launch_gemm(desc, 1, np, t->d[s] * r1, 1, false, dummy, nullptr, nullptr, st);
-      eval_select_kernel<<<592, 256, 0, st>>>(W, V, ix, L, s, t->d[s], r1, np);
+      const double *X = t->cplx ? E + eoff[s] : t->dcores + t->off[s];
+      eval_desc_kernel<<<1, 1, 0, st>>>(desc, V, X, W, np, z * r0, z * t->d[s] * r1);
+      launch_gemm(desc, 1, np, z * t->d[s] * r1, 1, false, dummy, nullptr, nullptr, st);
+      eval_select_kernel<<<592, 256, 0, st>>>(W, V, ix, L, s, t->d[s], z * r1, np);
     }
-    cudaMemcpyAsync(dev_out + p0, V, sizeof(double) * np, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(dev_out + z * p0, V, sizeof(double) * np * z, cudaMemcpyDeviceToDevice, st);
   }
   cudaFreeAsync(V, st);
   cudaFreeAsync(W, st);
   cudaFreeAsync(desc, st);
+  if (E) cudaFreeAsync(E, st);
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return fail(ACI_ERR_CUDA, std::string("tt_evaluate: ") + cudaGetErrorString(e));
   return ACI_OK;
@@ -1531,12 +1760,13 @@ extern "C" int tt_evaluate(const tt_t *t, int64_t npts, const uint8_t *idx, doub
       if (idx[p * L + s] >= t->d[s]) return fail(ACI_ERR_INVALID, "tt_evaluate: index >= d_s");
   uint8_t *di = nullptr;
   double *dout = nullptr;
+  const size_t nout = (size_t)npts * (t->cplx ? 2 : 1);
   CUDA_TRY(cudaMalloc(&di, (size_t)npts * L));
-  if (cudaMalloc(&dout, sizeof(double) * npts) != cudaSuccess) { cudaFree(di); return fail(ACI_ERR_OOM, "tt_evaluate"); }
+  if (cudaMalloc(&dout, sizeof(double) * nout) != cudaSuccess) { cudaFree(di); return fail(ACI_ERR_OOM, "tt_evaluate"); }
   cudaMemcpy(di, idx, (size_t)npts * L, cudaMemcpyHostToDevice);
   int st = tt_evaluate_device(t, npts, di, dout, nullptr);
   if (st == ACI_OK) {
-    cudaError_t e = cudaMemcpy(out, dout, sizeof(double) * npts, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(out, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) st = fail(ACI_ERR_CUDA, cudaGetErrorString(e));
   }
   cudaFree(di);

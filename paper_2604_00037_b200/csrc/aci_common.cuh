@@ -17,6 +17,12 @@ struct GemmDesc {
   const double *A[ACI_GEMM_MAX_IN];
   const double *B[ACI_GEMM_MAX_IN];
   int K[ACI_GEMM_MAX_IN], lda[ACI_GEMM_MAX_IN], ldb[ACI_GEMM_MAX_IN];
+  // complex GEMMs run as real GEMMs on interleaved (re, im) storage against a right operand in
+  // 2x2-block EXPANDED form (row 2k: re, im; row 2k+1: -im, re), so that
+  // [a_re a_im] [[b_re, b_im], [-b_im, b_re]] = [re(ab), im(ab)].
+  // EPI_STORE_X writes the complex result C ((K' xd) x n, viewed K' x (xd n)) in expanded form:
+  // row i -> block row i / xd, column block (i % xd) n + j; ldc is the expanded leading dim.
+  int xd;
 };
 
 // Elementwise f = sum_t coef[t] prod_n x_n^expo[t][n].
@@ -65,13 +71,18 @@ void launch_gemm_split(const GemmDesc *d_descs, int ndesc, int max_m, int max_n,
 int gemm_small_k();
 // Sets kernel attributes (dynamic shared memory) once; call before any stream capture.
 void gemm_init();
+// Complex GEMMs (interleaved storage, expanded right operand): mode 0 = plain store, 1 = expanded
+// store (GemmDesc::xd), 2 = complex f of nin inputs (max |Pi| into sb, NaN flag into nf).
+void launch_gemm_z(const GemmDesc *d, int ndesc, int max_m, int max_n, int mode, int nin, const FOp &op,
+                   unsigned long long *sb, int *nf, cudaStream_t st);
 // C = S - A B for every descriptor (blocked triangular solve updates).
 void launch_gemm_sub(const GemmDesc *d_descs, int ndesc, int max_m, int max_n, cudaStream_t st);
 
 // Picks the tier for a (max_m x max_n) problem; returns false if it is out of the envelope.
-bool prrlu_supported(int max_m, int max_n);
+bool prrlu_supported(int max_m, int max_n, bool cplx = false);
 size_t prrlu_exchange_bytes(int max_m, int max_n);
-void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st);
+// cplx: complex entries (interleaved; ldm/ldu in complex elements; colcap >= 2 m).
+void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx = false);
 // Chooses the prrLU exchange tier (cluster size) once; call before any stream capture.
 void prrlu_init();
 void prrlu_envelope(int *max_rows, int *max_cols);

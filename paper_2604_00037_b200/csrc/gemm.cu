@@ -34,6 +34,11 @@ void gemm_init() {
   set_attr<CfgPi, 0, 2, EPI_F>();
   set_attr<CfgPi, 1, 2, EPI_F>();
   set_attr<CfgPi, 0, 3, EPI_F>();
+  set_attr<CfgAB, 1, 0, EPI_STORE_X>();
+  set_attr<CfgPi, 1, 0, EPI_FZ>();
+  set_attr<CfgPi, 2, 0, EPI_FZ>();
+  set_attr<CfgPi, 3, 0, EPI_FZ>();
+  set_attr<CfgPi, 4, 0, EPI_FZ>();
   done = true;
 }
 
@@ -67,6 +72,23 @@ void launch_gemm_split(const GemmDesc *d, int ndesc, int max_m, int max_n, int n
     case 12: launch_pi<1, 2>(d, ndesc, max_m, max_n, op, sb, nf, st); break;
     case 3: launch_pi<0, 3>(d, ndesc, max_m, max_n, op, sb, nf, st); break;
     default: break;
+  }
+}
+
+void launch_gemm_z(const GemmDesc *d, int ndesc, int max_m, int max_n, int mode, int nin, const FOp &op,
+                   unsigned long long *sb, int *nf, cudaStream_t st) {
+  if (max_m <= 0 || max_n <= 0 || ndesc <= 0) return;
+  if (mode == 0) {
+    launch<CfgAB, 1, 0, EPI_STORE>(d, ndesc, max_m, max_n, op, sb, nf, st);
+  } else if (mode == 1) {
+    launch<CfgAB, 1, 0, EPI_STORE_X>(d, ndesc, max_m, max_n, op, sb, nf, st);
+  } else {
+    switch (nin) {
+      case 1: launch<CfgPi, 1, 0, EPI_FZ>(d, ndesc, max_m, max_n, op, sb, nf, st); break;
+      case 2: launch<CfgPi, 2, 0, EPI_FZ>(d, ndesc, max_m, max_n, op, sb, nf, st); break;
+      case 3: launch<CfgPi, 3, 0, EPI_FZ>(d, ndesc, max_m, max_n, op, sb, nf, st); break;
+      default: launch<CfgPi, 4, 0, EPI_FZ>(d, ndesc, max_m, max_n, op, sb, nf, st); break;
+    }
   }
 }
 

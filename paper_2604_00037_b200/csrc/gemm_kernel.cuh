@@ -18,7 +18,9 @@
 namespace gemmk {
 
 constexpr int kSmallK = 4;
-enum { EPI_STORE = 0, EPI_F = 1, EPI_SUB = 2 };
+// EPI_STORE_X: complex result written in expanded form (GemmDesc::xd); EPI_FZ: complex f (every
+// input through the DMMA main loop; each thread's accumulator pair (2c, 2c+1) is one complex entry)
+enum { EPI_STORE = 0, EPI_F = 1, EPI_SUB = 2, EPI_STORE_X = 3, EPI_FZ = 4 };
 
 template <int BM_, int BN_, int WM_, int WN_, int BK_, int ST_, int MINB_>
 struct Cfg {
@@ -258,6 +260,65 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB)
           }
         }
       }
+  } else if (EPI == EPI_FZ) {
+    // f = sum_t coef_t prod_n x_n^{e_tn} on complex values (RZ6); |z| = sqrt(re^2 + im^2) (RZ1)
+    const bool mono = op.monomial_all_ones != 0;
+#pragma unroll
+    for (int mi = 0; mi < CF::MI; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < CF::NI; ++ni) {
+        const int row = m0 + wm + mi * 8 + g, col0 = n0 + wn + ni * 8 + 2 * c;
+        double yr = 0.0, yi = 0.0;
+        if (mono) {
+          yr = op.coef[0];
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            const double xr = acc[i][mi][ni][0], xi = acc[i][mi][ni][1];
+            const double t1 = __dmul_rn(yr, xr), t2 = __dmul_rn(yi, xi), t3 = __dmul_rn(yr, xi), t4 = __dmul_rn(yi, xr);
+            yr = __dsub_rn(t1, t2);
+            yi = __dadd_rn(t3, t4);
+          }
+        } else {
+          for (int t = 0; t < op.T; ++t) {
+            double pr = op.coef[t], pi = 0.0;
+#pragma unroll
+            for (int i = 0; i < NB; ++i)
+              for (int q = 0; q < op.expo[t * op.N + i]; ++q) {
+                const double xr = acc[i][mi][ni][0], xi = acc[i][mi][ni][1];
+                const double t1 = __dmul_rn(pr, xr), t2 = __dmul_rn(pi, xi), t3 = __dmul_rn(pr, xi), t4 = __dmul_rn(pi, xr);
+                pr = __dsub_rn(t1, t2);
+                pi = __dadd_rn(t3, t4);
+              }
+            yr += pr;
+            yi += pi;
+          }
+        }
+        bad |= !isfinite(yr) || !isfinite(yi);
+        vmax = fmax(vmax, __dsqrt_rn(__dadd_rn(__dmul_rn(yr, yr), __dmul_rn(yi, yi))));
+        if (row < M && col0 + 1 < N) {
+          double *dst = D.C + (size_t)row * D.ldc + col0;
+          dst[0] = yr;
+          dst[1] = yi;
+        }
+      }
+  } else if (EPI == EPI_STORE_X) {
+    const int nc = N >> 1;  // complex columns
+#pragma unroll
+    for (int mi = 0; mi < CF::MI; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < CF::NI; ++ni) {
+        const int row = m0 + wm + mi * 8 + g, col0 = n0 + wn + ni * 8 + 2 * c;
+        if (row < M && col0 + 1 < N) {
+          const double yr = acc[0][mi][ni][0], yi = acc[0][mi][ni][1];
+          const int k = row / D.xd, cc = (row - k * D.xd) * nc + (col0 >> 1);
+          double *e0 = D.C + (size_t)(2 * k) * D.ldc + 2 * cc;
+          double *e1 = e0 + D.ldc;
+          e0[0] = yr;
+          e0[1] = yi;
+          e1[0] = -yi;
+          e1[1] = yr;
+        }
+      }
   } else {
 #pragma unroll
     for (int mi = 0; mi < CF::MI; ++mi)
@@ -273,7 +334,7 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB)
           }
         }
   }
-  if (EPI == EPI_F) {
+  if (EPI == EPI_F || EPI == EPI_FZ) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));

@@ -185,9 +185,10 @@ constexpr int kMaxCTAs = 148;
 constexpr int kMaxCB = 512;      // NW * EB_max
 
 struct PrrluSmem {
-  double l[kMaxRows];    // l_i (R4), l[p] = 1
-  double raw[kMaxRows];  // CTA tier: raw pivot column
-  double u[kMaxCB];      // pivot row segment
+  // complex factorisations keep real parts in [0, kMax) and imaginary parts in [kMax, 2 kMax)
+  double l[2 * kMaxRows];    // l_i (R4), l[p] = 1
+  double raw[2 * kMaxRows];  // CTA tier: raw pivot column
+  double u[2 * kMaxCB];      // pivot row segment
   unsigned hi[32], lo[32], id[32];
   unsigned win[4];  // grid winner broadcast (key-poll mode)
   uint4 ck[2][16];                // cluster tier: CTA keys pushed by the cluster's CTAs (by parity)
@@ -201,9 +202,14 @@ struct PrrluSmem {
 // packets, counter or key-poll barrier); 2 = grid of whole thread-block clusters: CTA keys are
 // pushed through DSMEM (st.async + mbarrier), cluster winners (if more than one cluster) and
 // candidate columns go through L2 as tagged packets.
-template <int EA, int EB, int NW, int XM>
+// CPLX: complex entries (interleaved (re, im) in A.M and A.U; ldm, ldu count complex elements),
+// readings RZ1-RZ4: the key is w = fl(re^2) + fl(im^2), |c| = sqrt(w),
+// inv = (c_re / w, -c_im / w), l_i = S_iq * inv and u-row products as RZ3 (no FMA contraction),
+// the Schur update as the RZ4 fma sequence. Bit-identical to oracle/aci_oracle_z.c for equal Pi.
+template <int EA, int EB, int NW, int XM, bool CPLX = false>
 __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const int G, const int g) {
   constexpr bool GRID = XM != 0;
+  constexpr int Z = CPLX ? 2 : 1;  // doubles per entry
   constexpr int T = NW * 32;
   constexpr int MROWS = 32 * EA;
   constexpr int CB = NW * EB;  // columns per CTA
@@ -221,7 +227,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   if (A.thr_mode == 0) thr = A.tol * __longlong_as_double((long long)*A.scale_bits);
 
   // ---- load; padding = 0 and never a candidate
-  double v[EA][EB];
+  double v[EA][EB][Z];
   bool rok[EA], cok[EB];
 #pragma unroll
   for (int a = 0; a < EA; ++a) rok[a] = lane + 32 * a < m;
@@ -231,9 +237,11 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   for (int a = 0; a < EA; ++a)
 #pragma unroll
     for (int b = 0; b < EB; ++b)
-      v[a][b] = (rok[a] && cok[b]) ? A.M[(size_t)(lane + 32 * a) * ldm + c0 + w + NW * b] : 0.0;
-  for (int i = tid; i < MROWS; i += T) s_l[i] = 0.0;
-  for (int j = tid; j < CB; j += T) s_u[j] = 0.0;
+#pragma unroll
+      for (int z = 0; z < Z; ++z)
+        v[a][b][z] = (rok[a] && cok[b]) ? A.M[((size_t)(lane + 32 * a) * ldm + c0 + w + NW * b) * Z + z] : 0.0;
+  for (int i = tid; i < Z * kMaxRows; i += T) s_l[i] = 0.0;
+  for (int j = tid; j < Z * kMaxCB; j += T) s_u[j] = 0.0;
 
   // Flat candidate index = row * NC + col with the PADDED width NC (>= every column of the
   // grid), so padding entries (always exact zeros) never alias a real index and never need a
@@ -251,11 +259,16 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     // no FP64-pipe instruction is spent materialising |v|
     double cx[NCH];
     int ce[NCH];
+    // complex: the chains hold w = fl(re^2) + fl(im^2) (RZ1), compared directly
+    auto mag = [&](int e) -> double {
+      const double *x = v[e / EB][e % EB];
+      return CPLX ? __dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[Z - 1], x[Z - 1])) : x[0];
+    };
 #pragma unroll
-    for (int t = 0; t < NCH; ++t) { cx[t] = v[t / EB][t % EB]; ce[t] = t; }
+    for (int t = 0; t < NCH; ++t) { cx[t] = mag(t); ce[t] = t; }
 #pragma unroll
     for (int e = NCH; e < NE; ++e) {
-      const double x = v[e / EB][e % EB];
+      const double x = mag(e);
       const bool take = fabs(x) > fabs(cx[e % NCH]);
       cx[e % NCH] = take ? x : cx[e % NCH];
       ce[e % NCH] = take ? e : ce[e % NCH];
@@ -331,10 +344,13 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
           if (b == bc)
 #pragma unroll
             for (int a = 0; a < EA; ++a)
-              if (rok[a]) {
-                const unsigned long long bits = (unsigned long long)__double_as_longlong(v[a][b]);
-                st_pkt(dst + 2 * (lane + 32 * a), tagged(tag, (unsigned)bits), tagged(tag, (unsigned)(bits >> 32)));
-              }
+              if (rok[a])
+#pragma unroll
+                for (int z = 0; z < Z; ++z) {
+                  const unsigned long long bits = (unsigned long long)__double_as_longlong(v[a][b][z]);
+                  st_pkt(dst + 2 * (Z * (lane + 32 * a) + z), tagged(tag, (unsigned)bits),
+                         tagged(tag, (unsigned)(bits >> 32)));
+                }
         if (XM == 1 && lane == 0) {
           unsigned long long *kd = A.keys + ((size_t)par * G + g) * 4;
           st_pkt(kd, tagged(tag, ck.hi), tagged(tag, ck.lo));
@@ -459,8 +475,9 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       PHASE(4);
     }
 
-    // ---- stop rule (R2), uniform across the grid
-    const double absc = key_abs(win);
+    // ---- stop rule (R2), uniform across the grid; complex keys carry w = |c|^2 (RZ1)
+    const double wkey = key_abs(win);
+    const double absc = CPLX ? __dsqrt_rn(wkey) : wkey;
     if (k == 0) {
       first = absc;
       if (A.thr_mode == 1) thr = A.tol * first;
@@ -472,7 +489,9 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     if (k == 0 && absc == 0.0) {
       // R17: zero block -> rank 1, dummy pivot (0,0), U row e_q, eps 0
       if (A.U)
-        for (int j = c0 + tid; j < c0 + CB && j < n; j += T) A.U[(size_t)k * ldu + j] = (j == q) ? 1.0 : 0.0;
+        for (int j = c0 + tid; j < c0 + CB && j < n; j += T)
+#pragma unroll
+          for (int z = 0; z < Z; ++z) A.U[((size_t)k * ldu + j) * Z + z] = (j == q && z == 0) ? 1.0 : 0.0;
       eps = 0.0;
       k = 1;
       break;
@@ -485,8 +504,11 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       for (int a = 0; a < EA; ++a)
         if (a == ap)
 #pragma unroll
-          for (int b = 0; b < EB; ++b) s_u[w + NW * b] = v[a][b];
+          for (int b = 0; b < EB; ++b)
+#pragma unroll
+            for (int z = 0; z < Z; ++z) s_u[z * kMaxCB + w + NW * b] = v[a][b][z];
     }
+    if constexpr (!CPLX) {
     // 1/|c| from the key, off the column's critical path; the sign arrives with the column
     // (1/(-x) = -(1/x) exactly). CTA tier: l_i = S_iq * (1/S_pq) (R4) is applied as
     // fma(l'_i, -/+u_j, v) with l'_i = S_iq * (1/|c|): negation is exact, so this is
@@ -534,7 +556,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       for (int a = 0; a < EA; ++a) {
         const double li = s_l[lane + 32 * a];
 #pragma unroll
-        for (int b = 0; b < EB; ++b) v[a][b] = fma(-li, ub[b], v[a][b]);
+        for (int b = 0; b < EB; ++b) v[a][b][0] = fma(-li, ub[b], v[a][b][0]);
       }
     } else {
       const int jq = q - c0;
@@ -544,7 +566,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         for (int b = 0; b < EB; ++b)
           if (b == bq)
 #pragma unroll
-            for (int a = 0; a < EA; ++a) s_raw[lane + 32 * a] = v[a][b];
+            for (int a = 0; a < EA; ++a) s_raw[lane + 32 * a] = v[a][b][0];
       }
       __syncthreads();  // S2 (CTA tier): raw pivot column and pivot row in smem
       const bool neg = s_raw[p] < 0.0;
@@ -563,8 +585,112 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         const int i = lane + 32 * a;
         const double li = (i == p) ? (neg ? -1.0 : 1.0) : s_raw[i] * inv_abs;
 #pragma unroll
-        for (int b = 0; b < EB; ++b) v[a][b] = fma(li, ub[b], v[a][b]);
+        for (int b = 0; b < EB; ++b) v[a][b][0] = fma(li, ub[b], v[a][b][0]);
       }
+    }
+    } else {
+    // ---- complex (RZ2-RZ4): inv = conj(c) / w with w the key's |c|^2
+    double cr, ci;
+    if (GRID) {
+      const unsigned tag = (ep << 12) | (unsigned)(k + 1);
+      const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2;
+      constexpr int PPT = (MROWS + T - 1) / T;  // column entries per thread (2 packets each)
+      unsigned long long cw[PPT + 1][2][2];
+#pragma unroll
+      for (int t = 0; t < PPT; ++t) {
+        const int i = tid + T * t;
+        if (i < m)
+#pragma unroll
+          for (int z = 0; z < 2; ++z) ld_pkt(src + 2 * (2 * i + z), cw[t][z][0], cw[t][z][1]);
+      }
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        ld_pkt(src + 2 * (2 * p + z), cw[PPT][z][0], cw[PPT][z][1]);
+        while ((unsigned)(cw[PPT][z][0] >> 32) != tag || (unsigned)(cw[PPT][z][1] >> 32) != tag)
+          ld_pkt(src + 2 * (2 * p + z), cw[PPT][z][0], cw[PPT][z][1]);
+      }
+      cr = pkt_double(cw[PPT][0][0], cw[PPT][0][1]);
+      ci = pkt_double(cw[PPT][1][0], cw[PPT][1][1]);
+      const double ir = __ddiv_rn(cr, wkey), ii = __ddiv_rn(-ci, wkey);
+#pragma unroll
+      for (int t = 0; t < PPT; ++t) {
+        const int i = tid + T * t;
+        if (i < m) {
+#pragma unroll
+          for (int z = 0; z < 2; ++z)
+            while ((unsigned)(cw[t][z][0] >> 32) != tag || (unsigned)(cw[t][z][1] >> 32) != tag)
+              ld_pkt(src + 2 * (2 * i + z), cw[t][z][0], cw[t][z][1]);
+          const double xr = pkt_double(cw[t][0][0], cw[t][0][1]), xi = pkt_double(cw[t][1][0], cw[t][1][1]);
+          double lr = 1.0, li = 0.0;
+          if (i != p) {  // RZ3
+            lr = __dsub_rn(__dmul_rn(xr, ir), __dmul_rn(xi, ii));
+            li = __dadd_rn(__dmul_rn(xr, ii), __dmul_rn(xi, ir));
+          }
+          s_l[i] = lr;
+          s_l[kMaxRows + i] = li;
+        }
+      }
+      __syncthreads();  // S3
+    } else {
+      const int jq = q - c0;
+      if ((jq % NW) == w) {
+        const int bq = jq / NW;
+#pragma unroll
+        for (int b = 0; b < EB; ++b)
+          if (b == bq)
+#pragma unroll
+            for (int a = 0; a < EA; ++a) {
+              s_raw[lane + 32 * a] = v[a][b][0];
+              s_raw[kMaxRows + lane + 32 * a] = v[a][b][Z - 1];
+            }
+      }
+      __syncthreads();  // S2 (CTA tier)
+      cr = s_raw[p];
+      ci = s_raw[kMaxRows + p];
+    }
+    const double ir = __ddiv_rn(cr, wkey), ii = __ddiv_rn(-ci, wkey);
+    PHASE(5);
+    if (A.U)
+      for (int jj = tid; jj < CB; jj += T) {
+        const int j = c0 + jj;
+        if (j < n) {
+          double yr = 1.0, yi = 0.0;
+          if (j != q) {  // RZ3
+            const double ur = s_u[jj], ui = s_u[kMaxCB + jj];
+            yr = __dsub_rn(__dmul_rn(ur, ir), __dmul_rn(ui, ii));
+            yi = __dadd_rn(__dmul_rn(ur, ii), __dmul_rn(ui, ir));
+          }
+          A.U[((size_t)k * ldu + j) * 2] = yr;
+          A.U[((size_t)k * ldu + j) * 2 + 1] = yi;
+        }
+      }
+    double ubr[EB], ubi[EB];
+#pragma unroll
+    for (int b = 0; b < EB; ++b) {
+      ubr[b] = s_u[w + NW * b];
+      ubi[b] = s_u[kMaxCB + w + NW * b];
+    }
+#pragma unroll
+    for (int a = 0; a < EA; ++a) {
+      const int i = lane + 32 * a;
+      double lr, li;
+      if (GRID) {
+        lr = s_l[i];
+        li = s_l[kMaxRows + i];
+      } else {  // every thread forms its own l_i (RZ3)
+        const double xr = s_raw[i], xi = s_raw[kMaxRows + i];
+        lr = __dsub_rn(__dmul_rn(xr, ir), __dmul_rn(xi, ii));
+        li = __dadd_rn(__dmul_rn(xr, ii), __dmul_rn(xi, ir));
+        if (i == p) { lr = 1.0; li = 0.0; }
+      }
+#pragma unroll
+      for (int b = 0; b < EB; ++b) {  // RZ4
+        const double tr = fma(-lr, ubr[b], v[a][b][0]);
+        const double ti = fma(-lr, ubi[b], v[a][b][Z - 1]);
+        v[a][b][0] = fma(li, ubi[b], tr);
+        v[a][b][Z - 1] = fma(-li, ubr[b], ti);
+      }
+    }
     }
     // column q -> exact zeros (owner warp; warp-uniform branch)
     {
@@ -575,7 +701,9 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         for (int b = 0; b < EB; ++b)
           if (b == bq)
 #pragma unroll
-            for (int a = 0; a < EA; ++a) v[a][b] = 0.0;
+            for (int a = 0; a < EA; ++a)
+#pragma unroll
+              for (int z = 0; z < Z; ++z) v[a][b][z] = 0.0;
       }
     }
     scan();
@@ -602,14 +730,14 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
 // CTA (up to 255 registers, so the 32-row-slot tiles do not spill; measured faster than 16).
 // XM = 1: cooperative grid, L2 exchange. XM = 2: cluster launch; the participating CTAs are
 // rounded up to whole clusters (CTAs past the live columns hold padding only).
-template <int NWT, int XM>
+template <int NWT, int XM, bool CPLX>
 __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
   __shared__ PrrluSmem S;
   const int m = A.dims->m, n = A.dims->n;
   const int g = blockIdx.x;
 #define ACI_CTA_VARIANT(EA, EB)                                        \
   if (m <= 32 * (EA) && n <= NWT * (EB)) {                              \
-    if (g == 0) prrlu_body<(EA), (EB), NWT, 0>(A, S, 1, 0);            \
+    if (g == 0) prrlu_body<(EA), (EB), NWT, 0, CPLX>(A, S, 1, 0);      \
     return;                                                            \
   }
 #define ACI_GRID_VARIANT2(EA, EB)                                      \
@@ -619,31 +747,49 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
       const int CS = (int)cluster_size();                              \
       Gl = (Gl + CS - 1) / CS * CS;                                    \
     }                                                                  \
-    if (g < Gl) prrlu_body<(EA), (EB), NWT, XM>(A, S, Gl, g);          \
+    if (g < Gl) prrlu_body<(EA), (EB), NWT, XM, CPLX>(A, S, Gl, g);    \
     return;                                                            \
   }
-  ACI_CTA_VARIANT(1, 4)    //   32 x   32
-  ACI_CTA_VARIANT(2, 8)    //   64 x   64
-  ACI_CTA_VARIANT(4, 4)    //  128 x   32
-  ACI_CTA_VARIANT(1, 16)   //   32 x  128
-  ACI_CTA_VARIANT(4, 16)   //  128 x  128
-  ACI_CTA_VARIANT(8, 8)    //  256 x   64
-  ACI_CTA_VARIANT(2, 32)   //   64 x  256
-  ACI_CTA_VARIANT(32, 2)   // 1024 x   16
-  ACI_GRID_VARIANT2(4, ACI_W8_EB128)   //  128 x 8*EB per CTA
-  ACI_GRID_VARIANT2(8, ACI_W8_EB256)   //  256 x 8*EB per CTA
-  ACI_GRID_VARIANT2(16, ACI_W8_EB512)  //  512 x 8*EB per CTA
-  ACI_GRID_VARIANT2(32, ACI_BIG_EB)    // 1024 x 8*EB per CTA
+  if constexpr (!CPLX) {
+    ACI_CTA_VARIANT(1, 4)    //   32 x   32
+    ACI_CTA_VARIANT(2, 8)    //   64 x   64
+    ACI_CTA_VARIANT(4, 4)    //  128 x   32
+    ACI_CTA_VARIANT(1, 16)   //   32 x  128
+    ACI_CTA_VARIANT(4, 16)   //  128 x  128
+    ACI_CTA_VARIANT(8, 8)    //  256 x   64
+    ACI_CTA_VARIANT(2, 32)   //   64 x  256
+    ACI_CTA_VARIANT(32, 2)   // 1024 x   16
+    ACI_GRID_VARIANT2(4, ACI_W8_EB128)   //  128 x 8*EB per CTA
+    ACI_GRID_VARIANT2(8, ACI_W8_EB256)   //  256 x 8*EB per CTA
+    ACI_GRID_VARIANT2(16, ACI_W8_EB512)  //  512 x 8*EB per CTA
+    ACI_GRID_VARIANT2(32, ACI_BIG_EB)    // 1024 x 8*EB per CTA
+  } else {
+    // complex entries take two registers: at most 32 entries per thread
+    ACI_CTA_VARIANT(1, 8)    //   32 x   64
+    ACI_CTA_VARIANT(2, 8)    //   64 x   64
+    ACI_CTA_VARIANT(4, 4)    //  128 x   32
+    ACI_CTA_VARIANT(1, 16)   //   32 x  128
+    ACI_CTA_VARIANT(4, 8)    //  128 x   64
+    ACI_CTA_VARIANT(2, 16)   //   64 x  128
+    ACI_CTA_VARIANT(8, 4)    //  256 x   32
+    ACI_CTA_VARIANT(16, 2)   //  512 x   16
+    ACI_GRID_VARIANT2(4, 4)  //  128 x 32 per CTA
+    ACI_GRID_VARIANT2(8, 2)  //  256 x 16 per CTA
+    ACI_GRID_VARIANT2(16, 2) //  512 x 16 per CTA
+  }
 #undef ACI_CTA_VARIANT
 #undef ACI_GRID_VARIANT2
 }
 
 constexpr int kNWT = 8;
 
-bool fits_one_cta(int m, int n) {
+bool fits_one_cta(int m, int n, bool cplx) {
   const int v8[][2] = {{1, 4}, {2, 8}, {4, 4}, {1, 16}, {4, 16}, {8, 8}, {2, 32}, {32, 2}};
-  for (auto &e : v8)
+  const int z8[][2] = {{1, 8}, {2, 8}, {4, 4}, {1, 16}, {4, 8}, {2, 16}, {8, 4}, {16, 2}};
+  for (int t = 0; t < 8; ++t) {
+    const int *e = cplx ? z8[t] : v8[t];
     if (m <= 32 * e[0] && n <= kNWT * e[1]) return true;
+  }
   return false;
 }
 
@@ -653,7 +799,7 @@ bool fits_one_cta(int m, int n) {
 int cluster_choice() {
   static int cs = -1;
   if (cs >= 0) return cs;
-  const void *kern = (const void *)prrlu_kernel<kNWT, 2>;
+  const void *kern = (const void *)prrlu_kernel<kNWT, 2, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   auto active = [&](int c) {
     cudaLaunchConfig_t cfg = {};
@@ -683,8 +829,10 @@ int cluster_choice() {
 
 }  // namespace
 
-bool prrlu_supported(int max_m, int max_n) {
-  return fits_one_cta(max_m, max_n) || (max_m <= kMaxRows && (max_n + 7) / 8 <= kMaxCTAs);
+bool prrlu_supported(int max_m, int max_n, bool cplx) {
+  if (fits_one_cta(max_m, max_n, cplx)) return true;
+  if (cplx) return max_m <= 512 && (max_n + 15) / 16 <= 64;
+  return max_m <= kMaxRows && (max_n + 7) / 8 <= kMaxCTAs;
 }
 
 void prrlu_envelope(int *max_rows, int *max_cols) {
@@ -700,10 +848,11 @@ size_t prrlu_exchange_bytes(int max_m, int max_n) {
 
 void prrlu_init() { cluster_choice(); }
 
-void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st) {
-  if (fits_one_cta(max_m, max_n)) {
+template <bool CPLX>
+static void launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t st) {
+  if (fits_one_cta(max_m, max_n, CPLX)) {
     void *params[] = {const_cast<LuArgs *>(&a)};
-    cudaLaunchKernel((const void *)prrlu_kernel<kNWT, 1>, dim3(1), dim3(kNWT * 32), params, 0, st);
+    cudaLaunchKernel((const void *)prrlu_kernel<kNWT, 1, CPLX>, dim3(1), dim3(kNWT * 32), params, 0, st);
     return;
   }
   int G = (max_n + kNWT - 1) / kNWT;  // enough for every variant the live size may select
@@ -722,10 +871,20 @@ void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 2>, args);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute((const void *)prrlu_kernel<kNWT, 2, CPLX>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      attr = true;
+    }
+    cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 2, CPLX>, args);
     return;
   }
   cudaMemsetAsync(a.counter, 0, sizeof(unsigned), st);
   void *params[] = {&args};
-  cudaLaunchCooperativeKernel((const void *)prrlu_kernel<kNWT, 1>, dim3(G), dim3(kNWT * 32), params, 0, st);
+  cudaLaunchCooperativeKernel((const void *)prrlu_kernel<kNWT, 1, CPLX>, dim3(G), dim3(kNWT * 32), params, 0, st);
+}
+
+void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx) {
+  if (cplx) launch_prrlu_t<true>(a, max_m, max_n, st);
+  else launch_prrlu_t<false>(a, max_m, max_n, st);
 }

@@ -198,14 +198,15 @@ def _tt_compress(cores: list, cutoff: float) -> list:
     return cores
 
 
-def fourier_tt(L: int, coefs, cutoff: float = 1e-12, chunk: int = 256) -> TT:
+def fourier_tt(L: int, coefs, cutoff: float = 1e-12, chunk: int = 64) -> TT:
     """Complex QTT of g(x) = sum_{k=0..K} coefs[k] e^{i k x} on x = sum_l 2^-l sigma_l in [0, 1)
-    (P:289-293). Each e^{ikx} = prod_l e^{i k 2^-l sigma_l} is rank 1; the terms are block-summed
-    in chunks of `chunk` frequencies and rounded after each chunk (cutoff rule of R14), so the
-    rank stays at the numerical rank O(sqrt K)."""
+    (P:289-293). Each e^{ikx} = prod_l e^{i k 2^-l sigma_l} is rank 1; chunks of `chunk`
+    frequencies are block-summed and rounded (cutoff rule of R14), then the chunk TTs are summed
+    pairwise with rounding after each sum, so every rounding sees a rank of at most twice the
+    numerical rank O(sqrt K)."""
     coefs = np.asarray(coefs, dtype=np.complex128)
     K = len(coefs) - 1
-    acc = None
+    parts = []
     for k0 in range(0, K + 1, chunk):
         ks = np.arange(k0, min(K + 1, k0 + chunk))
         n = len(ks)
@@ -226,9 +227,15 @@ def fourier_tt(L: int, coefs, cutoff: float = 1e-12, chunk: int = 256) -> TT:
                 c[i, 0, i] = 1.0
                 c[i, 1, i] = ph
             cores.append(c)
-        part = TT(cores)
-        acc = part if acc is None else _block_sum([acc, part])
-        acc = TT(_tt_compress(acc.cores, cutoff))
+        parts.append(TT(_tt_compress(cores, cutoff)))
+    while len(parts) > 1:
+        nxt = []
+        for a in range(0, len(parts) - 1, 2):
+            nxt.append(TT(_tt_compress(_block_sum([parts[a], parts[a + 1]]).cores, cutoff)))
+        if len(parts) % 2:
+            nxt.append(parts[-1])
+        parts = nxt
+    acc = parts[0]
     acc.meta = {"kind": "fourier", "coefs": coefs}
     return acc
 

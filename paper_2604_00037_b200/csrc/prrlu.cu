@@ -793,15 +793,20 @@ bool fits_one_cta(int m, int n, bool cplx) {
   return false;
 }
 
-// Cluster size of the XM = 2 launch, chosen once: 16 (non-portable) if four 16-CTA clusters of
-// this kernel can be co-resident (the 1024-row tier uses 64 CTAs), else 8, else 0 = L2 tier.
-// ACI_PRRLU_CLUSTER=0/8/16 overrides (measurements).
+// Cluster size of the XM = 2 launch, chosen once. Every participating cluster spins on the others
+// (cross-cluster exchange), so ALL clusters a live block can use must be co-resident: the widest
+// grid variant uses ceil(kMaxCTAs * 8 / 16) = 74 CTAs (16 columns per CTA at the envelope's 1184
+// columns). 16-CTA clusters (non-portable) if ceil(74 / 16) of them fit at once for both the real
+// and the complex kernel, else 8-CTA clusters under the same rule, else 0 = the cooperative L2
+// tier (co-residency guaranteed by the cooperative launch). ACI_PRRLU_CLUSTER=0/8/16 restricts
+// the choice (measurements). Measured on this pool: 7 co-resident 16-CTA clusters, 15 8-CTA ones.
+constexpr int kWidestGrid = (kMaxCTAs * 8 + 15) / 16;
+
 int cluster_choice() {
   static int cs = -1;
   if (cs >= 0) return cs;
-  const void *kern = (const void *)prrlu_kernel<kNWT, 2, false>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  auto active = [&](int c) {
+  auto active = [&](const void *kern, int c) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c * 8);
     cfg.blockDim = dim3(kNWT * 32);
@@ -819,11 +824,16 @@ int cluster_choice() {
     }
     return n;
   };
+  auto fits = [&](int c) {
+    const int need = (kWidestGrid + c - 1) / c;
+    return active((const void *)prrlu_kernel<kNWT, 2, false>, c) >= need &&
+           active((const void *)prrlu_kernel<kNWT, 2, true>, c) >= need;
+  };
   const char *env = getenv("ACI_PRRLU_CLUSTER");
   int want = env ? atoi(env) : 16;
   cs = 0;
-  if (want >= 16 && active(16) * 16 >= 64) cs = 16;
-  else if (want >= 8 && active(8) * 8 >= 64) cs = 8;
+  if (want >= 16 && fits(16)) cs = 16;
+  else if (want >= 8 && fits(8)) cs = 8;
   return cs;
 }
 

@@ -45,6 +45,22 @@ int main(int argc, char **argv) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   int only = argc > 1 ? atoi(argv[1]) : -1;
+  {
+    const void *kern = (const void *)prrlu_kernel<kNWT, 2, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int c : {8, 16}) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(c * 8);
+      cfg.blockDim = dim3(kNWT * 32);
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = c; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.attrs = at; cfg.numAttrs = 1;
+      int n = 0;
+      cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+      printf("max active %d-CTA clusters of prrlu_kernel: %d\n", c, n);
+    }
+  }
   for (auto &sz : sizes) {
     int m = sz[0], n = sz[1], kmax = sz[2], stat = sz[3] ? sz[3] : sz[0];
     if (only > 0 && m != only) continue;

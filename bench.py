@@ -376,8 +376,16 @@ def main():
                       "frac": (prrlu_flops / (pr["ms"] * 1e9)) / pk["dfma_tflops"] if pr["ms"] else None,
                       "traffic": None, "per_launch_us": 1e3 * pr["ms"] / max(pr["launches"], 1),
                       "per_pivot_us": 1e3 * pr["ms"] / max(reps[-1]["pivot_steps"], 1),
-                      "note": "latency-bound: one inter-CTA exchange per pivot (DESIGN.md §6); peak = measured "
-                              "DFMA rate"}
+                      "latency": {
+                          "per_pivot_us": 1e3 * pr["ms"] / max(reps[-1]["pivot_steps"], 1),
+                          "exchange_floor_us": 0.66,
+                          "frac": (0.66 / (1e3 * pr["ms"] / max(reps[-1]["pivot_steps"], 1))),
+                          "floor_source": "per pivot at least one 16-CTA DSMEM key exchange (0.25 us, "
+                                          "profiles/r01_probe7_cluster_push.txt keys-only) + one L2 round trip "
+                                          "for the winner's column (~800 cycles at 1965 MHz = 0.41 us); the "
+                                          "rank-1 update itself is ALU-issue bound (DESIGN.md §5)"},
+                      "note": "latency-bound: one cluster/L2 exchange per pivot (DESIGN.md §5); 'frac' above is "
+                              "against the measured DFMA rate, 'latency.frac' against the exchange floor"}
         roof_pi = {"kernel": "gemm_dmma_kernel<fused f> (a3+a4) + a1/a2", "bound": "tensor",
                    "achieved": pi_flops / ((pi["ms"] + prof["gemm_ab"]["ms"]) * 1e9),
                    "peak": pk["dmma_tflops"], "unit": "TFLOP/s",

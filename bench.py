@@ -339,6 +339,44 @@ def main():
                 "note": "paper (EPYC 9474F, 1 thread, Julia): ACI runtime ~ chi^2.3 (P:307); flops counted as 4x "
                         "the real contraction model (complex products)"}
 
+    def run_steady(chis, iters=6):
+        """Steady-state full-rank iterations: configs[3] run for `iters`
+        iterations so that the last one is at the saturated ranks (2 chi); its device time
+        (CUDA events around the iteration's graph) and its contraction-model flops (from the
+        update log) per half-sweep."""
+        pts = []
+        for chi in chis:
+            cf = make_config(3, chi, npts=0)
+            xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+            y0 = aci.TensorTrain.from_cores(cf["y_init"])
+            best = None
+            for _ in range(3):
+                out, st, rep, ex = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], iters, y_init=y0,
+                                                       stream=sptr, log=True, iter_times=True)
+                out.free()
+                last = ex["iter_ms"][-1]
+                best = last if best is None else min(best, last)
+            L, nb = 40, 39
+            tail = ex["log"][-2 * nb:]
+            fl = 0.0
+            for e in tail:
+                b, rl, rr = e["bond"], e["rl"], e["rr"]
+                m, n = 2 * rl, 2 * rr
+                for xr in ([1] + [chi] * (L - 1) + [1], [1] + [2] * (L - 1) + [1]):
+                    c0, c1, c2 = xr[b], xr[b + 1], xr[b + 2]
+                    fl += 2.0 * rl * c0 * 2 * c1 + 2.0 * c1 * 2 * c2 * rr + 2.0 * m * c1 * n
+            pts.append({"chi": chi, "iteration": len(ex["iter_ms"]), "ms_per_half_sweep": best / 2,
+                        "gflop_per_half_sweep": fl / 2 / 1e9, "tflops": fl / best / 1e9,
+                        "pivots_per_half_sweep": sum(e["r"] for e in tail) / 2,
+                        "max_rank": max(e["r"] for e in tail)})
+        lx = np.log([p["chi"] for p in pts])
+        fit = lambda ys: float(np.polyfit(lx, np.log(ys), 1)[0])
+        return {"points": pts, "exponent_half_sweep_time": fit([p["ms_per_half_sweep"] for p in pts]),
+                "exponent_half_sweep_flops": fit([p["gflop_per_half_sweep"] for p in pts]),
+                "note": "last iteration of a run allowed 6 (it converges once the ranks saturate at 2 chi): "
+                        "contraction work per half-sweep scales as chi^3; the wall time grows slower "
+                        "because the prrLU (one exchange per pivot, pivots ~ chi) dominates"}
+
     # the metric is quoted vs chi (B:2, configs[3]): time the chi = 64 and 128 products as well
     sweep = []
     if not args.no_chi_sweep:
@@ -352,6 +390,7 @@ def main():
 
     cf, tot_ms, tot_flops, launches, prof, reps, clocks, e2e = run_chi(args.chi, args.steps, args.warmup,
                                                                        with_e2e=True)
+    steady = run_steady((64, 128, 256)) if (ws == 1 and not args.no_chi_sweep) else None
     cplx = None
     if ws == 1 and not args.no_complex:
         cplx = run_complex((1000, 4000, 16000), max(2, args.steps // 2))
@@ -436,6 +475,8 @@ def main():
                                  "note": "fixed 4-iteration runs from a rank-2 y_init: the contraction work is "
                                          "sub-cubic here because ranks saturate late (SURVEY 8(d)); the pivot "
                                          "count grows ~linearly in chi"}
+        if steady is not None:
+            line["steady_state_half_sweep"] = steady
         if cplx is not None:
             line["complex_fourier"] = cplx
         if ws == 1 and not args.no_cpu_baseline:

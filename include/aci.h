@@ -168,6 +168,8 @@ typedef struct {
   uint8_t **I_sets;
   uint8_t **J_sets;
   aci_profile *profile;      /* optional: per-class device times of this call */
+  float *iter_ms;            /* optional, max_sweeps floats: device time of each iteration (both
+                              * half-sweeps + convergence test; CUDA events on the call's stream) */
 } aci_options;
 
 /*

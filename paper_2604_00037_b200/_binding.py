@@ -65,7 +65,8 @@ class aci_options(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("y_init", C.c_void_p), ("tol_mode", C.c_int),
                 ("log", C.POINTER(aci_pivot_log)), ("stream", C.c_void_p), ("workspace", C.c_void_p),
                 ("workspace_bytes", C.c_size_t), ("I_sets", C.POINTER(C.POINTER(C.c_uint8))),
-                ("J_sets", C.POINTER(C.POINTER(C.c_uint8))), ("profile", C.POINTER(aci_profile))]
+                ("J_sets", C.POINTER(C.POINTER(C.c_uint8))), ("profile", C.POINTER(aci_profile)),
+                ("iter_ms", C.POINTER(C.c_float))]
 
 
 _lib = None
@@ -203,7 +204,7 @@ def _make_op(op, n_inputs):
 
 
 def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, tol_mode=TOL_RELATIVE,
-                    log=False, stream=0, workspace=None, index_sets=False, profile=False):
+                    log=False, stream=0, workspace=None, index_sets=False, profile=False, iter_times=False):
     """Run aci_elementwise_ex. ``inputs`` are TensorTrain handles (aliases allowed).
 
     Returns (TensorTrain, status, report dict, extras dict).
@@ -225,6 +226,9 @@ def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, t
     if profile:
         prof = aci_profile()
         opts.profile = C.pointer(prof)
+    if iter_times:
+        iter_ms = np.zeros(max_sweeps, np.float32)
+        opts.iter_ms = iter_ms.ctypes.data_as(C.POINTER(C.c_float))
     L = len(inputs[0].shape()[0])
     if log:
         cap_u = 2 * (L - 1) * max_sweeps
@@ -253,6 +257,8 @@ def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, t
     res = TensorTrain(out)
     if profile:
         extras["profile"] = prof.as_dict()
+    if iter_times:
+        extras["iter_ms"] = [float(x) for x in iter_ms[:rep.iterations]]
     if log:
         nw = lg.n_written
         extras["log"] = [{"bond": int(info[u, 0]), "dir": int(info[u, 1]), "rl": int(info[u, 2]),

@@ -1465,7 +1465,13 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   }
   const float ms_graph = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - tg0).count();
   int it = 0, converged = 0;
+  cudaEvent_t ev_it[2] = {nullptr, nullptr};
+  if (o.iter_ms) {
+    cudaEventCreate(&ev_it[0]);
+    cudaEventCreate(&ev_it[1]);
+  }
   for (it = 1; it <= max_sweeps; ++it) {
+    if (ev_it[0]) cudaEventRecord(ev_it[0], strm);
     if (gexec) {
       cudaGraphLaunch(gexec, strm);
       prof.total += prof.per_iter_launches;
@@ -1473,6 +1479,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
     } else {
       one_iteration();
     }
+    if (ev_it[1]) cudaEventRecord(ev_it[1], strm);
     int flag = 0;
     cudaMemcpyAsync(&flag, R.conv, sizeof(int), cudaMemcpyDeviceToHost, strm);
     cudaError_t e = cudaStreamSynchronize(strm);
@@ -1481,8 +1488,11 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
       cleanup();
       return fail(ACI_ERR_CUDA, std::string("aci sweep: ") + cudaGetErrorString(e));
     }
+    if (ev_it[0]) cudaEventElapsedTime(&o.iter_ms[it - 1], ev_it[0], ev_it[1]);
     if (flag) { converged = 1; break; }
   }
+  for (auto ev : ev_it)
+    if (ev) cudaEventDestroy(ev);
   if (it > max_sweeps) it = max_sweeps;
   const int slot = it * 2 * (L - 1);
 

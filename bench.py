@@ -377,6 +377,43 @@ def main():
                         "contraction work per half-sweep scales as chi^3; the wall time grows slower "
                         "because the prrLU (one exchange per pivot, pivots ~ chi) dominates"}
 
+    def run_concurrent(chi=64, ks=(1, 2, 4, 8), reps=3):
+        """Product-level concurrency: k independent configs[3] products, each
+        on its own stream from its own host thread with aci_options.concurrent (single-cluster
+        prrLU launches, safe to co-schedule); products per second vs k (wall clock around the
+        batch, device work only: inputs resident)."""
+        import threading
+        cf = make_config(3, chi, npts=0)
+        pts = []
+        for k in ks:
+            streams = [torch.cuda.Stream() for _ in range(k)]
+            data = [([aci.TensorTrain.from_cores(t) for t in cf["inputs"]], aci.TensorTrain.from_cores(cf["y_init"]))
+                    for _ in range(k)]
+
+            def work(i, n):
+                xs, y0 = data[i]
+                for _ in range(n):
+                    out, *_ = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"],
+                                                  y_init=y0, stream=streams[i].cuda_stream, concurrent=True)
+                    out.free()
+
+            ths = [threading.Thread(target=work, args=(i, 1)) for i in range(k)]  # warm-up (graphs)
+            [t.start() for t in ths]
+            [t.join() for t in ths]
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ths = [threading.Thread(target=work, args=(i, reps)) for i in range(k)]
+            [t.start() for t in ths]
+            [t.join() for t in ths]
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            pts.append({"streams": k, "products": k * reps, "seconds": dt, "products_per_s": k * reps / dt,
+                        "ms_per_product_amortised": 1e3 * dt / (k * reps)})
+        base = pts[0]["products_per_s"]
+        for p in pts:
+            p["speedup_vs_1"] = p["products_per_s"] / base
+        return {"workload": cf["name"], "mode": "aci_options.concurrent (single-cluster prrLU)", "points": pts}
+
     # the metric is quoted vs chi (B:2, configs[3]): time the chi = 64 and 128 products as well
     sweep = []
     if not args.no_chi_sweep:
@@ -391,6 +428,7 @@ def main():
     cf, tot_ms, tot_flops, launches, prof, reps, clocks, e2e = run_chi(args.chi, args.steps, args.warmup,
                                                                        with_e2e=True)
     steady = run_steady((64, 128, 256)) if (ws == 1 and not args.no_chi_sweep) else None
+    conc = run_concurrent() if (ws == 1 and not args.no_chi_sweep) else None
     cplx = None
     if ws == 1 and not args.no_complex:
         cplx = run_complex((1000, 4000, 16000), max(2, args.steps // 2))
@@ -477,6 +515,8 @@ def main():
                                          "count grows ~linearly in chi"}
         if steady is not None:
             line["steady_state_half_sweep"] = steady
+        if conc is not None:
+            line["concurrent_products"] = conc
         if cplx is not None:
             line["complex_fourier"] = cplx
         if ws == 1 and not args.no_cpu_baseline:

@@ -170,6 +170,14 @@ typedef struct {
   aci_profile *profile;      /* optional: per-class device times of this call */
   float *iter_ms;            /* optional, max_sweeps floats: device time of each iteration (both
                               * half-sweeps + convergence test; CUDA events on the call's stream) */
+  int concurrent;            /* 1: this call may run concurrently with other aci calls on other
+                              * streams (host threads). Every prrLU launch then uses at most one
+                              * 16-CTA thread-block cluster, which the hardware schedules as a unit,
+                              * so concurrent products cannot deadlock on each other's spinning CTAs.
+                              * 2-site blocks must fit one cluster (real: 128 x 1024, 256 x 512,
+                              * 512 x 512, 1024 x 256; complex: 128 x 1024, 256 x 512, 512 x 256),
+                              * else ACI_ERR_UNSUPPORTED. 0 (default): the fastest tiers, which may
+                              * span several clusters — do not run those calls concurrently. */
 } aci_options;
 
 /*

@@ -66,7 +66,7 @@ class aci_options(C.Structure):
                 ("log", C.POINTER(aci_pivot_log)), ("stream", C.c_void_p), ("workspace", C.c_void_p),
                 ("workspace_bytes", C.c_size_t), ("I_sets", C.POINTER(C.POINTER(C.c_uint8))),
                 ("J_sets", C.POINTER(C.POINTER(C.c_uint8))), ("profile", C.POINTER(aci_profile)),
-                ("iter_ms", C.POINTER(C.c_float))]
+                ("iter_ms", C.POINTER(C.c_float)), ("concurrent", C.c_int)]
 
 
 _lib = None
@@ -204,7 +204,8 @@ def _make_op(op, n_inputs):
 
 
 def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, tol_mode=TOL_RELATIVE,
-                    log=False, stream=0, workspace=None, index_sets=False, profile=False, iter_times=False):
+                    log=False, stream=0, workspace=None, index_sets=False, profile=False, iter_times=False,
+                    concurrent=False):
     """Run aci_elementwise_ex. ``inputs`` are TensorTrain handles (aliases allowed).
 
     Returns (TensorTrain, status, report dict, extras dict).
@@ -220,6 +221,7 @@ def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, t
     opts.y_init = y_init.handle.value if y_init is not None else None
     opts.tol_mode = tol_mode
     opts.stream = stream or None
+    opts.concurrent = 1 if concurrent else 0
     extras = {}
     if workspace is not None:
         opts.workspace, opts.workspace_bytes = workspace

@@ -749,6 +749,7 @@ struct Prof {
 struct Run {
   Prof *P = nullptr;
   int cplx = 0, Z = 1, ZE = 1;  // complex run: Z = 2 doubles per entry, ZE = 4 for expanded operands
+  int one = 0;                  // aci_options.concurrent: single-cluster prrLU launches
   int L = 0, N = 0, maxrank = 0, max_sweeps = 0, log_cap_upd = 0, log_cap_piv = 0, colcap = 0;
   std::vector<int> d, yr;
   std::vector<std::vector<int>> xr;      // [n][s], s = 0..L
@@ -1021,7 +1022,7 @@ static std::vector<uint64_t> graph_key(const Run &R, const FOp &op, double tol, 
     u(b);
   };
   u((uint64_t)(uintptr_t)ws); u(need); u((uint64_t)(uintptr_t)st);
-  u(R.L); u(R.N); u(R.maxrank); u(R.log_cap_upd); u(R.log_cap_piv); u(R.colcap); u(R.cplx);
+  u(R.L); u(R.N); u(R.maxrank); u(R.log_cap_upd); u(R.log_cap_piv); u(R.colcap); u(R.cplx); u(R.one);
   dbl(tol); u(tol_mode);
   for (int x : R.d) u(x);
   for (int x : R.yr) u(x);
@@ -1185,7 +1186,7 @@ static void bond_update(Run &R, double tol, int tol_mode, int b, int dir, int lo
   a.U = dir == 1 ? R.Ust[b] : nullptr;
   a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter; a.epoch = R.epoch;
   R.P->begin(ACI_PROF_PRRLU);
-  launch_prrlu(a, R.mmax[b], R.nmax[b], st, R.cplx != 0);
+  launch_prrlu(a, R.mmax[b], R.nmax[b], st, R.cplx != 0, R.one != 0);
   R.P->end(1);
   R.P->begin(ACI_PROF_UPDATE);
   launch_update(R, b, dir, logslot, next, st);
@@ -1225,7 +1226,7 @@ static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st)
   a.rows = R.prow[s - 1]; a.cols = R.pcol[s - 1]; a.r_out = R.rout + (s - 1); a.eps_out = R.epsb + (s - 1);
   a.U = nullptr;
   a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter; a.epoch = R.epoch;
-  launch_prrlu(a, max_m, max_n, st, R.cplx != 0);
+  launch_prrlu(a, max_m, max_n, st, R.cplx != 0, R.one != 0);
   CanonUpd U = {};
   U.s = s; U.L = L; U.N = N; U.ds = R.d[s]; U.yr_s = R.yr[s]; U.yr_prev_rows = R.yr[s - 1] * R.d[s - 1];
   U.cols = R.pcol[s - 1]; U.r_in = R.rout + (s - 1);
@@ -1262,7 +1263,7 @@ extern "C" int aci_limits(int *max_rows, int *max_cols) {
   return ACI_OK;
 }
 
-static int build_run(const Inputs &I, const tt_s *y, int maxrank, int max_sweeps, Run &R) {
+static int build_run(const Inputs &I, const tt_s *y, int maxrank, int max_sweeps, Run &R, int one = 0) {
   const tt_s *t0 = I.tts[0];
   R.L = t0->L;
   R.N = (int)I.tts.size();
@@ -1290,12 +1291,14 @@ static int build_run(const Inputs &I, const tt_s *y, int maxrank, int max_sweeps
   for (int s = 0; s < R.L; ++s) R.colcap = std::max(R.colcap, R.yr[s]);
   R.colcap *= R.Z;
   // envelope
+  R.one = one;
+  auto ok = [&](int m, int n) { return one ? prrlu_supported_one(m, n, R.cplx != 0) : prrlu_supported(m, n, R.cplx != 0); };
   for (int b = 0; b < R.L - 1; ++b)
-    if (!prrlu_supported(R.mmax[b], R.nmax[b], R.cplx != 0))
+    if (!ok(R.mmax[b], R.nmax[b]))
       return fail(ACI_ERR_UNSUPPORTED, "aci: 2-site block " + std::to_string(R.mmax[b]) + "x" +
                                            std::to_string(R.nmax[b]) + " exceeds the prrLU envelope");
   for (int s = 1; s < R.L; ++s)
-    if (!prrlu_supported(R.yr[s], R.nmax[s - 1], R.cplx != 0))
+    if (!ok(R.yr[s], R.nmax[s - 1]))
       return fail(ACI_ERR_UNSUPPORTED, "aci: y_init bond too large for the prrLU envelope");
   return ACI_OK;
 }
@@ -1348,7 +1351,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   }
 
   Run R;
-  st = build_run(I, y, maxrank, max_sweeps, R);
+  st = build_run(I, y, maxrank, max_sweeps, R, o.concurrent ? 1 : 0);
   if (st) { tt_destroy(ygen); return st; }
   size_t need = carve(R, nullptr);
   char *ws = nullptr;

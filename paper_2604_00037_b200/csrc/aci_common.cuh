@@ -82,7 +82,9 @@ void launch_gemm_sub(const GemmDesc *d_descs, int ndesc, int max_m, int max_n, c
 bool prrlu_supported(int max_m, int max_n, bool cplx = false);
 size_t prrlu_exchange_bytes(int max_m, int max_n);
 // cplx: complex entries (interleaved; ldm/ldu in complex elements; colcap >= 2 m).
-void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx = false);
+// one: single-cluster mode (aci_options.concurrent): at most one 16-CTA cluster per launch.
+void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx = false, bool one = false);
+bool prrlu_supported_one(int m, int n, bool cplx);
 // Chooses the prrLU exchange tier (cluster size) once; call before any stream capture.
 void prrlu_init();
 void prrlu_envelope(int *max_rows, int *max_cols);

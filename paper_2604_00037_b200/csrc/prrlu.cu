@@ -781,6 +781,55 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
 #undef ACI_GRID_VARIANT2
 }
 
+// Single-cluster mode (aci_options.concurrent): every grid variant uses
+// exactly one 16-CTA cluster (gang-scheduled by the hardware), so prrLU launches of products
+// running concurrently on other streams can never hold part of each other's participants while
+// spinning. More columns per CTA than the default tiers where needed to fit 16 CTAs.
+template <int NWT, bool CPLX>
+__global__ void __launch_bounds__(NWT * 32) prrlu_kernel_one(LuArgs A) {
+  __shared__ PrrluSmem S;
+  const int m = A.dims->m, n = A.dims->n;
+  const int g = blockIdx.x;
+#define ACI_CTA_VARIANT(EA, EB)                                        \
+  if (m <= 32 * (EA) && n <= NWT * (EB)) {                              \
+    if (g == 0) prrlu_body<(EA), (EB), NWT, 0, CPLX>(A, S, 1, 0);      \
+    return;                                                            \
+  }
+#define ACI_ONE_VARIANT(EA, EB)                                        \
+  if (m <= 32 * (EA) && n <= 16 * NWT * (EB)) {                         \
+    prrlu_body<(EA), (EB), NWT, 2, CPLX>(A, S, 16, g);                 \
+    return;                                                            \
+  }
+  if constexpr (!CPLX) {
+    ACI_CTA_VARIANT(1, 4)
+    ACI_CTA_VARIANT(2, 8)
+    ACI_CTA_VARIANT(4, 4)
+    ACI_CTA_VARIANT(1, 16)
+    ACI_CTA_VARIANT(4, 16)
+    ACI_CTA_VARIANT(8, 8)
+    ACI_CTA_VARIANT(2, 32)
+    ACI_CTA_VARIANT(32, 2)
+    ACI_ONE_VARIANT(4, 8)    //  128 x 1024
+    ACI_ONE_VARIANT(8, 4)    //  256 x  512
+    ACI_ONE_VARIANT(16, 4)   //  512 x  512
+    ACI_ONE_VARIANT(32, 2)   // 1024 x  256
+  } else {
+    ACI_CTA_VARIANT(1, 8)
+    ACI_CTA_VARIANT(2, 8)
+    ACI_CTA_VARIANT(4, 4)
+    ACI_CTA_VARIANT(1, 16)
+    ACI_CTA_VARIANT(4, 8)
+    ACI_CTA_VARIANT(2, 16)
+    ACI_CTA_VARIANT(8, 4)
+    ACI_CTA_VARIANT(16, 2)
+    ACI_ONE_VARIANT(4, 8)    //  128 x 1024
+    ACI_ONE_VARIANT(8, 4)    //  256 x  512
+    ACI_ONE_VARIANT(16, 2)   //  512 x  256
+  }
+#undef ACI_CTA_VARIANT
+#undef ACI_ONE_VARIANT
+}
+
 constexpr int kNWT = 8;
 
 bool fits_one_cta(int m, int n, bool cplx) {
@@ -802,9 +851,8 @@ bool fits_one_cta(int m, int n, bool cplx) {
 // the choice (measurements). Measured on this pool: 7 co-resident 16-CTA clusters, 15 8-CTA ones.
 constexpr int kWidestGrid = (kMaxCTAs * 8 + 15) / 16;
 
-int cluster_choice() {
-  static int cs = -1;
-  if (cs >= 0) return cs;
+static int cluster_choice_once() {
+  int cs = -1;
   auto active = [&](const void *kern, int c) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
@@ -837,7 +885,27 @@ int cluster_choice() {
   return cs;
 }
 
+// thread-safe one-time choice (C++11 function-local static initialisation)
+int cluster_choice() {
+  static const int cs = cluster_choice_once();
+  return cs;
+}
+
 }  // namespace
+
+bool prrlu_supported_one(int m, int n, bool cplx) {
+  if (fits_one_cta(m, n, cplx)) return true;
+  const int v[][2] = {{128, 1024}, {256, 512}, {512, 512}, {1024, 256}};
+  const int z[][2] = {{128, 1024}, {256, 512}, {512, 256}};
+  if (cplx) {
+    for (auto &e : z)
+      if (m <= e[0]) return n <= e[1];
+  } else {
+    for (auto &e : v)
+      if (m <= e[0]) return n <= e[1];
+  }
+  return false;
+}
 
 bool prrlu_supported(int max_m, int max_n, bool cplx) {
   if (fits_one_cta(max_m, max_n, cplx)) return true;
@@ -859,7 +927,28 @@ size_t prrlu_exchange_bytes(int max_m, int max_n) {
 void prrlu_init() { cluster_choice(); }
 
 template <bool CPLX>
-static void launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t st) {
+static void launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool one) {
+  if (one && !fits_one_cta(max_m, max_n, CPLX)) {
+    LuArgs args = a;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16);
+    cfg.blockDim = dim3(kNWT * 32);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 16;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute((const void *)prrlu_kernel_one<kNWT, CPLX>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      attr = true;
+    }
+    cudaLaunchKernelEx(&cfg, prrlu_kernel_one<kNWT, CPLX>, args);
+    return;
+  }
   if (fits_one_cta(max_m, max_n, CPLX)) {
     void *params[] = {const_cast<LuArgs *>(&a)};
     cudaLaunchKernel((const void *)prrlu_kernel<kNWT, 1, CPLX>, dim3(1), dim3(kNWT * 32), params, 0, st);
@@ -894,7 +983,7 @@ static void launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t s
   cudaLaunchCooperativeKernel((const void *)prrlu_kernel<kNWT, 1, CPLX>, dim3(G), dim3(kNWT * 32), params, 0, st);
 }
 
-void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx) {
-  if (cplx) launch_prrlu_t<true>(a, max_m, max_n, st);
-  else launch_prrlu_t<false>(a, max_m, max_n, st);
+void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx, bool one) {
+  if (cplx) launch_prrlu_t<true>(a, max_m, max_n, st, one);
+  else launch_prrlu_t<false>(a, max_m, max_n, st, one);
 }

@@ -286,3 +286,52 @@ def test_caller_workspace_and_stream(aci):
         aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0,
                             workspace=(ws.data_ptr(), nbytes // 2))
     assert "OOM" in str(e.value)
+
+
+def test_concurrent_mode_matches_default_and_runs_in_threads(aci):
+    """aci_options.concurrent: single-cluster prrLU launches give the same
+    pivots and cores as the default tiers, and several products run concurrently on their own
+    streams from host threads with results identical to the sequential runs."""
+    import threading
+    import torch
+    cfgs = [make_config(3, 64, npts=0), make_config(1, npts=0), make_config(0, npts=0)]
+    ref = []
+    for cf in cfgs:
+        xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+        y0 = aci.TensorTrain.from_cores(cf["y_init"])
+        a, _, ra, ea = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0, log=True)
+        b, _, rb, eb = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0, log=True,
+                                           concurrent=True)
+        assert len(ea["log"]) == len(eb["log"])
+        for g, o in zip(ea["log"], eb["log"]):
+            assert np.array_equal(g["rows"], o["rows"]) and np.array_equal(g["cols"], o["cols"])
+        ca, cb = a.cores(), b.cores()
+        assert all(np.array_equal(x, y) for x, y in zip(ca, cb))
+        ref.append(ca)
+    results = [None] * len(cfgs)
+
+    def work(i):
+        cf = cfgs[i]
+        s = torch.cuda.Stream()
+        xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+        y0 = aci.TensorTrain.from_cores(cf["y_init"])
+        for _ in range(2):
+            out, *_ = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0,
+                                          stream=s.cuda_stream, concurrent=True)
+        results[i] = out.cores()
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(cfgs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for r, c in zip(results, ref):
+        assert all(np.array_equal(x, y) for x, y in zip(r, c))
+
+
+def test_concurrent_mode_rejects_blocks_beyond_one_cluster(aci):
+    cf = make_config(3, 256, npts=0)  # 1024 x 1024 blocks need four clusters
+    xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+    with pytest.raises(aci.AciError) as e:
+        aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], 1, concurrent=True)
+    assert e.value.code == -6

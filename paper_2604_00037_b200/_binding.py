@@ -10,7 +10,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libaci.so")
+# ACI_LIB overrides the library path (A/B measurements of two builds)
+LIB_PATH = os.environ.get("ACI_LIB", os.path.join(_HERE, "libaci.so"))
 
 ACI_OK, ACI_NOT_CONVERGED = 0, 1
 ERRORS = {-1: "ACI_ERR_INVALID", -2: "ACI_ERR_SHAPE", -3: "ACI_ERR_NONFINITE", -4: "ACI_ERR_OOM",

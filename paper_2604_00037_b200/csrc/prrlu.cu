@@ -1,28 +1,31 @@
 // prrLU with full pivoting (Alg. 2) — the latency-critical step a5 of the 2-site
 // update. Readings: R1 (relative threshold), R2 (stop rule, eps = first rejected candidate),
 // R3 (ties -> smallest (row, col)), R4 (l_i = S_iq * [S_pq]^{-1} — P:535 multiplies by the
-// inverse pivot, so one IEEE reciprocal per pivot —, S_ij <- fma(-l_i, S_pj, S_ij)), R17.
+// inverse pivot, so one IEEE reciprocal per pivot —, S_ij <- fma(-l_i, S_pj, S_ij)), R17;
+// complex entries: RZ1-RZ4.
 //
 // Design. The Schur complement lives in REGISTERS for the whole factorisation.
 // Rows run across the 32 lanes of a warp and columns across warps: thread (lane, w) holds
 // S[lane + 32 a][c0 + w + NW b] for a < EA, b < EB. So one warp owns whole columns, which
-// makes the pivot-column publication a coalesced single-warp store and lets that warp do the
-// release itself. Per pivot:
+// makes the pivot-column publication a coalesced single-warp store. Per pivot:
 //   rank-1 update, then a branch-free running (value, slot) max per thread
 //   -> warp argmax: 3 x redux.sync on the exact key (|v| bits hi, lo; flat index)
 //   -> CTA argmax: per-warp keys in smem, every warp reduces them itself
-//   -> [grid tier: the owner warp of the CTA candidate publishes key + column as tagged
-//       packets (each 8-byte word carries epoch|step, so no release/acquire fence is needed),
-//       arrives on a counter; one poll; every warp reads the G keys with all loads in flight]
+//   -> cross-CTA exchange of the tier (below)
 //   -> pivot column l = S_iq * (1/c) (R4) and pivot row u through smem.
-// The pivot's sign comes from the (published) pivot column, so keys carry only |v|.
+// The pivot's sign comes from the pivot column, so keys carry only |v| (complex: w = |z|^2).
 // Row p is zeroed exactly by l_p = 1 (fma(-1, u_j, u_j) = 0); column q by the owner warp.
 // Eliminated entries are exact zeros: for every active entry the arithmetic equals the
 // oracle's, so identical Pi gives bit-identical pivots.
-//   * CTA tier (GRID = false): one CTA (up to 32 register entries per thread), three
-//     __syncthreads per pivot.
-//   * grid tier (GRID = true): G co-resident CTAs (cooperative launch), column-partitioned.
-// The tier is chosen per launch on the device from the live block size (prrlu_kernel).
+// Tiers (chosen per launch on the device from the live block size, prrlu_kernel):
+//   * CTA tier (XM = 0): one CTA (up to 32 register entries per thread), two barriers per pivot.
+//   * cluster tier (XM = 2, default): whole 16-CTA clusters; keys pushed through DSMEM
+//     (st.async + mbarrier), the candidate column published to L2 as tagged packets (each
+//     8-byte word carries epoch|step, so no release/acquire fence is needed); several clusters
+//     exchange cluster winners through L2 (one poller per cluster + DSMEM broadcast).
+//   * L2 grid tier (XM = 1): cooperative launch, tagged key packets with a key-poll or counter
+//     barrier — used only when 16- and 8-CTA clusters cannot all be co-resident.
+//   * single-cluster mode (prrlu_kernel_one, aci_options.concurrent): at most one cluster.
 #include <cstdlib>
 
 #include "aci_common.cuh"

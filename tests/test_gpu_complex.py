@@ -142,3 +142,39 @@ def test_complex_identity_and_mixed_dtype_error(aci):
     r = aci.TensorTrain.from_cores(random_tt(10, 2, 4, _rng(92, 0)).cores)
     with pytest.raises(aci.AciError):
         aci.aci_elementwise({"coef": [1.0], "expo": [[1, 1]]}, [xs[0], r], 1e-12, 8, 4)
+
+
+def test_complex_concurrent_mode_and_zero_op(aci):
+    """Single-cluster mode (aci_options.concurrent) on complex data gives the default path's
+    pivots and cores; f == 0 gives the R17 rank-1 zero output."""
+    cf = make_config(5, 1000, npts=0)
+    xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+    y0 = aci.TensorTrain.from_cores(cf["y_init"])
+    cap = 128  # complex single-cluster blocks are limited to 256 x 512 (aci.h)
+    a, _, _, ea = aci.aci_elementwise(cf["op"], xs, cf["tol"], cap, cf["max_sweeps"], y_init=y0, log=True)
+    b, _, _, eb = aci.aci_elementwise(cf["op"], xs, cf["tol"], cap, cf["max_sweeps"], y_init=y0, log=True,
+                                      concurrent=True)
+    for g, o in zip(ea["log"], eb["log"]):
+        assert np.array_equal(g["rows"], o["rows"]) and np.array_equal(g["cols"], o["cols"])
+    assert all(np.array_equal(x, y) for x, y in zip(a.cores(), b.cores()))
+    z, st, rep, _ = aci.aci_elementwise({"coef": [0.0], "expo": [[1, 1]]}, xs, 1e-10, 16, 2, y_init=y0)
+    _, ranks = z.shape()
+    assert max(ranks) == 1
+    assert np.abs(z.cores()[0]).max() == 0.0  # Y_0 = Pi[:, J] = 0; the other cores are U rows e_q (R17)
+    idx = np.random.default_rng(1).integers(0, 2, size=(1000, 30)).astype(np.uint8)
+    assert np.abs(z.evaluate(idx)).max() == 0.0
+
+
+def test_complex_absolute_tolerance_mode(aci):
+    """Paper-literal absolute tau (tol_mode = ACI_TOL_ABSOLUTE) on complex data: identical
+    pivots to the oracle's absolute mode and max-norm error within 10 tau on samples."""
+    cf = make_config(5, 100, npts=5000)
+    xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+    y0 = aci.TensorTrain.from_cores(cf["y_init"])
+    tau = 1e-6
+    out, st, rep, ex = aci.aci_elementwise(cf["op"], xs, tau, cf["maxrank"], cf["max_sweeps"], y_init=y0, log=True,
+                                           tol_mode=aci.TOL_ABSOLUTE)
+    ref = oracle.aci_z(cf["inputs"], cf["op"], cf["y_init"], tau, cf["maxrank"], cf["max_sweeps"], relative=False)
+    assert _pivots_identical_or_tie(ex, ref) >= 20
+    exact = _fourier_values(cf["inputs"][0], cf["samples"]) * _fourier_values(cf["inputs"][1], cf["samples"])
+    assert np.abs(out.evaluate(cf["samples"]) - exact).max() <= 10 * tau

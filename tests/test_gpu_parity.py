@@ -335,3 +335,13 @@ def test_concurrent_mode_rejects_blocks_beyond_one_cluster(aci):
     with pytest.raises(aci.AciError) as e:
         aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], 1, concurrent=True)
     assert e.value.code == -6
+
+
+def test_iteration_times_reported(aci):
+    cf = make_config(3, 64, npts=0)
+    xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+    y0 = aci.TensorTrain.from_cores(cf["y_init"])
+    out, st, rep, ex = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0,
+                                           iter_times=True)
+    assert len(ex["iter_ms"]) == rep["iterations"]
+    assert all(t > 0 for t in ex["iter_ms"]) and sum(ex["iter_ms"]) < rep["ms"]

@@ -4,6 +4,8 @@
 //                                the configs[3] chi=256 shape 1024 x 1024 x 256, 53% of DMMA peak)
 //   A = L X, B = X R, C = S - AB: 64x32 CTA tile, 4 warps of 32x16 (more CTAs for the 512-row
 //                                shapes)
+#include <mutex>
+
 #include "gemm_kernel.cuh"
 
 namespace {
@@ -18,10 +20,7 @@ void launch_pi(const GemmDesc *d, int ndesc, int max_m, int max_n, const FOp &op
 }
 }  // namespace
 
-void gemm_init() {
-  // kernel attributes are set once, outside any stream capture
-  static bool done = false;
-  if (done) return;
+static void gemm_init_once() {
   set_attr<CfgAB, 1, 0, EPI_STORE>();
   set_attr<CfgAB, 1, 0, EPI_SUB>();
   set_attr<CfgPi, 1, 0, EPI_F>();
@@ -39,7 +38,12 @@ void gemm_init() {
   set_attr<CfgPi, 2, 0, EPI_FZ>();
   set_attr<CfgPi, 3, 0, EPI_FZ>();
   set_attr<CfgPi, 4, 0, EPI_FZ>();
-  done = true;
+}
+
+void gemm_init() {
+  // kernel attributes are set once (thread-safe), outside any stream capture
+  static std::once_flag once;
+  std::call_once(once, gemm_init_once);
 }
 
 int gemm_small_k() { return kSmallK; }

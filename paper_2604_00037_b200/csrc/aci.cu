@@ -231,7 +231,7 @@ struct InBond {
   const double *Xeb, *Xeb1;  // complex runs: expanded cores of sites b, b+1 (right operands)
   int c0, c1, c2;       // chi^n_b, chi^n_{b+1}, chi^n_{b+2}
 };
-struct BondStatic {
+struct alignas(8) BondStatic {
   int b, L, N, dir, db, db1;
   int Z;                // 1 real, 2 complex (interleaved left operands, expanded right operands)
   int ldu;              // static ld of the U store (nmax[b])
@@ -351,9 +351,18 @@ __global__ void update_bond_kernel(UpdateArgs U) {
   const int n = U.db1 * rr;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
   const size_t slot = (size_t)(*U.iter) * U.per_iter + U.step;
+  // warp 0 stages the next update's static description in shared memory with one coalesced pass
+  // (the planner's field-by-field reads from global memory were a ~15k-cycle dependent chain)
+  __shared__ BondStatic s_next;
+  if (blockIdx.x == 0 && threadIdx.x < 32 && U.next) {
+    const unsigned long long *src = reinterpret_cast<const unsigned long long *>(U.next);
+    unsigned long long *dst = reinterpret_cast<unsigned long long *>(&s_next);
+    for (int t = threadIdx.x; t < (int)(sizeof(BondStatic) / 8); t += 32) dst[t] = src[t];
+    __syncwarp();
+  }
   if (gt == 0) {
     U.rk[b + 1] = r;  // no thread of this kernel reads rk[b+1]
-    if (U.next) plan_bond(*U.next, U.rk, U.ab, U.pi, U.lu);  // reads the rank just written
+    if (U.next) plan_bond(s_next, U.rk, U.ab, U.pi, U.lu);  // reads the rank just written
     const double eps = *U.eps_in;
     atomicMax(U.maxeps_bits, (unsigned long long)__double_as_longlong(eps));
     int *li = U.log_info + slot * 5;

@@ -95,6 +95,8 @@ def test_fourier_product_identical_pivots_and_tolerance(aci, K):
     assert np.abs(y - exact).max() <= 10 * cf["tol"] * np.abs(exact).max()
     yo = oracle.tt_evaluate(ref.cores, cf["samples"])
     assert np.abs(y - yo).max() <= 10 * cf["tol"] * np.abs(yo).max()
+    frob = oracle.tt_norm(oracle.tt_axpby(1.0, out.cores(), -1.0, ref.cores)) / oracle.tt_norm(ref.cores)
+    assert frob <= 10 * cf["tol"]
     if agree == len(ref.log):
         assert rep["iterations"] == ref.report["iterations"]
         assert abs(rep["flops_contraction"] - ref.report["flops_contraction"]) <= 1e-9 * ref.report["flops_contraction"]

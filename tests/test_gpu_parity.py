@@ -61,6 +61,11 @@ def _rel(y, r):
     return np.abs(y - r).max() / np.abs(r).max()
 
 
+def _frob_rel(a, b):
+    """||a - b||_F / ||b||_F for two TTs, by a QR sweep over the difference TT (no cancellation)."""
+    return oracle.tt_norm(oracle.tt_axpby(1.0, a, -1.0, b)) / oracle.tt_norm(b)
+
+
 def test_cfg0_identical_pivots_and_dense(aci):
     cf = make_config(0, npts=0)
     out, st, rep, ex, ref = _run_both(aci, cf, index_sets=True)
@@ -113,6 +118,7 @@ def test_cfg3_chi64_vs_oracle(aci):
     exact = oracle.tt_evaluate(cf["inputs"][0], s) * oracle.tt_evaluate(cf["inputs"][1], s)
     assert _rel(y, oracle.tt_evaluate(ref.cores, s)) <= 10 * cf["tol"]
     assert _rel(y, exact) <= 10 * cf["tol"]
+    assert _frob_rel(out.cores(), ref.cores) <= 10 * cf["tol"]
     assert max(out.shape()[1]) == 128
     agree = _pivot_agreement(ex, ref)
     assert agree == len(ref.log), f"pivots identical for {agree}/{len(ref.log)} updates"
@@ -218,6 +224,7 @@ def test_cfg2_psi_cubed(aci):
     y = out.evaluate(s)
     assert _rel(y, oracle.tt_evaluate(ref.cores, s)) <= 10 * cf["tol"]
     assert _rel(y, _closed_psi(cf["inputs"][0].meta, s) ** 3) <= 10 * cf["tol"]
+    assert _frob_rel(out.cores(), ref.cores) <= 10 * cf["tol"]
     agree = _pivot_agreement(ex, ref)
     assert agree == len(ref.log), f"pivots identical for {agree}/{len(ref.log)} updates"
 
@@ -234,6 +241,7 @@ def test_cfg4_planewave_two_iterations(aci):
     agree = _pivot_agreement(ex, ref)
     assert agree == len(ref.log), f"pivots identical for {agree}/{len(ref.log)} updates"
     assert _rel(y, yo) <= 10 * cf["tol"]
+    assert _frob_rel(out.cores(), ref.cores) <= 10 * cf["tol"]
     assert max(out.shape()[1]) == 256
 
 
@@ -248,6 +256,8 @@ def test_cfg3_chi256_full_size(aci):
     exact = oracle.tt_evaluate(cf["inputs"][0], s) * oracle.tt_evaluate(cf["inputs"][1], s)
     assert _rel(y, exact) <= 10 * cf["tol"]
     assert _rel(y, oracle.tt_evaluate(ref.cores, s)) <= 10 * cf["tol"]
+    assert _frob_rel(out.cores(), ref.cores) <= 10 * cf["tol"]
+    assert _frob_rel(out.cores(), oracle.exact_product(cf["inputs"], cf["op"])) <= 10 * cf["tol"]
     agree = _pivot_agreement(ex, ref)
     assert agree == len(ref.log), f"pivots identical for {agree}/{len(ref.log)} updates"
 

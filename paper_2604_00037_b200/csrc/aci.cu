@@ -986,38 +986,56 @@ struct GraphEntry {
   cudaGraphExec_t exec;
   int64_t launches;
   uint64_t last_use;
+  int inuse;  // calls currently replaying it (concurrent calls on other streams): never evicted
 };
 static std::mutex g_cache_mu;
 static std::vector<GraphEntry> g_cache;
 static uint64_t g_cache_clock = 0;
 constexpr size_t kGraphCacheCap = 8;
 
-static cudaGraphExec_t graph_cache_get(const std::vector<uint64_t> &key, int64_t *launches) {
+// A hit is pinned (inuse) until graph_cache_release.
+static cudaGraphExec_t graph_cache_acquire(const std::vector<uint64_t> &key, int64_t *launches) {
   std::lock_guard<std::mutex> lk(g_cache_mu);
   for (auto &e : g_cache)
     if (e.key == key) {
       e.last_use = ++g_cache_clock;
+      ++e.inuse;
       *launches = e.launches;
       return e.exec;
     }
   return nullptr;
 }
-static void graph_cache_put(const std::vector<uint64_t> &key, cudaGraphExec_t exec, int64_t launches) {
+// Insert a freshly instantiated graph, pinned; evicts the least recently used idle entry when
+// full. Returns false (the caller keeps ownership) if every entry is in use.
+static bool graph_cache_insert(const std::vector<uint64_t> &key, cudaGraphExec_t exec, int64_t launches) {
   std::lock_guard<std::mutex> lk(g_cache_mu);
   if (g_cache.size() >= kGraphCacheCap) {
-    auto lru = std::min_element(g_cache.begin(), g_cache.end(),
-                                [](const GraphEntry &a, const GraphEntry &b) { return a.last_use < b.last_use; });
+    auto lru = g_cache.end();
+    for (auto it = g_cache.begin(); it != g_cache.end(); ++it)
+      if (it->inuse == 0 && (lru == g_cache.end() || it->last_use < lru->last_use)) lru = it;
+    if (lru == g_cache.end()) return false;
     cudaGraphExecDestroy(lru->exec);
     g_cache.erase(lru);
   }
-  g_cache.push_back({key, exec, launches, ++g_cache_clock});
+  g_cache.push_back({key, exec, launches, ++g_cache_clock, 1});
+  return true;
 }
-static void graph_cache_drop(cudaGraphExec_t exec) {
+// End of a call: unpin a cached graph (drop: also remove and destroy it, after a failure), or
+// destroy an uncached one.
+static void graph_cache_release(cudaGraphExec_t exec, bool cached, bool drop) {
+  if (!exec) return;
+  if (!cached) {
+    cudaGraphExecDestroy(exec);
+    return;
+  }
   std::lock_guard<std::mutex> lk(g_cache_mu);
   for (size_t i = 0; i < g_cache.size(); ++i)
     if (g_cache[i].exec == exec) {
-      cudaGraphExecDestroy(exec);
-      g_cache.erase(g_cache.begin() + i);
+      --g_cache[i].inuse;
+      if (drop && g_cache[i].inuse == 0) {
+        cudaGraphExecDestroy(exec);
+        g_cache.erase(g_cache.begin() + i);
+      }
       return;
     }
 }
@@ -1452,13 +1470,15 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
     prof.end(1);
   };
   cudaGraphExec_t gexec = nullptr;
+  bool gcached = false;
   int graph_iters = 0;
   auto tg0 = std::chrono::steady_clock::now();
   if (!prof.on && strm != nullptr) {
     // the captured iteration depends only on host values (shapes, pointers, op, tol), so a call
     // that repeats them (same workspace address and inputs) replays the instantiated graph
     const std::vector<uint64_t> key = graph_key(R, I.op, tol, o.tol_mode, ws, need, strm);
-    gexec = graph_cache_get(key, &prof.per_iter_launches);
+    gexec = graph_cache_acquire(key, &prof.per_iter_launches);
+    gcached = gexec != nullptr;
     if (!gexec) {
       cudaGraph_t graph = nullptr;
       const int64_t before = prof.total;
@@ -1472,7 +1492,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
       cudaGetLastError();  // a failed capture falls back to direct launches
       prof.per_iter_launches = prof.total - before;
       prof.total = before;
-      if (gexec) graph_cache_put(key, gexec, prof.per_iter_launches);
+      if (gexec) gcached = graph_cache_insert(key, gexec, prof.per_iter_launches);
     }
   }
   const float ms_graph = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - tg0).count();
@@ -1496,7 +1516,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
     cudaMemcpyAsync(&flag, R.conv, sizeof(int), cudaMemcpyDeviceToHost, strm);
     cudaError_t e = cudaStreamSynchronize(strm);
     if (e != cudaSuccess) {
-      if (gexec) graph_cache_drop(gexec);
+      graph_cache_release(gexec, gcached, true);
       cleanup();
       return fail(ACI_ERR_CUDA, std::string("aci sweep: ") + cudaGetErrorString(e));
     }
@@ -1505,6 +1525,8 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   }
   for (auto ev : ev_it)
     if (ev) cudaEventDestroy(ev);
+  graph_cache_release(gexec, gcached, false);  // every replay of this call is complete (synchronised)
+  gexec = nullptr;
   if (it > max_sweeps) it = max_sweeps;
   const int slot = it * 2 * (L - 1);
 

@@ -355,3 +355,32 @@ def test_iteration_times_reported(aci):
                                            iter_times=True)
     assert len(ex["iter_ms"]) == rep["iterations"]
     assert all(t > 0 for t in ex["iter_ms"]) and sum(ex["iter_ms"]) < rep["ms"]
+
+
+def test_graph_cache_under_concurrent_eviction(aci):
+    """More concurrent callers (own streams) than cached graphs: entries in use are never evicted
+    (the cache holds 8); every thread's results equal the sequential run's."""
+    import threading
+    import torch
+    cf = make_config(0, npts=0)
+    xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+    y0 = aci.TensorTrain.from_cores(cf["y_init"])
+    ref, *_ = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0)
+    ref = ref.cores()
+    n = 12
+    out = [None] * n
+
+    def work(i):
+        s = torch.cuda.Stream()
+        for _ in range(3):
+            o, *_ = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0,
+                                        stream=s.cuda_stream, concurrent=True)
+        out[i] = o.cores()
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(n)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for r in out:
+        assert all(np.array_equal(x, y) for x, y in zip(r, ref))

@@ -177,7 +177,8 @@ typedef struct {
                               * 2-site blocks must fit one cluster (real: 128 x 1024, 256 x 512,
                               * 512 x 512, 1024 x 256; complex: 128 x 1024, 256 x 512, 512 x 256),
                               * else ACI_ERR_UNSUPPORTED. 0 (default): the fastest tiers, which may
-                              * span several clusters — do not run those calls concurrently. */
+                              * span several clusters; such calls from several host threads are
+                              * serialised by the library (a process-wide lock). */
 } aci_options;
 
 /*

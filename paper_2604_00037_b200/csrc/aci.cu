@@ -1339,6 +1339,13 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   aci_options o = {};
   if (opts) o = *opts;
   if (o.tol_mode != ACI_TOL_RELATIVE && o.tol_mode != ACI_TOL_ABSOLUTE) return fail(ACI_ERR_INVALID, "aci: bad tol_mode");
+  // Default-tier calls may launch prrLU grids of several clusters that spin on each other; two
+  // such launches co-scheduled from different host threads could each hold part of their
+  // clusters and wait forever, so those calls are serialised within the process. Calls with
+  // aci_options.concurrent use single-cluster launches and run concurrently.
+  static std::mutex multi_cluster_mu;
+  std::unique_lock<std::mutex> serial(multi_cluster_mu, std::defer_lock);
+  if (!o.concurrent) serial.lock();
   Inputs I;
   int st = prepare(op, inputs, n_inputs, I);
   if (st) return st;

@@ -384,3 +384,18 @@ def test_graph_cache_under_concurrent_eviction(aci):
         t.join()
     for r in out:
         assert all(np.array_equal(x, y) for x, y in zip(r, ref))
+
+
+def test_warm_start_from_previous_output(aci):
+    """Repeated products (time stepping): passing the previous output
+    as y_init warm-starts the index sets, so the second product converges in at most 2
+    iterations with the same accuracy."""
+    cf = make_config(1, npts=20_000)
+    xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+    y0 = aci.TensorTrain.from_cores(cf["y_init"])
+    first, st1, r1, _ = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0)
+    second, st2, r2, _ = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=first)
+    assert r2["converged"] and r2["iterations"] <= 2 < r1["iterations"]
+    s = cf["samples"]
+    exact = oracle.tt_evaluate(cf["inputs"][0], s) * oracle.tt_evaluate(cf["inputs"][1], s)
+    assert _rel(second.evaluate(s), exact) <= 10 * cf["tol"]

@@ -87,31 +87,46 @@ static tt_s *tt_alloc_shape(int L, const int *d, const int *ranks, int cplx = 0)
   return t;
 }
 
+// NaN/Inf scan of a device buffer (flag |= 1), so tt_create validates on the device after the
+// upload instead of walking every host element before it.
+__global__ void nonfinite_scan_kernel(const double *x, size_t n, int *flag) {
+  int bad = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
 static int tt_create_impl(int L, const int *d, const int *ranks, const double *const *cores, int cplx,
                           tt_t **out) {
   if (!out || !cores) return fail(ACI_ERR_INVALID, "tt_create: null argument");
   int st = validate_shape(L, d, ranks);
   if (st) return st;
   if ((st = check_device())) return st;
+  for (int s = 0; s < L; ++s)
+    if (!cores[s]) return fail(ACI_ERR_INVALID, "tt_create: null core");
   tt_s *t = tt_alloc_shape(L, d, ranks, cplx);
-  for (int s = 0; s < L; ++s) {
-    if (!cores[s]) { delete t; return fail(ACI_ERR_INVALID, "tt_create: null core"); }
-    size_t sz = t->off[s + 1] - t->off[s];
-    for (size_t i = 0; i < sz; ++i)
-      if (!std::isfinite(cores[s][i])) { delete t; return fail(ACI_ERR_NONFINITE, "tt_create: NaN/Inf in core"); }
-  }
-  if (cudaMalloc(&t->dcores, sizeof(double) * std::max<size_t>(t->total, 1)) != cudaSuccess) {
+  if (cudaMalloc(&t->dcores, sizeof(double) * std::max<size_t>(t->total, 1) + sizeof(int)) != cudaSuccess) {
     delete t;
     return fail(ACI_ERR_OOM, "tt_create: cudaMalloc failed");
   }
-  for (int s = 0; s < L; ++s) {
-    cudaError_t e = cudaMemcpy(t->dcores + t->off[s], cores[s], sizeof(double) * (t->off[s + 1] - t->off[s]),
-                               cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-      cudaFree(t->dcores);
-      delete t;
-      return fail(ACI_ERR_CUDA, std::string("tt_create: ") + cudaGetErrorString(e));
-    }
+  // all cores enqueued back to back on the library stream (asynchronous DMA from pinned host
+  // memory), then one device-side NaN/Inf scan and a single synchronisation
+  cudaStream_t strm = lib_stream();
+  int *flag = reinterpret_cast<int *>(t->dcores + std::max<size_t>(t->total, 1));
+  cudaMemsetAsync(flag, 0, sizeof(int), strm);
+  for (int s = 0; s < L; ++s)
+    cudaMemcpyAsync(t->dcores + t->off[s], cores[s], sizeof(double) * (t->off[s + 1] - t->off[s]),
+                    cudaMemcpyHostToDevice, strm);
+  const size_t n = t->total;
+  if (n) nonfinite_scan_kernel<<<(int)std::min<size_t>(1184, (n + 255) / 256), 256, 0, strm>>>(t->dcores, n, flag);
+  int bad = 0;
+  cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, strm);
+  cudaError_t e = cudaStreamSynchronize(strm);
+  if (e != cudaSuccess || bad) {
+    cudaFree(t->dcores);
+    delete t;
+    if (e != cudaSuccess) return fail(ACI_ERR_CUDA, std::string("tt_create: ") + cudaGetErrorString(e));
+    return fail(ACI_ERR_NONFINITE, "tt_create: NaN/Inf in core");
   }
   *out = t;
   return ACI_OK;
@@ -179,11 +194,13 @@ extern "C" const double *tt_device_cores(const tt_t *t) { return t ? t->dcores :
 
 extern "C" int tt_get_cores(const tt_t *t, double *const *host_cores) {
   if (!t || !host_cores) return fail(ACI_ERR_INVALID, "tt_get_cores: null argument");
-  for (int s = 0; s < t->L; ++s) {
+  for (int s = 0; s < t->L; ++s)
     if (!host_cores[s]) return fail(ACI_ERR_INVALID, "tt_get_cores: null core buffer");
-    CUDA_TRY(cudaMemcpy(host_cores[s], t->dcores + t->off[s], sizeof(double) * (t->off[s + 1] - t->off[s]),
-                        cudaMemcpyDeviceToHost));
-  }
+  cudaStream_t strm = lib_stream();
+  for (int s = 0; s < t->L; ++s)
+    cudaMemcpyAsync(host_cores[s], t->dcores + t->off[s], sizeof(double) * (t->off[s + 1] - t->off[s]),
+                    cudaMemcpyDeviceToHost, strm);
+  CUDA_TRY(cudaStreamSynchronize(strm));
   return ACI_OK;
 }
 

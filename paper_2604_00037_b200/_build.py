@@ -35,6 +35,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+EXAMPLE_SRC = os.path.join(ROOT, "examples", "aci_example.c")
+EXAMPLE_BIN = os.path.join(ROOT, "examples", "aci_example")
+
+
+def build_example() -> str:
+    """Compile examples/aci_example.c (plain C against include/aci.h and libaci.so)."""
+    build()
+    cmd = ["gcc", "-O2", "-I", os.path.join(ROOT, "include"), EXAMPLE_SRC, "-L", HERE, "-laci",
+           "-Wl,-rpath," + HERE, "-lm", "-o", EXAMPLE_BIN]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return EXAMPLE_BIN
+
+
 if __name__ == "__main__":
     build(force=True, verbose=False)
     print(LIB)

@@ -72,3 +72,10 @@ def test_invalid_shapes_rejected(lib):
     st = lib.tt_create(2, d.ctypes.data_as(C.POINTER(C.c_int)), r.ctypes.data_as(C.POINTER(C.c_int)), ptrs, C.byref(h))
     assert st == -1
     assert b"boundary" in lib.aci_last_error()
+
+
+def test_c_example_builds_against_the_header():
+    """examples/aci_example.c uses only include/aci.h and links against libaci.so."""
+    from paper_2604_00037_b200 import _build
+    exe = _build.build_example()
+    assert os.path.exists(exe)

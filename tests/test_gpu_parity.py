@@ -399,3 +399,13 @@ def test_warm_start_from_previous_output(aci):
     s = cf["samples"]
     exact = oracle.tt_evaluate(cf["inputs"][0], s) * oracle.tt_evaluate(cf["inputs"][1], s)
     assert _rel(second.evaluate(s), exact) <= 10 * cf["tol"]
+
+
+def test_c_example_runs(aci):
+    """The plain-C example (no Python on the compute path) checks its own result."""
+    import subprocess
+    from paper_2604_00037_b200 import _build
+    exe = _build.build_example()
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "rel max error" in r.stdout

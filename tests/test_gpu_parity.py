@@ -409,3 +409,48 @@ def test_c_example_runs(aci):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "rel max error" in r.stdout
+
+
+def test_edge_shapes_vs_oracle(aci):
+    """Edge cases: maxrank 1 (every bond rank 1), mixed local dimensions including d = 1 sites,
+    four distinct inputs with an eight-term polynomial (the op limits of aci.h), and the same in
+    complex arithmetic; identical pivots (or roundoff ties for complex) and dense agreement."""
+    rng = np.random.default_rng(77)
+    # maxrank 1
+    xs = [G.random_tt(7, 2, 3, rng) for _ in range(2)]
+    y0 = G.random_init(xs, 1, rng)
+    op = {"coef": [1.0], "expo": [[1, 1]]}
+    out, st, rep, ex = aci.aci_elementwise(op, [aci.TensorTrain.from_cores(x) for x in xs], 1e-12, 1, 4,
+                                           y_init=aci.TensorTrain.from_cores(y0), log=True)
+    ref = oracle.aci(xs, op, y0, 1e-12, 1, 4)
+    assert max(out.shape()[1]) == 1 and _pivot_agreement(ex, ref) == len(ref.log)
+    assert _rel(oracle.tt_dense(out.cores()), oracle.tt_dense(ref.cores)) <= 1e-12
+    # mixed d (1, 3, 2, ...) and four inputs, eight terms
+    dims = [2, 1, 3, 2, 1, 2]
+    def rtt(chi):
+        ranks = [1] + [chi] * (len(dims) - 1) + [1]
+        return [rng.standard_normal((ranks[s], dims[s], ranks[s + 1])) / np.sqrt(chi * dims[s]) for s in range(len(dims))]
+    xs = [rtt(int(c)) for c in (2, 3, 2, 1)]
+    op = {"coef": [1.0, -0.5, 0.25, 2.0, -1.0, 0.5, 1.5, -0.75],
+          "expo": [[1, 1, 0, 0], [0, 0, 1, 1], [2, 0, 0, 0], [0, 2, 0, 0], [0, 0, 2, 0], [1, 0, 0, 1],
+                   [0, 1, 1, 0], [1, 1, 1, 1]]}
+    from workloads import TT
+    # y_init at the full-tensor bond bounds: the rank-1 input would otherwise make the R9
+    # initial guess rank 1, which the d = 1 sites keep from growing (a legitimate ACI stall)
+    full = [1] + [min(int(np.prod(dims[:s])), int(np.prod(dims[s:]))) for s in range(1, len(dims))] + [1]
+    y0 = TT([rng.standard_normal((full[s], dims[s], full[s + 1])) for s in range(len(dims))])
+    out, st, rep, ex = aci.aci_elementwise(op, [aci.TensorTrain.from_cores(x) for x in xs], 1e-12, 64, 6,
+                                           y_init=aci.TensorTrain.from_cores(y0), log=True)
+    ref = oracle.aci(xs, op, y0, 1e-12, 64, 6)
+    assert _pivot_agreement(ex, ref) == len(ref.log)
+    D = [oracle.tt_dense(x) for x in xs]
+    exact = sum(c * np.prod([D[n] ** e for n, e in enumerate(ex_)], axis=0) for c, ex_ in zip(op["coef"], op["expo"]))
+    assert _rel(oracle.tt_dense(out.cores()), exact) <= 1e-10
+    # the same four inputs made complex
+    xz = [[c + 1j * rng.standard_normal(c.shape) / 3 for c in x] for x in xs]
+    yz = [c + 1j * rng.standard_normal(c.shape) for c in y0.cores]
+    outz, st, rep, exz = aci.aci_elementwise(op, [aci.TensorTrain.from_cores(x) for x in xz], 1e-12, 64, 6,
+                                             y_init=aci.TensorTrain.from_cores(yz), log=True)
+    Dz = [oracle.tt_dense(x) for x in xz]
+    exactz = sum(c * np.prod([Dz[n] ** e for n, e in enumerate(ex_)], axis=0) for c, ex_ in zip(op["coef"], op["expo"]))
+    assert _rel(oracle.tt_dense(outz.cores()), exactz) <= 1e-10

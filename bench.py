@@ -339,6 +339,43 @@ def main():
                 "note": "paper (EPYC 9474F, 1 thread, Julia): ACI runtime ~ chi^2.3 (P:307); flops counted as 4x "
                         "the real contraction model (complex products)"}
 
+    def run_all_configs(reps=2):
+        """Every BASELINE.json config (and the complex configs[5]) once more: device ms per product
+        (CUDA events, after one warm-up), iterations, pivots, max rank, and the relative max error
+        against f applied to the inputs' values on 10^4 seeded points (R16)."""
+        rows = []
+        for cfg, arg in ((0, 0), (1, 0), (2, 0), (3, 64), (4, 0), (5, 4000)):
+            cf = make_config(cfg, arg, npts=10_000)
+            xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+            handles, op = xs, cf["op"]
+            if cfg == 2:  # psi^3 with three aliased handles, merged by the library
+                handles, op = [xs[0]] * 3, {"coef": [1.0], "expo": [[1, 1, 1]]}
+            y0 = aci.TensorTrain.from_cores(cf["y_init"])
+            out, st, rep, _ = aci.aci_elementwise(op, handles, cf["tol"], cf["maxrank"], cf["max_sweeps"],
+                                                  y_init=y0, stream=sptr)
+            out.free()
+            tot = 0.0
+            for _ in range(reps):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                out, st, rep, _ = aci.aci_elementwise(op, handles, cf["tol"], cf["maxrank"], cf["max_sweeps"],
+                                                      y_init=y0, stream=sptr)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                tot += e0.elapsed_time(e1)
+            smp = cf["samples"]
+            vals = [x.evaluate(smp) for x in xs]
+            ref = sum(c * np.prod([vals[n] ** e for n, e in enumerate(ex_)], axis=0)
+                      for c, ex_ in zip(cf["op"]["coef"], cf["op"]["expo"]))
+            err = float(np.abs(out.evaluate(smp) - ref).max() / np.abs(ref).max())
+            rows.append({"config": cf["name"], "ms_per_product": tot / reps, "iterations": rep["iterations"],
+                         "converged": bool(rep["converged"]), "pivots": rep["pivot_steps"],
+                         "max_rank": rep["max_rank"], "tol": cf["tol"], "rel_max_err_vs_f_of_inputs": err,
+                         "tflops": rep["flops_contraction"] / (tot / reps) / 1e9})
+            out.free()
+        return rows
+
     def run_steady(chis, iters=6):
         """Steady-state full-rank iterations: configs[3] run for `iters`
         iterations so that the last one is at the saturated ranks (2 chi); its device time
@@ -428,6 +465,7 @@ def main():
     cf, tot_ms, tot_flops, launches, prof, reps, clocks, e2e = run_chi(args.chi, args.steps, args.warmup,
                                                                        with_e2e=True)
     steady = run_steady((64, 128, 256)) if (ws == 1 and not args.no_chi_sweep) else None
+    allcfg = run_all_configs() if (ws == 1 and not args.no_chi_sweep) else None
     conc = run_concurrent() if (ws == 1 and not args.no_chi_sweep) else None
     cplx = None
     if ws == 1 and not args.no_complex:
@@ -515,6 +553,8 @@ def main():
                                          "count grows ~linearly in chi"}
         if steady is not None:
             line["steady_state_half_sweep"] = steady
+        if allcfg is not None:
+            line["all_configs"] = allcfg
         if conc is not None:
             line["concurrent_products"] = conc
         if cplx is not None:

@@ -995,6 +995,61 @@ static double normal_at(uint64_t seed, uint64_t i) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------- workspaces
+// One persistent workspace per stream, grown on demand: calls on a stream are serialised (each
+// returns after synchronising it), and a stable address lets repeated products hit the graph
+// cache (the captured iteration embeds workspace pointers). At most kWsCap idle workspaces are
+// kept (least recently used freed first); a workspace in use by a running call is never freed.
+struct WsEntry {
+  cudaStream_t st;
+  char *ptr;
+  size_t size;
+  int inuse;
+  uint64_t last_use;
+};
+static std::mutex g_ws_mu;
+static std::vector<WsEntry> g_ws;
+static uint64_t g_ws_clock = 0;
+constexpr size_t kWsCap = 16;
+
+static char *stream_workspace_acquire(cudaStream_t st, size_t need) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  for (auto &e : g_ws)
+    if (e.st == st) {
+      if (e.size < need) {
+        cudaFree(e.ptr);
+        e.ptr = nullptr;
+        e.size = 0;
+        if (cudaMalloc((void **)&e.ptr, need) != cudaSuccess) return nullptr;
+        e.size = need;
+      }
+      ++e.inuse;
+      e.last_use = ++g_ws_clock;
+      return e.ptr;
+    }
+  while (g_ws.size() >= kWsCap) {
+    auto lru = g_ws.end();
+    for (auto it = g_ws.begin(); it != g_ws.end(); ++it)
+      if (it->inuse == 0 && (lru == g_ws.end() || it->last_use < lru->last_use)) lru = it;
+    if (lru == g_ws.end()) break;
+    cudaFree(lru->ptr);
+    g_ws.erase(lru);
+  }
+  char *p = nullptr;
+  if (cudaMalloc((void **)&p, need) != cudaSuccess) return nullptr;
+  g_ws.push_back({st, p, need, 1, ++g_ws_clock});
+  return p;
+}
+
+static void stream_workspace_release(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  for (auto &e : g_ws)
+    if (e.st == st) {
+      --e.inuse;
+      return;
+    }
+}
+
 // ---------------------------------------------------------------------------- graph cache
 // Instantiated iteration graphs keyed by every host value the capture reads: capture plus
 // instantiation of ~1500 nodes costs ~10 ms of host time per call, the replay is free.
@@ -1411,26 +1466,16 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
     if (o.workspace_bytes < need) { tt_destroy(ygen); return fail(ACI_ERR_OOM, "aci: caller workspace too small"); }
     ws = (char *)o.workspace;
   } else {
-    static bool pool_cfg = false;
-    if (!pool_cfg) {
-      cudaMemPool_t pool;
-      int dev = 0;
-      cudaGetDevice(&dev);
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      }
-      pool_cfg = true;
-    }
-    if (cudaMallocAsync((void **)&ws, need, strm) != cudaSuccess) {
+    ws = stream_workspace_acquire(strm, need);  // pinned until cleanup()
+    own_ws = ws != nullptr;
+    if (!ws) {
       tt_destroy(ygen);
       return fail(ACI_ERR_OOM, "aci: workspace allocation failed");
     }
-    own_ws = true;
   }
   carve(R, ws);
   auto cleanup = [&]() {
-    if (own_ws) cudaFreeAsync(ws, strm);
+    if (own_ws) stream_workspace_release(strm);
     tt_destroy(ygen);
   };
 

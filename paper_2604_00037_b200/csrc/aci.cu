@@ -40,6 +40,8 @@ struct tt_s {
   std::vector<size_t> off;  // L+1 offsets (doubles; 2 per complex entry)
   double *dcores = nullptr;
   size_t total = 0;
+  int dev = 0;              // device the cores live on
+  int pooled = 0;           // 1: dcores came from core_pool()
 };
 
 // The library's own stream (per host thread), used when the caller passes NULL.
@@ -47,6 +49,56 @@ static cudaStream_t lib_stream() {
   static thread_local cudaStream_t s = nullptr;
   if (!s) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
   return s;
+}
+
+// Core storage comes from a library-owned stream-ordered pool per device that never returns
+// memory to the driver (release threshold = max): an output reuses the pages of the TT destroyed
+// before it instead of paying for fresh page mappings (a fresh cudaMalloc of the 160 MB
+// chi = 256 output measured 0-95 ms on top of a 72 ms product).
+static cudaMemPool_t core_pool() {
+  constexpr int kMaxDev = 64;
+  static std::mutex mu;
+  static cudaMemPool_t pools[kMaxDev] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDev) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps pp = {};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = dev;
+    if (cudaMemPoolCreate(&pools[dev], &pp) != cudaSuccess) { pools[dev] = nullptr; cudaGetLastError(); return nullptr; }
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  return pools[dev];
+}
+
+static cudaError_t core_alloc(tt_s *t, size_t bytes, cudaStream_t st) {
+  cudaGetDevice(&t->dev);
+  cudaMemPool_t pool = core_pool();
+  t->pooled = pool != nullptr;
+  if (!pool) return cudaMalloc(&t->dcores, bytes);
+  return cudaMallocFromPoolAsync((void **)&t->dcores, bytes, pool, st);
+}
+
+// cudaFree's contract (outstanding work that may read the cores finishes first), then the
+// memory goes back to the pool.
+static void core_free(tt_s *t) {
+  if (!t->dcores) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != t->dev) cudaSetDevice(t->dev);
+  if (t->pooled) {
+    cudaDeviceSynchronize();
+    cudaFreeAsync(t->dcores, lib_stream());
+    cudaStreamSynchronize(lib_stream());
+  } else {
+    cudaFree(t->dcores);
+  }
+  if (cur != t->dev) cudaSetDevice(cur);
+  t->dcores = nullptr;
 }
 
 static int check_device() {
@@ -105,13 +157,14 @@ static int tt_create_impl(int L, const int *d, const int *ranks, const double *c
   for (int s = 0; s < L; ++s)
     if (!cores[s]) return fail(ACI_ERR_INVALID, "tt_create: null core");
   tt_s *t = tt_alloc_shape(L, d, ranks, cplx);
-  if (cudaMalloc(&t->dcores, sizeof(double) * std::max<size_t>(t->total, 1) + sizeof(int)) != cudaSuccess) {
-    delete t;
-    return fail(ACI_ERR_OOM, "tt_create: cudaMalloc failed");
-  }
   // all cores enqueued back to back on the library stream (asynchronous DMA from pinned host
   // memory), then one device-side NaN/Inf scan and a single synchronisation
   cudaStream_t strm = lib_stream();
+  if (core_alloc(t, sizeof(double) * std::max<size_t>(t->total, 1) + sizeof(int), strm) != cudaSuccess) {
+    cudaGetLastError();
+    delete t;
+    return fail(ACI_ERR_OOM, "tt_create: device allocation failed");
+  }
   int *flag = reinterpret_cast<int *>(t->dcores + std::max<size_t>(t->total, 1));
   cudaMemsetAsync(flag, 0, sizeof(int), strm);
   for (int s = 0; s < L; ++s)
@@ -123,7 +176,7 @@ static int tt_create_impl(int L, const int *d, const int *ranks, const double *c
   cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, strm);
   cudaError_t e = cudaStreamSynchronize(strm);
   if (e != cudaSuccess || bad) {
-    cudaFree(t->dcores);
+    core_free(t);
     delete t;
     if (e != cudaSuccess) return fail(ACI_ERR_CUDA, std::string("tt_create: ") + cudaGetErrorString(e));
     return fail(ACI_ERR_NONFINITE, "tt_create: NaN/Inf in core");
@@ -149,15 +202,16 @@ static int tt_create_device_impl(int L, const int *d, const int *ranks, const do
   if (st) return st;
   if ((st = check_device())) return st;
   tt_s *t = tt_alloc_shape(L, d, ranks, cplx);
-  if (cudaMalloc(&t->dcores, sizeof(double) * std::max<size_t>(t->total, 1)) != cudaSuccess) {
-    delete t;
-    return fail(ACI_ERR_OOM, "tt_create_device: cudaMalloc failed");
-  }
   cudaStream_t s = (cudaStream_t)stream;
+  if (core_alloc(t, sizeof(double) * std::max<size_t>(t->total, 1), s) != cudaSuccess) {
+    cudaGetLastError();
+    delete t;
+    return fail(ACI_ERR_OOM, "tt_create_device: device allocation failed");
+  }
   cudaMemcpyAsync(t->dcores, dev_cores, sizeof(double) * t->total, cudaMemcpyDeviceToDevice, s);
   cudaError_t e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
-    cudaFree(t->dcores);
+    core_free(t);
     delete t;
     return fail(ACI_ERR_CUDA, std::string("tt_create_device: ") + cudaGetErrorString(e));
   }
@@ -177,7 +231,7 @@ extern "C" int tt_create_device_z(int L, const int *d, const int *ranks, const d
 
 extern "C" int tt_destroy(tt_t *t) {
   if (!t) return ACI_OK;
-  if (t->dcores) cudaFree(t->dcores);
+  core_free(t);
   delete t;
   return ACI_OK;
 }
@@ -1615,7 +1669,8 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
 
   // ---- a8: output cores from the last right-to-left half-sweep (R5)
   tt_s *res = tt_alloc_shape(L, t0->d.data(), rk.data(), R.cplx);
-  if (cudaMalloc(&res->dcores, sizeof(double) * std::max<size_t>(res->total, 1)) != cudaSuccess) {
+  if (core_alloc(res, sizeof(double) * std::max<size_t>(res->total, 1), strm) != cudaSuccess) {
+    cudaGetLastError();
     delete res;
     cleanup();
     return fail(ACI_ERR_OOM, "aci: output allocation failed");

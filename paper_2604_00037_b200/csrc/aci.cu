@@ -293,12 +293,13 @@ __global__ void eval_desc_kernel(GemmDesc *desc, const double *V, const double *
 // ---------------------------------------------------------------------------- sweep state
 // Static (host-known) pointers and dims of one bond for one input.
 struct InBond {
-  const double *Lprev;  // L^n_{b-1} (rmax[b-1] x chi_b, ld chi_b); null at b == 0 (L_{-1} = [1])
   const double *Xb, *Xb1;
-  const double *Rnext;  // R^n_{b+2} (chi_{b+2} x rmax[b+1], ld ldR); null at b == L-2 (R_L = [1])
+  const double *Rnext;  // R^n_{b+2} (chi_{b+2} x rmax[b+1], ld ldR) of the canonicalisation; null at
+                        // b == L-2 (R_L = [1]); read once, for the first L->R half-sweep's B^n_b
   int ldR;
-  double *Abuf, *Bbuf;  // per-bond scratch of the half that depends on this sweep's pivots
-  double *Apre, *Bpre;  // this bond's half that does not (computed for all bonds at half-sweep start)
+  double *Ast, *Bst;    // this bond's Pi operands A^n_b (null at b == 0: X^n_0) and B^n_b (null at
+                        // b == L-2: X^n_{L-1}), kept across half-sweeps
+  double *Ahat, *Bhat;  // look-ahead scratch (A^n_b X^n_{b+1} in L->R, X^n_b B^n_b in R->L)
   const double *Xeb, *Xeb1;  // complex runs: expanded cores of sites b, b+1 (right operands)
   int c0, c1, c2;       // chi^n_b, chi^n_{b+1}, chi^n_{b+2}
 };
@@ -314,16 +315,6 @@ struct alignas(8) BondStatic {
 // Complex runs (S.Z = 2) use the same real GEMMs: a complex left operand (M x K) is read as the
 // real M x 2K matrix of its interleaved storage, a right operand is stored 2x2-block expanded
 // (2K x 2N), so K and N double; a2's result is written expanded (EPI_STORE_X, xd = d_{b+1}).
-// a1: A^n = L^n_{b-1} X^n_b : (rl x c0) (c0 x db*c1) -> rl x (db c1) == (rl db) x c1
-__device__ __forceinline__ GemmDesc desc_a(const BondStatic &S, const InBond &I, int rl, double *C) {
-  GemmDesc a = {};
-  if (!I.Lprev) return a;
-  const int z = S.Z;
-  a.C = C; a.M = rl; a.N = z * S.db * I.c1; a.ldc = z * S.db * I.c1; a.nin = 1;
-  a.A[0] = I.Lprev; a.lda[0] = z * I.c0; a.K[0] = z * I.c0;
-  a.B[0] = z == 2 ? I.Xeb : I.Xb; a.ldb[0] = z * S.db * I.c1;
-  return a;
-}
 // a2: B^n = X^n_{b+1} R^n_{b+2} : (c1 db1 x c2) (c2 x rr) -> (c1 db1) x rr == c1 x (db1 rr)
 __device__ __forceinline__ GemmDesc desc_b(const BondStatic &S, const InBond &I, int rr, double *C) {
   GemmDesc bb = {};
@@ -336,10 +327,15 @@ __device__ __forceinline__ GemmDesc desc_b(const BondStatic &S, const InBond &I,
   return bb;
 }
 
-// Live sizes -> GEMM descriptors of one bond update and its prrLU dims. Only the half that
-// depends on the pivots of this sweep is computed per bond (A^n in L->R, B^n in R->L, into
-// ab[0..N-1]); the other half was computed for every bond at the start of the half-sweep
-// (plan_pre_kernel), because it reads frames of the previous half-sweep only (R20).
+// Live sizes -> the a3+a4 descriptor, the prrLU dims and the look-ahead GEMM of one bond update.
+// Pi's operands are stored per bond: A^n_b is written by the L->R update of bond b-1, B^n_b by the
+// R->L update of bond b+1 (before the first iteration: by a one-time launch from the canonical R
+// frames, plan_pre_kernel). The look-ahead computes, while this bond's prrLU runs on its own SMs,
+// the product whose rows (L->R) or columns (R->L) the new pivots select as the next bond's operand:
+//   L->R: A^n_{b+1} = L^n_b X^n_{b+1} = (A^n_b X^n_{b+1})[I_b rows]       (L^n_b = A^n_b[I_b])
+//   R->L: B^n_{b-1} = X^n_b R^n_{b+1} = (X^n_b B^n_b)[:, J_{b+1} cols]     (R^n_{b+1} = B^n_b[:, J])
+// so no GEMM sits between the update of one bond and the Pi of the next. An L->R bond reads B^n_b
+// of the previous R->L half-sweep and an R->L bond A^n_b of this iteration's L->R (R20).
 __device__ void plan_bond(const BondStatic &S, const int *rk, GemmDesc *ab, GemmDesc *pi, LuDims *lu) {
   const int b = S.b;
   const int rl = rk[b], rr = rk[b + 2];
@@ -349,13 +345,25 @@ __device__ void plan_bond(const BondStatic &S, const int *rk, GemmDesc *ab, Gemm
   P.C = S.Pi; P.M = m; P.N = z * n; P.ldc = z * n; P.nin = S.N;
   for (int i = 0; i < S.N; ++i) {
     const InBond &I = S.in[i];
-    ab[i] = S.dir == 0 ? desc_a(S, I, rl, I.Abuf) : desc_b(S, I, rr, I.Bbuf);
     // a3: Pi^n = A^n B^n : (m x c1) (c1 x n)
-    P.A[i] = I.Lprev ? (S.dir == 0 ? I.Abuf : I.Apre) : I.Xb;
+    P.A[i] = b > 0 ? I.Ast : I.Xb;
     P.lda[i] = z * I.c1;
     P.K[i] = z * I.c1;
-    P.B[i] = I.Rnext ? (S.dir == 0 ? I.Bpre : I.Bbuf) : (z == 2 ? I.Xeb1 : I.Xb1);
+    P.B[i] = b + 2 < S.L ? I.Bst : (z == 2 ? I.Xeb1 : I.Xb1);
     P.ldb[i] = z * n;
+    GemmDesc h = {};
+    if (S.dir == 0 && b + 2 < S.L) {
+      // (m x c1) (c1 x db1 c2) -> m x (db1 c2); complex: interleaved rows, expanded X
+      h.C = I.Ahat; h.M = m; h.N = z * S.db1 * I.c2; h.ldc = h.N; h.nin = 1;
+      h.A[0] = P.A[i]; h.lda[0] = z * I.c1; h.K[0] = z * I.c1;
+      h.B[0] = z == 2 ? I.Xeb1 : I.Xb1; h.ldb[0] = z * S.db1 * I.c2;
+    } else if (S.dir == 1 && b > 0) {
+      // (c0 db x c1) (c1 x n) -> (c0 db) x n == c0 x (db n); complex: written expanded (xd = db)
+      h.C = I.Bhat; h.M = I.c0 * S.db; h.N = z * n; h.ldc = z == 2 ? 2 * S.db * n : n; h.xd = S.db; h.nin = 1;
+      h.A[0] = I.Xb; h.lda[0] = z * I.c1; h.K[0] = z * I.c1;
+      h.B[0] = P.B[i]; h.ldb[0] = z * n;
+    }
+    ab[i] = h;
   }
   *pi = P;
   LuDims D;
@@ -369,14 +377,14 @@ __global__ void plan_bond_kernel(const BondStatic *S, const int *rk, GemmDesc *a
   plan_bond(*S, rk, ab, pi, lu);
 }
 
-// Descriptors of the pivot-independent half of every bond of a half-sweep (dir 0: B^n_b for
-// b = 0..L-3; dir 1: A^n_b for b = 1..L-2), one thread per (bond, input).
+// Descriptors of B^n_b = X^n_{b+1} R^n_{b+2} for every bond b = 0..L-3 from the canonical R frames
+// (once per product, before the first L->R half-sweep), one thread per (bond, input).
 __global__ void plan_pre_kernel(const BondStatic *S, int nb, int N, const int *rk, GemmDesc *pre) {
   for (int t = threadIdx.x; t < nb * N; t += blockDim.x) {
     const int b = t / N, i = t % N;
     const BondStatic &B = S[b];
     const InBond &I = B.in[i];
-    pre[t] = B.dir == 0 ? desc_b(B, I, rk[b + 2], I.Bpre) : desc_a(B, I, rk[b], I.Apre);
+    pre[t] = desc_b(B, I, rk[b + 2], I.Bst);
   }
 }
 
@@ -389,12 +397,12 @@ struct UpdateArgs {
   int *rk;
   uint8_t *Iprev, *Inew;      // Imi[b-1] (rmax[b-1] x b), Imi[b] (rmax[b] x (b+1))
   uint8_t *Jnext, *Jnew;      // Jmi[b+2] (x (L-b-2)), Jmi[b+1] (x (L-b-1))
-  const double *A[ACI_GEMM_MAX_IN];  // A^n (m x c1), ld c1   (L->R gather)
-  double *Lnew[ACI_GEMM_MAX_IN];     // L^n_b (rmax[b] x c1)
-  const double *B[ACI_GEMM_MAX_IN];  // B^n (c1 x n), ld n     (R->L gather)
-  double *Rnew[ACI_GEMM_MAX_IN];     // R^n_{b+1} (c1 x rmax[b]), ld ldRnew
-  int ldRnew;
-  int c1[ACI_GEMM_MAX_IN];
+  const double *Ahat[ACI_GEMM_MAX_IN];  // L->R: A^n_b X^n_{b+1} (m x W doubles)
+  double *Anext[ACI_GEMM_MAX_IN];       // A^n_{b+1} = Ahat[I_b rows] (r x W); null at b == L-2
+  int W[ACI_GEMM_MAX_IN];               // Z d_{b+1} chi^n_{b+2}
+  const double *Bhat[ACI_GEMM_MAX_IN];  // R->L: X^n_b B^n_b ((c0 d_b) x n; complex expanded, ld 2 d_b n)
+  double *Bprev[ACI_GEMM_MAX_IN];       // B^n_{b-1} = Bhat[:, J cols] (c0 x d_b r); null at b == 0
+  int c0[ACI_GEMM_MAX_IN];
   const double *Pi;           // for Y_0 at b == 0 (R->L)
   double *Y0;                 // d_0 x rmax[0], ld = r
   unsigned long long *maxeps_bits;
@@ -458,49 +466,51 @@ __global__ void update_bond_kernel(UpdateArgs U) {
     U.Jnew[t] = pos == 0 ? (uint8_t)(col / rr) : U.Jnext[(col % rr) * (wJ - 1) + pos - 1];
   }
   if (U.dir == 0) {
+    // A^n_{b+1}[k][:] = Ahat[rows[k]][:] (a row of the look-ahead product is (sigma', beta) of
+    // the next bond's (k, sigma') x beta operand)
     for (int i = 0; i < U.N; ++i) {
-      if (!U.Lnew[i]) continue;
-      const int c1 = U.c1[i] * U.Z;  // complex rows are 2 c1 doubles (interleaved)
-      for (int t = gt; t < r * c1; t += gs) {
-        const int k = t / c1, bb = t % c1;
-        U.Lnew[i][t] = U.A[i][(size_t)U.rows[k] * c1 + bb];
-      }
-    }
-  } else if (U.Z == 1) {
-    for (int i = 0; i < U.N; ++i) {
-      if (!U.Rnew[i]) continue;
-      const int c1 = U.c1[i];
-      for (int t = gt; t < c1 * r; t += gs) {
-        const int a = t / r, k = t % r;
-        U.Rnew[i][(size_t)a * U.ldRnew + k] = U.B[i][(size_t)a * n + U.cols[k]];
-      }
-    }
-    if (b == 0) {
-      const int m = rl * U.db;
-      for (int t = gt; t < m * r; t += gs) {
-        const int ii = t / r, k = t % r;
-        U.Y0[t] = U.Pi[(size_t)ii * n + U.cols[k]];
+      if (!U.Anext[i]) continue;
+      const int W = U.W[i];
+      for (int t = gt; t < r * W; t += gs) {
+        const int k = t / W, j = t - k * W;
+        U.Anext[i][t] = U.Ahat[i][(size_t)U.rows[k] * W + j];
       }
     }
   } else {
-    // complex: B^n and R frames are expanded (2 c1 x 2 n, ld 2 n / 2 ldRnew): copy the 2x2 blocks
+    const int db = U.db;
     for (int i = 0; i < U.N; ++i) {
-      if (!U.Rnew[i]) continue;
-      const int c1 = U.c1[i];
-      for (int t = gt; t < 2 * c1 * r; t += gs) {
-        const int a2 = t / r, k = t % r;
-        const double *src = U.B[i] + (size_t)a2 * 2 * n + 2 * U.cols[k];
-        double *dst = U.Rnew[i] + (size_t)a2 * 2 * U.ldRnew + 2 * k;
-        dst[0] = src[0];
-        dst[1] = src[1];
+      if (!U.Bprev[i]) continue;
+      const int c0 = U.c0[i];
+      if (U.Z == 1) {
+        // B^n_{b-1}[alpha][sigma r + k] = Bhat[alpha db + sigma][cols[k]]
+        for (int t = gt; t < c0 * db * r; t += gs) {
+          const int row = t / r, k = t - row * r;
+          U.Bprev[i][t] = U.Bhat[i][(size_t)row * n + U.cols[k]];
+        }
+      } else {
+        // expanded 2x2 blocks: rows 2 alpha + {0,1}, columns 2 (sigma x + k) + {0,1}
+        for (int t = gt; t < 2 * c0 * db * r; t += gs) {
+          const int a2 = t / (db * r), rem = t - a2 * (db * r), sg = rem / r, k = rem - sg * r;
+          const double *src = U.Bhat[i] + (size_t)a2 * 2 * db * n + 2 * ((size_t)sg * n + U.cols[k]);
+          double *dst = U.Bprev[i] + (size_t)a2 * 2 * db * r + 2 * ((size_t)sg * r + k);
+          dst[0] = src[0];
+          dst[1] = src[1];
+        }
       }
     }
     if (b == 0) {
       const int m = rl * U.db;
-      for (int t = gt; t < m * r; t += gs) {
-        const int ii = t / r, k = t % r;
-        U.Y0[2 * t] = U.Pi[((size_t)ii * n + U.cols[k]) * 2];
-        U.Y0[2 * t + 1] = U.Pi[((size_t)ii * n + U.cols[k]) * 2 + 1];
+      if (U.Z == 1) {
+        for (int t = gt; t < m * r; t += gs) {
+          const int ii = t / r, k = t % r;
+          U.Y0[t] = U.Pi[(size_t)ii * n + U.cols[k]];
+        }
+      } else {
+        for (int t = gt; t < m * r; t += gs) {
+          const int ii = t / r, k = t % r;
+          U.Y0[2 * t] = U.Pi[((size_t)ii * n + U.cols[k]) * 2];
+          U.Y0[2 * t + 1] = U.Pi[((size_t)ii * n + U.cols[k]) * 2 + 1];
+        }
       }
     }
   }
@@ -842,11 +852,11 @@ struct Run {
   double *epsb = nullptr, *err = nullptr;
   unsigned long long *scale = nullptr, *maxeps = nullptr;
   std::vector<int *> prow, pcol;
-  std::vector<std::vector<double *>> Lf, Rf;
-  std::vector<double *> Abuf, Bbuf, Ust, Yin, Yabs;
-  std::vector<std::vector<double *>> Apre, Bpre;  // [n][b]: pivot-independent halves (R->L A, L->R B)
+  std::vector<std::vector<double *>> Rf;  // [n][s]: R frames of the canonicalisation
+  std::vector<double *> Abuf, Bbuf, Ust, Yin, Yabs;  // Abuf/Bbuf: look-ahead scratch per input
+  std::vector<std::vector<double *>> Ast, Bst;  // [n][b]: Pi operands A^n_b, B^n_b (plan_bond)
   BondStatic *dStat = nullptr;   // [dir * (L-1) + b], uploaded once per call
-  GemmDesc *dPre = nullptr;      // (L-1) * N descriptors of the half-sweep's pre-launch
+  GemmDesc *dPre = nullptr;      // (L-1) * N descriptors of the one-time B^n_b launch
   std::vector<BondStatic> hStat;
   std::vector<int> nbig, nsmall; // [dir * (L-1) + b]: Pi kernel input split
   std::vector<FOp> opb;          // [dir * (L-1) + b]: op with exponents in Pi input order
@@ -909,30 +919,30 @@ static size_t carve(Run &R, char *base) {
     R.prow[s] = c.take<int>(cap + 1);
     R.pcol[s] = c.take<int>(cap + 1);
   }
-  R.Lf.assign(N, std::vector<double *>(L, nullptr));
   R.Rf.assign(N, std::vector<double *>(L + 1, nullptr));
   R.Abuf.assign(N, nullptr);
   R.Bbuf.assign(N, nullptr);
   for (int n = 0; n < N; ++n) {
     size_t acap = 1, bcap = 1;
-    // complex: left operands (L frames, A^n) interleaved (x Z), right operands (R frames, B^n)
-    // in 2x2-block expanded form (x ZE)
+    // complex: left operands (A^n) interleaved (x Z), right operands (R frames, B^n) in 2x2-block
+    // expanded form (x ZE). Abuf: A^n_b X^n_{b+1} (L->R look-ahead); Bbuf: X^n_b B^n_b (R->L
+    // look-ahead) and the canonicalisation's X_s R_{s+1}
     for (int b = 0; b < L - 1; ++b) {
-      R.Lf[n][b] = c.take<double>((size_t)R.rmax[b] * R.xr[n][b + 1] * R.Z);
-      acap = std::max(acap, (size_t)R.mmax[b] * R.xr[n][b + 1]);
+      if (b + 2 < L) acap = std::max(acap, (size_t)R.mmax[b] * R.d[b + 1] * R.xr[n][b + 2]);
+      if (b > 0) bcap = std::max(bcap, (size_t)R.xr[n][b] * R.d[b] * R.nmax[b]);
       bcap = std::max(bcap, (size_t)R.xr[n][b + 1] * R.nmax[b]);
     }
     for (int s = 1; s < L; ++s) R.Rf[n][s] = c.take<double>((size_t)R.xr[n][s] * R.rmax[s - 1] * R.ZE);
     R.Abuf[n] = c.take<double>(acap * R.Z);
     R.Bbuf[n] = c.take<double>(bcap * R.ZE);
   }
-  R.Apre.assign(N, std::vector<double *>(L, nullptr));
-  R.Bpre.assign(N, std::vector<double *>(L, nullptr));
+  R.Ast.assign(N, std::vector<double *>(L, nullptr));
+  R.Bst.assign(N, std::vector<double *>(L, nullptr));
   for (int n = 0; n < N; ++n) {
     for (int b = 1; b < L - 1; ++b)
-      R.Apre[n][b] = c.take<double>((size_t)R.rmax[b - 1] * R.d[b] * R.xr[n][b + 1] * R.Z);
+      R.Ast[n][b] = c.take<double>((size_t)R.rmax[b - 1] * R.d[b] * R.xr[n][b + 1] * R.Z);
     for (int b = 0; b + 2 < L; ++b)
-      R.Bpre[n][b] = c.take<double>((size_t)R.xr[n][b + 1] * R.d[b + 1] * R.rmax[b + 1] * R.ZE);
+      R.Bst[n][b] = c.take<double>((size_t)R.xr[n][b + 1] * R.d[b + 1] * R.rmax[b + 1] * R.ZE);
   }
   R.Xe.assign(N, std::vector<double *>(L, nullptr));
   for (int n = 0; n < N && R.cplx; ++n) {
@@ -1203,14 +1213,13 @@ static void launch_update(Run &R, int b, int dir, int logslot, const BondStatic 
   U.Jnext = b + 2 < R.L ? R.Jmi[b + 2] : nullptr;
   U.Jnew = R.Jmi[b + 1];
   for (int n = 0; n < R.N; ++n) {
-    const bool has_L = b > 0, has_R = b + 2 < R.L;
-    U.A[n] = has_L ? R.Abuf[n] : R.xcore0[n] + R.xoff[n][b];
-    U.Lnew[n] = R.Lf[n][b];
-    U.B[n] = has_R ? R.Bbuf[n] : (R.cplx ? R.Xe[n][b + 1] : R.xcore0[n] + R.xoff[n][b + 1]);
-    U.Rnew[n] = R.Rf[n][b + 1];
-    U.c1[n] = R.xr[n][b + 1];
+    U.Ahat[n] = R.Abuf[n];
+    U.Anext[n] = dir == 0 && b + 2 < R.L ? R.Ast[n][b + 1] : nullptr;
+    U.W[n] = b + 2 < R.L ? R.Z * R.d[b + 1] * R.xr[n][b + 2] : 0;
+    U.Bhat[n] = R.Bbuf[n];
+    U.Bprev[n] = dir == 1 && b > 0 ? R.Bst[n][b - 1] : nullptr;
+    U.c0[n] = R.xr[n][b];
   }
-  U.ldRnew = R.rmax[b];
   U.Z = R.Z;
   U.Pi = R.Pi;
   U.Y0 = R.Y0;
@@ -1265,13 +1274,12 @@ static void build_statics(Run &R, const FOp &op) {
         I.c0 = R.xr[n][b]; I.c1 = R.xr[n][b + 1]; I.c2 = R.xr[n][b + 2];
         I.Xb = R.xcore0[n] + R.xoff[n][b];
         I.Xb1 = R.xcore0[n] + R.xoff[n][b + 1];
-        I.Lprev = b > 0 ? R.Lf[n][b - 1] : nullptr;
         I.Rnext = b + 2 < L ? R.Rf[n][b + 2] : nullptr;
         I.ldR = b + 2 < L ? R.rmax[b + 1] : 1;
-        I.Abuf = R.Abuf[n];
-        I.Bbuf = R.Bbuf[n];
-        I.Apre = R.Apre[n][b];
-        I.Bpre = R.Bpre[n][b];
+        I.Ahat = R.Abuf[n];
+        I.Bhat = R.Bbuf[n];
+        I.Ast = R.Ast[n][b];
+        I.Bst = R.Bst[n][b];
         I.Xeb = R.Xe[n][b];
         I.Xeb1 = R.Xe[n][b + 1];
       }
@@ -1280,49 +1288,59 @@ static void build_statics(Run &R, const FOp &op) {
 
 static const BondStatic *dstat(const Run &R, int dir, int b) { return R.dStat + dir * (R.L - 1) + b; }
 
-// Pivot-independent halves of every bond of one half-sweep in one launch (R20: an L->R bond
-// reads the previous sweep's R frames, an R->L bond the previous sweep's L frames).
-static void pre_launch(Run &R, int dir, cudaStream_t st) {
+// B^n_b = X^n_{b+1} R^n_{b+2} of every bond from the canonical R frames, in one launch (once per
+// product; afterwards every B^n_b is written by the R->L update of bond b+1).
+static void pre_launch(Run &R, cudaStream_t st) {
   const int L = R.L, N = R.N;
   int pm = 0, pn = 0;
-  for (int b = 0; b < L - 1; ++b)
+  for (int b = 0; b + 2 < L; ++b)
     for (int n = 0; n < N; ++n) {
-      if (dir == 0 && b + 2 < L) { pm = std::max(pm, R.xr[n][b + 1] * R.d[b + 1]); pn = std::max(pn, R.rmax[b + 1]); }
-      if (dir == 1 && b > 0) { pm = std::max(pm, R.rmax[b - 1]); pn = std::max(pn, R.d[b] * R.xr[n][b + 1]); }
+      pm = std::max(pm, R.xr[n][b + 1] * R.d[b + 1]);
+      pn = std::max(pn, R.rmax[b + 1]);
     }
   if (pm == 0) return;
   R.P->begin(ACI_PROF_GEMM_AB);
-  plan_pre_kernel<<<1, 256, 0, st>>>(dstat(R, dir, 0), L - 1, N, R.rk, R.dPre);
+  plan_pre_kernel<<<1, 256, 0, st>>>(dstat(R, 0, 0), L - 1, N, R.rk, R.dPre);
   FOp dummy = {};
   if (R.cplx)
-    launch_gemm_z(R.dPre, (L - 1) * N, pm, 2 * pn, dir == 0 ? 1 : 0, 1, dummy, nullptr, nullptr, st);
+    launch_gemm_z(R.dPre, (L - 1) * N, pm, 2 * pn, 1, 1, dummy, nullptr, nullptr, st);
   else
     launch_gemm(R.dPre, (L - 1) * N, pm, pn, 1, false, dummy, nullptr, nullptr, st);
   R.P->end(2);
 }
 
-// One 2-site update (Alg. 1): [plan] -> dependent half of a1/a2 -> a3+a4 -> a5 ->
-// a6/a7 (+ the plan of the next bond, fused into the update kernel when `next` is given).
+// The look-ahead GEMM runs on a second stream (per host thread) forked off the prrLU's
+// launch-completion event, so it starts once every prrLU CTA is resident and fills the SMs the
+// prrLU leaves idle; the update of the bond joins it.
+struct SideStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t started = nullptr, done = nullptr;
+};
+static SideStream &side_stream() {
+  static thread_local SideStream s;
+  if (!s.st) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&s.st, cudaStreamNonBlocking, lo);
+    cudaEventCreateWithFlags(&s.started, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming);
+  }
+  return s;
+}
+
+// One 2-site update (Alg. 1): [plan] -> a3+a4 -> a5 (|| look-ahead GEMM) -> a6/a7 (+ the
+// plan of the next bond, fused into the update kernel when `next` is given).
 static void bond_update(Run &R, double tol, int tol_mode, int b, int dir, int logslot, bool plan_here,
                         const BondStatic *next, cudaStream_t st) {
   const int L = R.L, N = R.N, k = dir * (L - 1) + b;
-  int ab_m = 0, ab_n = 0;
+  int la_m = 0, la_n = 0;  // look-ahead GEMM bounds (complex: in complex columns)
   for (int n = 0; n < N; ++n) {
-    if (dir == 0 && b > 0) { ab_m = std::max(ab_m, R.rmax[b - 1]); ab_n = std::max(ab_n, R.d[b] * R.xr[n][b + 1]); }
-    if (dir == 1 && b + 2 < L) { ab_m = std::max(ab_m, R.xr[n][b + 1] * R.d[b + 1]); ab_n = std::max(ab_n, R.rmax[b + 1]); }
+    if (dir == 0 && b + 2 < L) { la_m = R.mmax[b]; la_n = std::max(la_n, R.d[b + 1] * R.xr[n][b + 2]); }
+    if (dir == 1 && b > 0) { la_m = std::max(la_m, R.xr[n][b] * R.d[b]); la_n = R.nmax[b]; }
   }
   if (plan_here) {
     R.P->begin(ACI_PROF_UPDATE);
     plan_bond_kernel<<<1, 1, 0, st>>>(dstat(R, dir, b), R.rk, R.dAB, R.dPi, R.dLu);
-    R.P->end(1);
-  }
-  if (ab_m > 0) {
-    R.P->begin(ACI_PROF_GEMM_AB);
-    FOp dummy = {};
-    if (R.cplx)
-      launch_gemm_z(R.dAB, N, ab_m, 2 * ab_n, dir == 0 ? 0 : 1, 1, dummy, nullptr, nullptr, st);
-    else
-      launch_gemm(R.dAB, N, ab_m, ab_n, 1, false, dummy, nullptr, nullptr, st);
     R.P->end(1);
   }
   R.P->begin(ACI_PROF_GEMM_PI);
@@ -1338,9 +1356,26 @@ static void bond_update(Run &R, double tol, int tol_mode, int b, int dir, int lo
   a.rows = R.prow[b]; a.cols = R.pcol[b]; a.r_out = R.rout + b; a.eps_out = R.epsb + b;
   a.U = dir == 1 ? R.Ust[b] : nullptr;
   a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter; a.epoch = R.epoch;
+  SideStream &sd = side_stream();
+  const bool look = la_m > 0 && la_n > 0;
   R.P->begin(ACI_PROF_PRRLU);
-  launch_prrlu(a, R.mmax[b], R.nmax[b], st, R.cplx != 0, R.one != 0);
+  launch_prrlu(a, R.mmax[b], R.nmax[b], st, R.cplx != 0, R.one != 0, look ? sd.started : nullptr);
   R.P->end(1);
+  if (look) {
+    cudaStreamWaitEvent(sd.st, sd.started, 0);
+    cudaStream_t mine = R.P->st;
+    R.P->st = sd.st;
+    R.P->begin(ACI_PROF_GEMM_AB);
+    FOp dummy = {};
+    if (R.cplx)
+      launch_gemm_z(R.dAB, N, la_m, 2 * la_n, dir == 0 ? 0 : 1, 1, dummy, nullptr, nullptr, sd.st);
+    else
+      launch_gemm(R.dAB, N, la_m, la_n, 1, false, dummy, nullptr, nullptr, sd.st);
+    R.P->end(1);
+    R.P->st = mine;
+    cudaEventRecord(sd.done, sd.st);
+    cudaStreamWaitEvent(st, sd.done, 0);
+  }
   R.P->begin(ACI_PROF_UPDATE);
   launch_update(R, b, dir, logslot, next, st);
   R.P->end(1);
@@ -1575,16 +1610,15 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   prof.begin(ACI_PROF_CANON);
   copy_prev_kernel<<<1, 64, 0, strm>>>(R.rk, R.prev, L);
   prof.end(1);
+  pre_launch(R, strm);  // B^n_b of the first L->R half-sweep
 
   // ---- main loop. One iteration (L->R and R->L half-sweeps + convergence test)
   // is a fixed sequence of launches whose live sizes are read on the device, so it is captured
   // once as a CUDA graph and replayed; only the convergence flag comes back to the host.
   auto one_iteration = [&]() {
     int step = 0;
-    pre_launch(R, 0, strm);
     for (int b = 0; b < L - 1; ++b)
       bond_update(R, tol, o.tol_mode, b, 0, step++, b == 0, b + 1 < L - 1 ? dstat(R, 0, b + 1) : dstat(R, 1, L - 2), strm);
-    pre_launch(R, 1, strm);
     for (int b = L - 2; b >= 0; --b)
       bond_update(R, tol, o.tol_mode, b, 1, step++, false, b > 0 ? dstat(R, 1, b - 1) : nullptr, strm);
     prof.begin(ACI_PROF_CONV);

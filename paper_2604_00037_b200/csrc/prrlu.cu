@@ -929,21 +929,35 @@ size_t prrlu_exchange_bytes(int max_m, int max_n) {
 
 void prrlu_init() { cluster_choice(); }
 
+// Every variant goes through cudaLaunchKernelEx so that a launch-completion event (fired once all
+// CTAs have begun executing) can be attached: the sweep forks its look-ahead GEMM off it, onto the
+// SMs the prrLU does not hold (aci.cu bond_update).
 template <bool CPLX>
-static void launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool one) {
+static void launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool one, cudaEvent_t started) {
+  LuArgs args = a;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kNWT * 32);
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  auto cluster = [&](int cs) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = cs;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  };
+  if (started) {
+    at[na].id = cudaLaunchAttributeLaunchCompletionEvent;
+    at[na].val.launchCompletionEvent.event = started;
+    at[na].val.launchCompletionEvent.flags = 0;
+    ++na;
+  }
+  cfg.attrs = at;
   if (one && !fits_one_cta(max_m, max_n, CPLX)) {
-    LuArgs args = a;
-    cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(16);
-    cfg.blockDim = dim3(kNWT * 32);
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 16;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cluster(16);
+    cfg.numAttrs = na;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute((const void *)prrlu_kernel_one<kNWT, CPLX>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -953,26 +967,18 @@ static void launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t s
     return;
   }
   if (fits_one_cta(max_m, max_n, CPLX)) {
-    void *params[] = {const_cast<LuArgs *>(&a)};
-    cudaLaunchKernel((const void *)prrlu_kernel<kNWT, 1, CPLX>, dim3(1), dim3(kNWT * 32), params, 0, st);
+    cfg.gridDim = dim3(1);
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 1, CPLX>, args);
     return;
   }
   int G = (max_n + kNWT - 1) / kNWT;  // enough for every variant the live size may select
   const int cs = cluster_choice();
-  LuArgs args = a;
   if (cs > 0) {
     G = (G + cs - 1) / cs * cs;
-    cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(G);
-    cfg.blockDim = dim3(kNWT * 32);
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cluster(cs);
+    cfg.numAttrs = na;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute((const void *)prrlu_kernel<kNWT, 2, CPLX>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -982,11 +988,15 @@ static void launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t s
     return;
   }
   cudaMemsetAsync(a.counter, 0, sizeof(unsigned), st);
-  void *params[] = {&args};
-  cudaLaunchCooperativeKernel((const void *)prrlu_kernel<kNWT, 1, CPLX>, dim3(G), dim3(kNWT * 32), params, 0, st);
+  cfg.gridDim = dim3(G);
+  at[na].id = cudaLaunchAttributeCooperative;
+  at[na].val.cooperative = 1;
+  ++na;
+  cfg.numAttrs = na;
+  cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 1, CPLX>, args);
 }
 
-void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx, bool one) {
-  if (cplx) launch_prrlu_t<true>(a, max_m, max_n, st, one);
-  else launch_prrlu_t<false>(a, max_m, max_n, st, one);
+void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx, bool one, cudaEvent_t started) {
+  if (cplx) launch_prrlu_t<true>(a, max_m, max_n, st, one, started);
+  else launch_prrlu_t<false>(a, max_m, max_n, st, one, started);
 }

@@ -680,27 +680,37 @@ struct TriArgs {
   double *out;  // output core (r x n), rows R updated in place
   int n, r0, nr;
 };
-__global__ void __launch_bounds__(64) tri_block_kernel(const TriArgs *args) {
-  extern __shared__ double tri_smem[];
-  double(*su)[65] = reinterpret_cast<double(*)[65]>(tri_smem);
-  double(*sx)[65] = reinterpret_cast<double(*)[65]>(tri_smem + 64 * 65);
+// Right-looking substitution with the block's x in registers: once x_k is final, every x_i
+// (i < k) takes its fma independently, so a thread has up to k FMAs in flight instead of one
+// dependent chain per row; U_J[R,R] is read from shared memory as warp-uniform broadcasts.
+constexpr int kTriNB = 64, kTriThreads = 128;
+__global__ void __launch_bounds__(kTriThreads) tri_block_kernel(const TriArgs *args) {
+  __shared__ double su[kTriNB][kTriNB];  // su[i][k] = U_J[r0 + i][r0 + k]
   const TriArgs A = args[blockIdx.y];
-  const int j = blockIdx.x * 64 + threadIdx.x;
-  if (blockIdx.x * 64 >= A.n) return;
-  for (int t = threadIdx.x; t < A.nr * A.nr; t += 64) {
-    const int k = t / A.nr, i = t % A.nr;
-    su[k][i] = A.UJ[(size_t)(A.r0 + k) * A.ldj + A.r0 + i];
+  const int j = blockIdx.x * kTriThreads + threadIdx.x;
+  if (blockIdx.x * kTriThreads >= A.n) return;
+  const int nr = A.nr;
+  for (int t = threadIdx.x; t < nr * nr; t += kTriThreads) {
+    const int i = t / nr, k = t % nr;
+    su[i][k] = A.UJ[(size_t)(A.r0 + i) * A.ldj + A.r0 + k];
   }
-  if (j < A.n)
-    for (int k = 0; k < A.nr; ++k) sx[k][threadIdx.x] = A.out[(size_t)(A.r0 + k) * A.n + j];
+  const bool live = j < A.n;
+  double x[kTriNB];
+#pragma unroll
+  for (int k = 0; k < kTriNB; ++k) x[k] = (live && k < nr) ? A.out[(size_t)(A.r0 + k) * A.n + j] : 0.0;
   __syncthreads();
-  if (j >= A.n) return;
-  for (int k = A.nr - 1; k >= 0; --k) {
-    double acc = sx[k][threadIdx.x];
-    for (int i = k + 1; i < A.nr; ++i) acc = fma(-su[k][i], sx[i][threadIdx.x], acc);
-    sx[k][threadIdx.x] = acc;
+#pragma unroll
+  for (int k = kTriNB - 1; k > 0; --k) {
+    if (k < nr) {
+      const double xk = x[k];
+#pragma unroll
+      for (int i = 0; i < k; ++i) x[i] = fma(-su[i][k], xk, x[i]);
+    }
   }
-  for (int k = 0; k < A.nr; ++k) A.out[(size_t)(A.r0 + k) * A.n + j] = sx[k][threadIdx.x];
+  if (live)
+#pragma unroll
+    for (int k = 0; k < kTriNB; ++k)
+      if (k < nr) A.out[(size_t)(A.r0 + k) * A.n + j] = x[k];
 }
 
 __global__ void copy_prev_kernel(const int *rk, int *prev, int L) {
@@ -1735,7 +1745,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
     // Blocked back substitution B = U_J^{-1} U (64-row blocks from the bottom): per step one
     // batched DMMA GEMM B[R] = U[R] - U_J[R, below] B[below] over all bonds, then the diagonal
     // block solve. The final ranks are known on the host here, so descriptors are built here.
-    constexpr int NB = 64;
+    constexpr int NB = kTriNB;
     std::vector<TrsmArgs> ta(L - 1);
     int nmx = 1, nsteps = 0;
     for (int b = 0; b < L - 1; ++b) {
@@ -1770,18 +1780,12 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
     cudaMemcpyAsync(R.dtrsm, ta.data(), sizeof(TrsmArgs) * (L - 1), cudaMemcpyHostToDevice, strm);
     cudaMemcpyAsync(R.dtgemm, gd.data(), sizeof(GemmDesc) * gd.size(), cudaMemcpyHostToDevice, strm);
     cudaMemcpyAsync(R.dtri, tr.data(), sizeof(TriArgs) * tr.size(), cudaMemcpyHostToDevice, strm);
-    constexpr int kTriSmem = 2 * 64 * 65 * sizeof(double);
-    static bool tri_attr = false;
-    if (!tri_attr) {
-      cudaFuncSetAttribute(tri_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTriSmem);
-      tri_attr = true;
-    }
     prof.begin(ACI_PROF_TRSM);
     gather_uj_kernel<<<dim3(64, L - 1), 256, 0, strm>>>(R.dtrsm, R.rk);
     size_t go = 0;
     for (int s = 0; s < nsteps; ++s) {
       launch_gemm_sub(R.dtgemm + go, gcount[s], NB, nmx, strm);
-      tri_block_kernel<<<dim3((nmx + 63) / 64, tcount[s]), 64, kTriSmem, strm>>>(R.dtri + go);
+      tri_block_kernel<<<dim3((nmx + kTriThreads - 1) / kTriThreads, tcount[s]), kTriThreads, 0, strm>>>(R.dtri + go);
       go += gcount[s];
     }
     prof.end(1 + 2 * nsteps);

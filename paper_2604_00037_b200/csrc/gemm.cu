@@ -12,11 +12,30 @@ namespace {
 using namespace gemmk;
 using CfgPi = Cfg<64, 64, 32, 16, 16, 3, 2>;
 using CfgAB = Cfg<64, 32, 32, 16, 16, 3, 4>;
+// Small problems: 32x32 tiles of 4 warps. A 64x64-tile grid of fewer than ~2 CTAs per SM leaves
+// SMs idle and runs the K loop serially on the busy ones; measured per launch (tools/gemm_latency.cu,
+// f fused, K = 64..256): 64^2 6.5 -> 3.7 us, 256^2 9.7 -> 5.0 us, 512^2 16.0 -> 9.4 us, but
+// 1024^2 25.4 -> 28.1 us, so the 64x64 tiles stay for grids of >= 256 of them.
+using CfgS = Cfg<32, 32, 16, 16, 16, 3, 4>;
+inline bool small_grid(int max_m, int max_n) { return ((max_m + 63) / 64) * ((max_n + 63) / 64) < 256; }
 
 template <int NB, int NS>
 void launch_pi(const GemmDesc *d, int ndesc, int max_m, int max_n, const FOp &op, unsigned long long *sb, int *nf,
                cudaStream_t st) {
-  launch<CfgPi, NB, NS, EPI_F>(d, ndesc, max_m, max_n, op, sb, nf, st);
+  if (small_grid(max_m, max_n)) launch<CfgS, NB, NS, EPI_F>(d, ndesc, max_m, max_n, op, sb, nf, st);
+  else launch<CfgPi, NB, NS, EPI_F>(d, ndesc, max_m, max_n, op, sb, nf, st);
+}
+template <int EPI>
+void launch_ab(const GemmDesc *d, int ndesc, int max_m, int max_n, const FOp &op, unsigned long long *sb, int *nf,
+               cudaStream_t st) {
+  if (small_grid(max_m, max_n)) launch<CfgS, 1, 0, EPI>(d, ndesc, max_m, max_n, op, sb, nf, st);
+  else launch<CfgAB, 1, 0, EPI>(d, ndesc, max_m, max_n, op, sb, nf, st);
+}
+template <int NB>
+void launch_fz(const GemmDesc *d, int ndesc, int max_m, int max_n, const FOp &op, unsigned long long *sb, int *nf,
+               cudaStream_t st) {
+  if (small_grid(max_m, max_n)) launch<CfgS, NB, 0, EPI_FZ>(d, ndesc, max_m, max_n, op, sb, nf, st);
+  else launch<CfgPi, NB, 0, EPI_FZ>(d, ndesc, max_m, max_n, op, sb, nf, st);
 }
 }  // namespace
 
@@ -38,6 +57,22 @@ static void gemm_init_once() {
   set_attr<CfgPi, 2, 0, EPI_FZ>();
   set_attr<CfgPi, 3, 0, EPI_FZ>();
   set_attr<CfgPi, 4, 0, EPI_FZ>();
+  set_attr<CfgS, 1, 0, EPI_STORE>();
+  set_attr<CfgS, 1, 0, EPI_STORE_X>();
+  set_attr<CfgS, 1, 0, EPI_F>();
+  set_attr<CfgS, 2, 0, EPI_F>();
+  set_attr<CfgS, 3, 0, EPI_F>();
+  set_attr<CfgS, 4, 0, EPI_F>();
+  set_attr<CfgS, 0, 1, EPI_F>();
+  set_attr<CfgS, 1, 1, EPI_F>();
+  set_attr<CfgS, 2, 1, EPI_F>();
+  set_attr<CfgS, 0, 2, EPI_F>();
+  set_attr<CfgS, 1, 2, EPI_F>();
+  set_attr<CfgS, 0, 3, EPI_F>();
+  set_attr<CfgS, 1, 0, EPI_FZ>();
+  set_attr<CfgS, 2, 0, EPI_FZ>();
+  set_attr<CfgS, 3, 0, EPI_FZ>();
+  set_attr<CfgS, 4, 0, EPI_FZ>();
 }
 
 void gemm_init() {
@@ -58,7 +93,7 @@ void launch_gemm_split(const GemmDesc *d, int ndesc, int max_m, int max_n, int n
                        const FOp &op, unsigned long long *sb, int *nf, cudaStream_t st) {
   if (max_m <= 0 || max_n <= 0 || ndesc <= 0) return;
   if (!fuse) {
-    launch<CfgAB, 1, 0, EPI_STORE>(d, ndesc, max_m, max_n, op, sb, nf, st);
+    launch_ab<EPI_STORE>(d, ndesc, max_m, max_n, op, sb, nf, st);
     return;
   }
   if (nbig + nsmall >= 4) {  // rare shape: every input through DMMA (descriptor order unchanged)
@@ -83,15 +118,15 @@ void launch_gemm_z(const GemmDesc *d, int ndesc, int max_m, int max_n, int mode,
                    unsigned long long *sb, int *nf, cudaStream_t st) {
   if (max_m <= 0 || max_n <= 0 || ndesc <= 0) return;
   if (mode == 0) {
-    launch<CfgAB, 1, 0, EPI_STORE>(d, ndesc, max_m, max_n, op, sb, nf, st);
+    launch_ab<EPI_STORE>(d, ndesc, max_m, max_n, op, sb, nf, st);
   } else if (mode == 1) {
-    launch<CfgAB, 1, 0, EPI_STORE_X>(d, ndesc, max_m, max_n, op, sb, nf, st);
+    launch_ab<EPI_STORE_X>(d, ndesc, max_m, max_n, op, sb, nf, st);
   } else {
     switch (nin) {
-      case 1: launch<CfgPi, 1, 0, EPI_FZ>(d, ndesc, max_m, max_n, op, sb, nf, st); break;
-      case 2: launch<CfgPi, 2, 0, EPI_FZ>(d, ndesc, max_m, max_n, op, sb, nf, st); break;
-      case 3: launch<CfgPi, 3, 0, EPI_FZ>(d, ndesc, max_m, max_n, op, sb, nf, st); break;
-      default: launch<CfgPi, 4, 0, EPI_FZ>(d, ndesc, max_m, max_n, op, sb, nf, st); break;
+      case 1: launch_fz<1>(d, ndesc, max_m, max_n, op, sb, nf, st); break;
+      case 2: launch_fz<2>(d, ndesc, max_m, max_n, op, sb, nf, st); break;
+      case 3: launch_fz<3>(d, ndesc, max_m, max_n, op, sb, nf, st); break;
+      default: launch_fz<4>(d, ndesc, max_m, max_n, op, sb, nf, st); break;
     }
   }
 }

@@ -848,6 +848,7 @@ struct Prof {
 
 struct Run {
   Prof *P = nullptr;
+  cudaError_t launch_err = cudaSuccess;  // first rejected prrLU launch (eager launches)
   int cplx = 0, Z = 1, ZE = 1;  // complex run: Z = 2 doubles per entry, ZE = 4 for expanded operands
   int one = 0;                  // aci_options.concurrent: single-cluster prrLU launches
   int L = 0, N = 0, maxrank = 0, max_sweeps = 0, log_cap_upd = 0, log_cap_piv = 0, colcap = 0;
@@ -1369,7 +1370,8 @@ static void bond_update(Run &R, double tol, int tol_mode, int b, int dir, int lo
   SideStream &sd = side_stream();
   const bool look = la_m > 0 && la_n > 0;
   R.P->begin(ACI_PROF_PRRLU);
-  launch_prrlu(a, R.mmax[b], R.nmax[b], st, R.cplx != 0, R.one != 0, look ? sd.started : nullptr);
+  const cudaError_t le = launch_prrlu(a, R.mmax[b], R.nmax[b], st, R.cplx != 0, R.one != 0, look ? sd.started : nullptr);
+  if (le != cudaSuccess && R.launch_err == cudaSuccess) R.launch_err = le;
   R.P->end(1);
   if (look) {
     cudaStreamWaitEvent(sd.st, sd.started, 0);
@@ -1424,7 +1426,8 @@ static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st)
   a.rows = R.prow[s - 1]; a.cols = R.pcol[s - 1]; a.r_out = R.rout + (s - 1); a.eps_out = R.epsb + (s - 1);
   a.U = nullptr;
   a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter; a.epoch = R.epoch;
-  launch_prrlu(a, max_m, max_n, st, R.cplx != 0, R.one != 0);
+  const cudaError_t le = launch_prrlu(a, max_m, max_n, st, R.cplx != 0, R.one != 0);
+  if (le != cudaSuccess && R.launch_err == cudaSuccess) R.launch_err = le;
   CanonUpd U = {};
   U.s = s; U.L = L; U.N = N; U.ds = R.d[s]; U.yr_s = R.yr[s]; U.yr_prev_rows = R.yr[s - 1] * R.d[s - 1];
   U.cols = R.pcol[s - 1]; U.r_in = R.rout + (s - 1);
@@ -1657,6 +1660,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
         if (graph) cudaGraphDestroy(graph);
       }
       cudaGetLastError();  // a failed capture falls back to direct launches
+      if (!gexec) R.launch_err = cudaSuccess;  // (their launch results are what counts)
       prof.per_iter_launches = prof.total - before;
       prof.total = before;
       if (gexec) gcached = graph_cache_insert(key, gexec, prof.per_iter_launches);
@@ -1707,6 +1711,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   cudaMemcpyAsync(&err, R.err, sizeof(double), cudaMemcpyDeviceToHost, strm);
   cudaMemcpyAsync(&scale_bits, R.scale, sizeof(double), cudaMemcpyDeviceToHost, strm);
   cudaError_t e = cudaStreamSynchronize(strm);
+  if (e == cudaSuccess) e = R.launch_err;  // a rejected launch leaves the results unwritten
   if (e != cudaSuccess) { cleanup(); return fail(ACI_ERR_CUDA, std::string("aci: ") + cudaGetErrorString(e)); }
   std::memcpy(&scale, &scale_bits, sizeof(double));
   if (nonfinite) { cleanup(); return fail(ACI_ERR_NONFINITE, "aci: f produced NaN/Inf (S:255)"); }
@@ -1801,8 +1806,11 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   const int nupd = slot;
   std::vector<int> info((size_t)nupd * 5);
   std::vector<double> es((size_t)nupd * 2);
-  cudaMemcpy(info.data(), R.log_info, sizeof(int) * info.size(), cudaMemcpyDeviceToHost);
-  cudaMemcpy(es.data(), R.log_es, sizeof(double) * es.size(), cudaMemcpyDeviceToHost);
+  // stream-ordered copies (a synchronous cudaMemcpy would synchronise with the legacy stream,
+  // which other host threads' stream captures forbid)
+  cudaMemcpyAsync(info.data(), R.log_info, sizeof(int) * info.size(), cudaMemcpyDeviceToHost, strm);
+  cudaMemcpyAsync(es.data(), R.log_es, sizeof(double) * es.size(), cudaMemcpyDeviceToHost, strm);
+  cudaStreamSynchronize(strm);
   aci_report rp = {};
   rp.error_estimate = err;
   rp.scale = scale;
@@ -1833,31 +1841,36 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
       if (lg->info) std::memcpy(lg->info + u * 5, &info[u * 5], sizeof(int) * 5);
       if (lg->eps_scale) std::memcpy(lg->eps_scale + u * 2, &es[u * 2], sizeof(double) * 2);
       const int r = std::min(info[u * 5 + 4], lg->capacity_pivots);
-      if (lg->rows) cudaMemcpy(lg->rows + (size_t)u * lg->capacity_pivots, R.log_rows + (size_t)u * R.log_cap_piv,
-                               sizeof(int) * r, cudaMemcpyDeviceToHost);
-      if (lg->cols) cudaMemcpy(lg->cols + (size_t)u * lg->capacity_pivots, R.log_cols + (size_t)u * R.log_cap_piv,
-                               sizeof(int) * r, cudaMemcpyDeviceToHost);
+      if (lg->rows)
+        cudaMemcpyAsync(lg->rows + (size_t)u * lg->capacity_pivots, R.log_rows + (size_t)u * R.log_cap_piv,
+                        sizeof(int) * r, cudaMemcpyDeviceToHost, strm);
+      if (lg->cols)
+        cudaMemcpyAsync(lg->cols + (size_t)u * lg->capacity_pivots, R.log_cols + (size_t)u * R.log_cap_piv,
+                        sizeof(int) * r, cudaMemcpyDeviceToHost, strm);
     }
     lg->n_written = nw;
     if (lg->canon_n) {
       std::vector<int> cn(L + 1, 0);
-      cudaMemcpy(cn.data(), R.canon_n, sizeof(int) * (L + 1), cudaMemcpyDeviceToHost);
+      cudaMemcpyAsync(cn.data(), R.canon_n, sizeof(int) * (L + 1), cudaMemcpyDeviceToHost, strm);
+      cudaStreamSynchronize(strm);
       for (int s = 1; s < L; ++s) {
         lg->canon_n[s] = cn[s];
         if (lg->canon_cols)
-          cudaMemcpy(lg->canon_cols + (size_t)s * lg->capacity_pivots, R.canon_cols + (size_t)s * R.log_cap_piv,
-                     sizeof(int) * std::min(cn[s], lg->capacity_pivots), cudaMemcpyDeviceToHost);
+          cudaMemcpyAsync(lg->canon_cols + (size_t)s * lg->capacity_pivots, R.canon_cols + (size_t)s * R.log_cap_piv,
+                          sizeof(int) * std::min(cn[s], lg->capacity_pivots), cudaMemcpyDeviceToHost, strm);
       }
     }
   }
   if (o.I_sets)
     for (int b = 0; b < L - 1; ++b)
-      if (o.I_sets[b]) cudaMemcpy(o.I_sets[b], R.Imi[b], (size_t)rk[b + 1] * (b + 1), cudaMemcpyDeviceToHost);
+      if (o.I_sets[b])
+        cudaMemcpyAsync(o.I_sets[b], R.Imi[b], (size_t)rk[b + 1] * (b + 1), cudaMemcpyDeviceToHost, strm);
   if (o.J_sets)
     for (int s = 1; s < L; ++s)
-      if (o.J_sets[s]) cudaMemcpy(o.J_sets[s], R.Jmi[s], (size_t)rk[s] * (L - s), cudaMemcpyDeviceToHost);
-  cleanup();
+      if (o.J_sets[s])
+        cudaMemcpyAsync(o.J_sets[s], R.Jmi[s], (size_t)rk[s] * (L - s), cudaMemcpyDeviceToHost, strm);
   e = cudaStreamSynchronize(strm);
+  cleanup();
   if (e != cudaSuccess) { tt_destroy(res); return fail(ACI_ERR_CUDA, std::string("aci: ") + cudaGetErrorString(e)); }
   auto t_end = std::chrono::steady_clock::now();
   rp.ms = std::chrono::duration<float, std::milli>(t_end - t_start).count();

@@ -84,8 +84,9 @@ size_t prrlu_exchange_bytes(int max_m, int max_n);
 // cplx: complex entries (interleaved; ldm/ldu in complex elements; colcap >= 2 m).
 // one: single-cluster mode (aci_options.concurrent): at most one 16-CTA cluster per launch.
 // `started` (optional, created with cudaEventDisableTiming) fires once every CTA has begun.
-void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx = false, bool one = false,
-                  cudaEvent_t started = nullptr);
+// Returns the launch's own error (a rejected configuration leaves the outputs unwritten).
+cudaError_t launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx = false, bool one = false,
+                         cudaEvent_t started = nullptr);
 bool prrlu_supported_one(int m, int n, bool cplx);
 // Chooses the prrLU exchange tier (cluster size) once; call before any stream capture.
 void prrlu_init();

@@ -148,6 +148,21 @@ __device__ __forceinline__ void st_async_key(unsigned raddr, unsigned a, unsigne
                : "memory");
 }
 
+// DSMEM bulk copy (async proxy) from this CTA's shared memory into a cluster peer's, completing
+// `bytes` of transaction on the peer's mbarrier; 16-byte aligned, size a multiple of 16
+__device__ __forceinline__ void bulk_push(unsigned rdst, unsigned src, unsigned bytes, unsigned rbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(rdst),
+               "r"(src), "r"(bytes), "r"(rbar)
+               : "memory");
+}
+
+// push tier (XM = 3): one 8-CTA cluster; every CTA's candidate column is pushed into every
+// cluster CTA's shared memory (dynamic: [2 parities][8 ranks][kPushRows] + 2 staging columns)
+constexpr int kPushCS = 8;
+constexpr int kPushRows = 128;
+constexpr size_t kPushSmem = sizeof(double) * (2 * kPushCS * kPushRows + 2 * kPushRows);
+extern __shared__ __align__(16) double push_dyn[];
+
 struct Key {
   unsigned hi, lo, id;  // |v| bits (hi, lo); id = flat index (row * n + col)
 };
@@ -294,6 +309,18 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     return Key{(unsigned)(bits >> 32), (unsigned)bits, flat};
   };
   scan();
+  if constexpr (XM == 3) {
+    // keys (16 B) and candidate columns (MROWS doubles) of every cluster CTA land on one
+    // mbarrier per parity, armed for steps 0 and 1 before any CTA pushes
+    if (tid == 0) {
+      const unsigned CS = cluster_size();
+      for (int t = 0; t < 2; ++t) mbar_init(smem_u32(&S.mb[t]), 1u);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_arm(smem_u32(&S.mb[0]), CS * (16u + 8u * MROWS));
+      mbar_arm(smem_u32(&S.mb[1]), CS * (16u + 8u * MROWS));
+    }
+    cluster_sync_all();
+  }
   if (XM == 2) {
     // one mbarrier per parity, armed for steps 0 and 1 before any CTA of the cluster pushes
     if (tid == 0) {
@@ -324,7 +351,41 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     const Key ck = warp_argmax(lane < NW ? Key{s_hi[lane], s_lo[lane], s_id[lane]} : Key{0u, 0u, BAD_ID});
     Key win = ck;
     PHASE(1);
-    if (GRID) {
+    if constexpr (XM == 3) {
+      // ---- push tier: key + candidate column into every cluster CTA (DSMEM), one wait
+      const int par = k & 1;
+      const unsigned CS = cluster_size(), crank = cluster_rank();
+      const int jc = (int)(ck.id % NC) - c0;
+      const int pw = jc % NW;
+      if (w == 0 && lane < (int)CS)
+        st_async_key(mapa_u32(smem_u32(&S.ck[par][crank]), (unsigned)lane), ck.hi, ck.lo, ck.id,
+                     mapa_u32(smem_u32(&S.mb[par]), (unsigned)lane));
+      if (w == pw) {
+        double *stg = push_dyn + 2 * kPushCS * kPushRows + par * kPushRows;
+        const int bc = jc / NW;
+#pragma unroll
+        for (int b = 0; b < EB; ++b)
+          if (b == bc)
+#pragma unroll
+            for (int a = 0; a < EA; ++a) stg[lane + 32 * a] = v[a][b][0];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane < (int)CS) {
+          double *dst = push_dyn + ((size_t)par * kPushCS + crank) * kPushRows;
+          bulk_push(mapa_u32(smem_u32(dst), (unsigned)lane), smem_u32(stg), 8u * MROWS,
+                    mapa_u32(smem_u32(&S.mb[par]), (unsigned)lane));
+          asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+      }
+      PHASE(2);
+      const unsigned mbp = smem_u32(&S.mb[par]);
+      mbar_wait(mbp, (unsigned)(k >> 1) & 1u);
+      PHASE(3);
+      if (tid == 0) mbar_arm(mbp, CS * (16u + 8u * MROWS));  // for step k + 2
+      const uint4 q4 = S.ck[par][lane < (int)CS ? lane : 0];
+      win = warp_argmax(lane < (int)CS ? Key{q4.x, q4.y, q4.z} : Key{0u, 0u, BAD_ID});
+      PHASE(4);
+    } else if (GRID) {
       const int par = k & 1;
       const unsigned tag = (ep << 12) | (unsigned)(k + 1);
       // the owner warp of the CTA candidate's column publishes the column (tagged packets, no
@@ -522,7 +583,28 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     asm volatile("" : "+d"(inv_abs));
     double inv;       // signed 1/S_pq
     double ub[EB];    // pivot row (CTA tier: sign-folded, -u_j (c > 0) or +u_j (c < 0))
-    if (GRID) {
+    if constexpr (XM == 3) {
+      // the winner's column is already in this CTA's shared memory (pushed with its key)
+      const double *col = push_dyn + ((size_t)(k & 1) * kPushCS + q / CB) * kPushRows;
+      const bool neg = col[p] < 0.0;
+      inv = neg ? -inv_abs : inv_abs;
+      __syncthreads();  // S3: pivot row in smem
+      PHASE(5);
+      if (A.U)
+        for (int jj = tid; jj < CB; jj += T) {
+          const int j = c0 + jj;
+          if (j < n) A.U[(size_t)k * ldu + j] = (j == q) ? 1.0 : s_u[jj] * inv;
+        }
+#pragma unroll
+      for (int b = 0; b < EB; ++b) ub[b] = s_u[w + NW * b];
+#pragma unroll
+      for (int a = 0; a < EA; ++a) {
+        const int i = lane + 32 * a;
+        const double li = i < m ? ((i == p) ? 1.0 : col[i] * inv) : 0.0;
+#pragma unroll
+        for (int b = 0; b < EB; ++b) v[a][b][0] = fma(-li, ub[b], v[a][b][0]);
+      }
+    } else if (GRID) {
       const unsigned tag = (ep << 12) | (unsigned)(k + 1);
       const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2;
       constexpr int PPT = (MROWS + T - 1) / T;  // column packets per thread
@@ -725,7 +807,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     for (int t = 0; t < 8; ++t) A.dbg[t] = ph_[t];
 #endif
   }
-  if (XM == 2) cluster_sync_all();  // no CTA leaves while a cluster peer may still push to it
+  if (XM >= 2) cluster_sync_all();  // no CTA leaves while a cluster peer may still push to it
 }
 
 // Runtime tier selection from the LIVE sizes (device-resident ranks): the launch is sized for
@@ -833,7 +915,45 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel_one(LuArgs A) {
 #undef ACI_ONE_VARIANT
 }
 
+// Push tier (real blocks up to 128 x 256, one 8-CTA cluster): every CTA pushes its candidate
+// column into every cluster CTA's shared memory together with its key (cp.async.bulk DSMEM copy,
+// complete_tx on the receiver's mbarrier), so the winner's column is local once the keys are in —
+// no L2 round trip per pivot. Columns per CTA = 8 warps x EB. Measured per pivot
+// (tools/prrlu_bench): 128 x 128 1.21 us against 1.49 us in one CTA; at 256 rows the 8 x 2 KB
+// DSMEM pushes per CTA take ~1000 cycles and it loses to the 16-CTA L2 tier (1.88 vs 1.39 us).
+template <int NWT>
+__global__ void __launch_bounds__(NWT * 32) prrlu_kernel_push(LuArgs A) {
+  __shared__ PrrluSmem S;
+  const int m = A.dims->m, n = A.dims->n;
+  const int g = blockIdx.x;
+#define ACI_CTA_VARIANT(EA, EB)                                        \
+  if (m <= 32 * (EA) && n <= NWT * (EB)) {                              \
+    if (g == 0) prrlu_body<(EA), (EB), NWT, 0, false>(A, S, 1, 0);     \
+    return;                                                            \
+  }
+#define ACI_PUSH_VARIANT(EA, EB)                                       \
+  if (m <= 32 * (EA) && n <= kPushCS * NWT * (EB)) {                    \
+    prrlu_body<(EA), (EB), NWT, 3, false>(A, S, kPushCS, g);           \
+    return;                                                            \
+  }
+  ACI_CTA_VARIANT(1, 4)    //  32 x  32
+  ACI_CTA_VARIANT(2, 8)    //  64 x  64
+  ACI_PUSH_VARIANT(4, 2)   // 128 x 128
+  ACI_PUSH_VARIANT(2, 4)   //  64 x 256
+  ACI_PUSH_VARIANT(4, 4)   // 128 x 256
+#undef ACI_CTA_VARIANT
+#undef ACI_PUSH_VARIANT
+}
+
 constexpr int kNWT = 8;
+
+static bool push_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("ACI_PRRLU_PUSH");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
 
 bool fits_one_cta(int m, int n, bool cplx) {
   const int v8[][2] = {{1, 4}, {2, 8}, {4, 4}, {1, 16}, {4, 16}, {8, 8}, {2, 32}, {32, 2}};
@@ -927,13 +1047,25 @@ size_t prrlu_exchange_bytes(int max_m, int max_n) {
   return (size_t)2 * kMaxCTAs * cap * 16 + 2 * kMaxCTAs * 32 + 256;
 }
 
-void prrlu_init() { cluster_choice(); }
+// static + dynamic shared memory of the push tier exceeds the 48 KB default (set once, before any
+// stream capture)
+static int push_attr_once() {
+  cudaFuncSetAttribute((const void *)prrlu_kernel_push<kNWT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kPushSmem);
+  return 0;
+}
+
+void prrlu_init() {
+  cluster_choice();
+  static const int once = push_attr_once();
+  (void)once;
+}
 
 // Every variant goes through cudaLaunchKernelEx so that a launch-completion event (fired once all
 // CTAs have begun executing) can be attached: the sweep forks its look-ahead GEMM off it, onto the
 // SMs the prrLU does not hold (aci.cu bond_update).
 template <bool CPLX>
-static void launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool one, cudaEvent_t started) {
+static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool one, cudaEvent_t started) {
   LuArgs args = a;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kNWT * 32);
@@ -954,6 +1086,14 @@ static void launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t s
     ++na;
   }
   cfg.attrs = at;
+  if (!CPLX && !fits_one_cta(max_m, max_n, CPLX) && max_m <= kPushRows && max_n <= kPushCS * kNWT * 4 &&
+      push_enabled()) {
+    cfg.gridDim = dim3(kPushCS);
+    cfg.dynamicSmemBytes = kPushSmem;
+    cluster(kPushCS);
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, prrlu_kernel_push<kNWT>, args);
+  }
   if (one && !fits_one_cta(max_m, max_n, CPLX)) {
     cfg.gridDim = dim3(16);
     cluster(16);
@@ -963,14 +1103,12 @@ static void launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t s
       cudaFuncSetAttribute((const void *)prrlu_kernel_one<kNWT, CPLX>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       attr = true;
     }
-    cudaLaunchKernelEx(&cfg, prrlu_kernel_one<kNWT, CPLX>, args);
-    return;
+    return cudaLaunchKernelEx(&cfg, prrlu_kernel_one<kNWT, CPLX>, args);
   }
   if (fits_one_cta(max_m, max_n, CPLX)) {
     cfg.gridDim = dim3(1);
     cfg.numAttrs = na;
-    cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 1, CPLX>, args);
-    return;
+    return cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 1, CPLX>, args);
   }
   int G = (max_n + kNWT - 1) / kNWT;  // enough for every variant the live size may select
   const int cs = cluster_choice();
@@ -984,8 +1122,7 @@ static void launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t s
       cudaFuncSetAttribute((const void *)prrlu_kernel<kNWT, 2, CPLX>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       attr = true;
     }
-    cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 2, CPLX>, args);
-    return;
+    return cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 2, CPLX>, args);
   }
   cudaMemsetAsync(a.counter, 0, sizeof(unsigned), st);
   cfg.gridDim = dim3(G);
@@ -993,10 +1130,11 @@ static void launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t s
   at[na].val.cooperative = 1;
   ++na;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 1, CPLX>, args);
+  return cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 1, CPLX>, args);
 }
 
-void launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx, bool one, cudaEvent_t started) {
-  if (cplx) launch_prrlu_t<true>(a, max_m, max_n, st, one, started);
-  else launch_prrlu_t<false>(a, max_m, max_n, st, one, started);
+cudaError_t launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx, bool one,
+                         cudaEvent_t started) {
+  return cplx ? launch_prrlu_t<true>(a, max_m, max_n, st, one, started)
+              : launch_prrlu_t<false>(a, max_m, max_n, st, one, started);
 }

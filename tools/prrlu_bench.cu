@@ -11,7 +11,9 @@
 int main(int argc, char **argv) {
   // {m, n, kmax, static size}: static 1024 exercises the 8-warp instantiation on small live blocks
   int sizes[][4] = {{64, 64, 64, 0}, {128, 128, 128, 0}, {256, 256, 256, 0}, {512, 512, 512, 0}, {1024, 1024, 512, 0},
-                    {64, 64, 64, 1024}, {128, 128, 128, 1024}, {256, 256, 256, 1024}, {512, 512, 512, 1024}};
+                    {64, 64, 64, 1024}, {128, 128, 128, 1024}, {256, 256, 256, 1024}, {512, 512, 512, 1024},
+                    {64, 64, 64, 256}, {128, 128, 128, 256}, {256, 128, 128, 256}, {128, 256, 128, 256},
+                    {200, 250, 200, 256}};
   double *dM, *dU, *deps;
   unsigned long long *dcol;
   int *drows, *dcols, *dr;
@@ -45,6 +47,7 @@ int main(int argc, char **argv) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   int only = argc > 1 ? atoi(argv[1]) : -1;
+  prrlu_init();
   {
     const void *kern = (const void *)prrlu_kernel<kNWT, 2, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

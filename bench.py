@@ -45,11 +45,18 @@ def _peaks():
 
 
 class ClockSampler:
+    """nvidia-smi clocks sampled every 100 ms on a reader thread; start() returns once the first
+    sample has arrived, so even a short timed region is covered."""
+
     def __init__(self, gpu_index=0):
         self.proc = None
         self.gpu = gpu_index
+        self.lines = []
+        self.thread = None
 
     def start(self):
+        import threading
+        import time
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu),
@@ -59,12 +66,31 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return
+
+        def read():
+            for line in self.proc.stdout:
+                self.lines.append((time.monotonic(), line))
+
+        self.thread = threading.Thread(target=read, daemon=True)
+        self.thread.start()
+        t0 = time.monotonic()
+        while not self.lines and time.monotonic() - t0 < 5.0 and self.proc.poll() is None:
+            time.sleep(0.01)
+        self.t_begin = time.monotonic()
 
     def stop(self):
+        import time
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t_end = time.monotonic()
+        time.sleep(0.12)  # the sample covering the end of the timed region
         self.proc.terminate()
-        out = self.proc.communicate()[0].strip().splitlines()
+        if self.thread is not None:
+            self.thread.join(timeout=2.0)
+        # samples taken during the timed region (the one just before it stands in if it was shorter)
+        inside = [ln for t, ln in self.lines if self.t_begin - 0.1 <= t <= t_end + 0.11]
+        out = inside or [ln for _, ln in self.lines[-1:]]
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out:

@@ -67,7 +67,11 @@ int tt_create_device_z(int L, const int *d, const int *ranks, const double *dev_
 /* 1 if tt holds complex cores, else 0 (NULL: 0). */
 int tt_is_complex(const tt_t *tt);
 
-/* Free a TT (device memory included). NULL is a no-op. Returns ACI_OK. */
+/* Free a TT (device memory included; it returns to the library's stream-ordered pool). NULL is a
+ * no-op. Returns ACI_OK. Every library call that reads or writes a TT has finished with it when it
+ * returns; work the caller enqueued itself on tt_device_cores() must be complete before this call
+ * (there is no device-wide synchronisation here: it would break stream captures in other host
+ * threads). */
 int tt_destroy(tt_t *tt);
 
 /* Shape query: *L, and if non-NULL d[L], ranks[L+1]. */
@@ -77,7 +81,8 @@ int tt_shape(const tt_t *tt, int *L, int *d, int *ranks);
  * that, interleaved (re, im), for a complex TT). */
 int tt_get_cores(const tt_t *tt, double *const *host_cores);
 
-/* Device pointer to the contiguous core storage (core s at offset sum_{t<s} r_t d_t r_{t+1}). */
+/* Device pointer to the contiguous core storage (core s at offset sum_{t<s} r_t d_t r_{t+1}).
+ * Valid until tt_destroy; the caller synchronises its own work on it before destroying. */
 const double *tt_device_cores(const tt_t *tt);
 
 /* Evaluate x at npts full multi-indices (O(L chi^2) per point).

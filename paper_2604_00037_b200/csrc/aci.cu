@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -83,15 +84,17 @@ static cudaError_t core_alloc(tt_s *t, size_t bytes, cudaStream_t st) {
   return cudaMallocFromPoolAsync((void **)&t->dcores, bytes, pool, st);
 }
 
-// cudaFree's contract (outstanding work that may read the cores finishes first), then the
-// memory goes back to the pool.
+// Back to the pool, stream-ordered on the library stream. Every library call that touches a TT
+// has completed its work on it before returning, so nothing of ours can still read the cores;
+// work the caller enqueued on tt_device_cores() must be complete (aci.h). No device-wide
+// synchronisation: from a host thread it breaks stream captures running in other threads
+// (measured: driver crashes in concurrent-mode stress, tools/conc_stress.py).
 static void core_free(tt_s *t) {
   if (!t->dcores) return;
   int cur = 0;
   cudaGetDevice(&cur);
   if (cur != t->dev) cudaSetDevice(t->dev);
   if (t->pooled) {
-    cudaDeviceSynchronize();
     cudaFreeAsync(t->dcores, lib_stream());
     cudaStreamSynchronize(lib_stream());
   } else {
@@ -1323,20 +1326,25 @@ static void pre_launch(Run &R, cudaStream_t st) {
 // The look-ahead GEMM runs on a second stream (per host thread) forked off the prrLU's
 // launch-completion event, so it starts once every prrLU CTA is resident and fills the SMs the
 // prrLU leaves idle; the update of the bond joins it.
+// Created by side_stream_init() at the start of every call, before any stream capture (creating
+// streams or events inside a capture is refused, which left null events behind).
 struct SideStream {
   cudaStream_t st = nullptr;
   cudaEvent_t started = nullptr, done = nullptr;
 };
 static SideStream &side_stream() {
   static thread_local SideStream s;
-  if (!s.st) {
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStreamCreateWithPriority(&s.st, cudaStreamNonBlocking, lo);
-    cudaEventCreateWithFlags(&s.started, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming);
-  }
   return s;
+}
+static bool side_stream_init() {
+  SideStream &s = side_stream();
+  if (s.st && s.started && s.done) return true;
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if (!s.st && cudaStreamCreateWithPriority(&s.st, cudaStreamNonBlocking, lo) != cudaSuccess) s.st = nullptr;
+  if (!s.started && cudaEventCreateWithFlags(&s.started, cudaEventDisableTiming) != cudaSuccess) s.started = nullptr;
+  if (!s.done && cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming) != cudaSuccess) s.done = nullptr;
+  return s.st && s.started && s.done;
 }
 
 // One 2-site update (Alg. 1): [plan] -> a3+a4 -> a5 (|| look-ahead GEMM) -> a6/a7 (+ the
@@ -1530,6 +1538,10 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   cudaStream_t strm = o.stream ? (cudaStream_t)o.stream : lib_stream();
   gemm_init();
   prrlu_init();
+  if (!side_stream_init()) {
+    cudaGetLastError();
+    return fail(ACI_ERR_CUDA, "aci: could not create the look-ahead stream");
+  }
 
   // ---- y_init (R9)
   tt_s *ygen = nullptr;
@@ -1643,7 +1655,11 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   bool gcached = false;
   int graph_iters = 0;
   auto tg0 = std::chrono::steady_clock::now();
-  if (!prof.on && strm != nullptr) {
+  static const bool graphs = [] {  // ACI_NO_GRAPH=1: direct launches (debugging)
+    const char *e = getenv("ACI_NO_GRAPH");
+    return !e || atoi(e) == 0;
+  }();
+  if (!prof.on && strm != nullptr && graphs) {
     // the captured iteration depends only on host values (shapes, pointers, op, tol), so a call
     // that repeats them (same workspace address and inputs) replays the instantiated graph
     const std::vector<uint64_t> key = graph_key(R, I.op, tol, o.tol_mode, ws, need, strm);

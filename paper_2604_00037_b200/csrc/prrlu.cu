@@ -1047,17 +1047,21 @@ size_t prrlu_exchange_bytes(int max_m, int max_n) {
   return (size_t)2 * kMaxCTAs * cap * 16 + 2 * kMaxCTAs * 32 + 256;
 }
 
-// static + dynamic shared memory of the push tier exceeds the 48 KB default (set once, before any
-// stream capture)
-static int push_attr_once() {
+// Kernel attributes, set once before any stream capture: the push tier's static + dynamic shared
+// memory exceeds the 48 KB default; 16-CTA clusters need the non-portable size.
+static int attr_once() {
   cudaFuncSetAttribute((const void *)prrlu_kernel_push<kNWT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kPushSmem);
+  // 16-CTA clusters are a non-portable size
+  const void *k16[] = {(const void *)prrlu_kernel<kNWT, 2, false>, (const void *)prrlu_kernel<kNWT, 2, true>,
+                       (const void *)prrlu_kernel_one<kNWT, false>, (const void *)prrlu_kernel_one<kNWT, true>};
+  for (const void *f : k16) cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return 0;
 }
 
 void prrlu_init() {
   cluster_choice();
-  static const int once = push_attr_once();
+  static const int once = attr_once();
   (void)once;
 }
 
@@ -1098,11 +1102,6 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
     cfg.gridDim = dim3(16);
     cluster(16);
     cfg.numAttrs = na;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute((const void *)prrlu_kernel_one<kNWT, CPLX>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      attr = true;
-    }
     return cudaLaunchKernelEx(&cfg, prrlu_kernel_one<kNWT, CPLX>, args);
   }
   if (fits_one_cta(max_m, max_n, CPLX)) {
@@ -1117,11 +1116,6 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
     cfg.gridDim = dim3(G);
     cluster(cs);
     cfg.numAttrs = na;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute((const void *)prrlu_kernel<kNWT, 2, CPLX>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      attr = true;
-    }
     return cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 2, CPLX>, args);
   }
   cudaMemsetAsync(a.counter, 0, sizeof(unsigned), st);

@@ -203,6 +203,35 @@ def test_errors(aci):
     with pytest.raises(aci.AciError) as e:  # f overflows to inf
         aci.aci_elementwise({"coef": [1e308], "expo": [[4]]}, [big], 1e-8, 8, 2)
     assert "NONFINITE" in str(e.value)
+    # L = 1 has no bond to update (oracle: ORC_ERR_INVALID as well)
+    one = aci.TensorTrain.from_cores(G.random_tt(1, 4, 1, rng))
+    with pytest.raises(aci.AciError) as e:
+        aci.aci_elementwise({"coef": [1.0], "expo": [[2]]}, [one], 1e-8, 8, 2)
+    assert "INVALID" in str(e.value)
+
+
+def test_prrlu_envelope(aci):
+    """Blocks beyond the register-resident prrLU envelope are refused up front (ACI_ERR_UNSUPPORTED,
+    nothing launched): real 2-site blocks up to aci_limits() = 1024 rows x 1184 columns, complex
+    up to 512 rows; a product at the limit runs."""
+    rows, cols = aci.limits()
+    assert (rows, cols) == (1024, 1184)
+    rng = np.random.default_rng(12)
+    # maxrank 1024 at d = 2: the middle blocks have 2048 rows
+    x = aci.TensorTrain.from_cores(G.random_tt(24, 2, 600, rng))
+    with pytest.raises(aci.AciError) as e:
+        aci.aci_elementwise({"coef": [1.0], "expo": [[2]]}, [x], 1e-8, 1024, 1)
+    assert "UNSUPPORTED" in str(e.value)
+    # complex, maxrank 512 -> 1024-row blocks
+    tz = G.random_tt(20, 2, 300, rng)
+    z = aci.TensorTrain.from_cores([c + 0.5j * c for c in tz.cores])
+    with pytest.raises(aci.AciError) as e:
+        aci.aci_elementwise({"coef": [1.0], "expo": [[2]]}, [z], 1e-8, 512, 1)
+    assert "UNSUPPORTED" in str(e.value)
+    # complex at the limit (maxrank 256 -> 512-row blocks) runs
+    zs = aci.TensorTrain.from_cores([c[:min(c.shape[0], 8), :, :min(c.shape[2], 8)] + 0.5j for c in tz.cores])
+    out, st, rep, _ = aci.aci_elementwise({"coef": [1.0], "expo": [[2]]}, [zs], 1e-8, 256, 1)
+    assert rep["max_rank"] <= 256
 
 
 def _closed_psi(meta, s):

@@ -422,6 +422,7 @@ struct UpdateArgs {
   const BondStatic *next;
   GemmDesc *ab, *pi;
   LuDims *lu;
+  int *info;                  // 8 ints: this bond's (rl, rr, r, -, s bits) for index_bond_kernel
 };
 
 // Index-set update (a6, R21) and frame update (a7: the rows/columns of A^n / B^n the
@@ -445,29 +446,13 @@ __global__ void update_bond_kernel(UpdateArgs U) {
   if (gt == 0) {
     U.rk[b + 1] = r;  // no thread of this kernel reads rk[b+1]
     if (U.next) plan_bond(s_next, U.rk, U.ab, U.pi, U.lu);  // reads the rank just written
-    const double eps = *U.eps_in;
-    atomicMax(U.maxeps_bits, (unsigned long long)__double_as_longlong(eps));
-    int *li = U.log_info + slot * 5;
-    li[0] = b; li[1] = U.dir; li[2] = rl; li[3] = rr; li[4] = r;
-    U.log_es[slot * 2] = eps;
-    U.log_es[slot * 2 + 1] = __longlong_as_double((long long)*U.scale_bits);
+    // sizes and s as this bond saw them, for index_bond_kernel (which may trail the sweep while
+    // later bonds rewrite rk and s)
+    U.info[0] = rl; U.info[1] = rr; U.info[2] = r;
+    *reinterpret_cast<unsigned long long *>(U.info + 4) = *U.scale_bits;
   }
-  for (int k = gt; k < r; k += gs) {
-    U.log_rows[slot * U.cap_piv + k] = U.rows[k];
-    U.log_cols[slot * U.cap_piv + k] = U.cols[k];
-  }
-  // multi-indices: I_b[k] = (I_{b-1}[row / d_b], row % d_b); J_{b+1}[k] = (col / rr, J_{b+2}[col % rr])
-  for (int t = gt; t < r * (b + 1); t += gs) {
-    const int k = t / (b + 1), pos = t % (b + 1);
-    const int row = U.rows[k];
-    U.Inew[t] = pos == b ? (uint8_t)(row % U.db) : U.Iprev[(row / U.db) * b + pos];
-  }
-  const int wJ = L - b - 1;
-  for (int t = gt; t < r * wJ; t += gs) {
-    const int k = t / wJ, pos = t % wJ;
-    const int col = U.cols[k];
-    U.Jnew[t] = pos == 0 ? (uint8_t)(col / rr) : U.Jnext[(col % rr) * (wJ - 1) + pos - 1];
-  }
+  (void)L;
+  (void)slot;
   if (U.dir == 0) {
     // A^n_{b+1}[k][:] = Ahat[rows[k]][:] (a row of the look-ahead product is (sigma', beta) of
     // the next bond's (k, sigma') x beta operand)
@@ -519,6 +504,53 @@ __global__ void update_bond_kernel(UpdateArgs U) {
   }
 }
 
+
+// Index-set update (a6, R21), the error bookkeeping (a9) and the pivot log of one bond.
+// Nothing on the sweep's critical path reads them, so this runs on a side stream after the
+// bond's update kernel (whose snapshot of the bond's sizes and s it reads) and overlaps the next
+// bonds; the iteration joins it before the convergence test.
+struct IndexArgs {
+  int b, dir, L, db;
+  const int *rows, *cols, *info;
+  const double *eps_in;
+  uint8_t *Iprev, *Inew, *Jnext, *Jnew;
+  unsigned long long *maxeps_bits;
+  int *log_info;
+  double *log_es;
+  int *log_rows, *log_cols;
+  const int *iter;
+  int step, per_iter, cap_piv;
+};
+__global__ void index_bond_kernel(IndexArgs U) {
+  const int rl = U.info[0], rr = U.info[1], r = U.info[2];
+  const int b = U.b, L = U.L;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  const size_t slot = (size_t)(*U.iter) * U.per_iter + U.step;
+  if (gt == 0) {
+    const double eps = *U.eps_in;
+    atomicMax(U.maxeps_bits, (unsigned long long)__double_as_longlong(eps));
+    int *li = U.log_info + slot * 5;
+    li[0] = b; li[1] = U.dir; li[2] = rl; li[3] = rr; li[4] = r;
+    U.log_es[slot * 2] = eps;
+    U.log_es[slot * 2 + 1] = __longlong_as_double(*reinterpret_cast<const long long *>(U.info + 4));
+  }
+  for (int k = gt; k < r; k += gs) {
+    U.log_rows[slot * U.cap_piv + k] = U.rows[k];
+    U.log_cols[slot * U.cap_piv + k] = U.cols[k];
+  }
+  // multi-indices: I_b[k] = (I_{b-1}[row / d_b], row % d_b); J_{b+1}[k] = (col / rr, J_{b+2}[col % rr])
+  for (int t = gt; t < r * (b + 1); t += gs) {
+    const int k = t / (b + 1), pos = t % (b + 1);
+    const int row = U.rows[k];
+    U.Inew[t] = pos == b ? (uint8_t)(row % U.db) : U.Iprev[(row / U.db) * b + pos];
+  }
+  const int wJ = L - b - 1;
+  for (int t = gt; t < r * wJ; t += gs) {
+    const int k = t / wJ, pos = t % wJ;
+    const int col = U.cols[k];
+    U.Jnew[t] = pos == 0 ? (uint8_t)(col / rr) : U.Jnext[(col % rr) * (wJ - 1) + pos - 1];
+  }
+}
 
 // Convergence test after a full iteration (R10).
 __global__ void converge_kernel(int *rk, int *prev, int L, unsigned long long *maxeps_bits,
@@ -851,6 +883,7 @@ struct Prof {
 
 struct Run {
   Prof *P = nullptr;
+  int *binfo = nullptr;         // 8 ints per bond: the update's snapshot for index_bond_kernel
   cudaError_t launch_err = cudaSuccess;  // first rejected prrLU launch (eager launches)
   int cplx = 0, Z = 1, ZE = 1;  // complex run: Z = 2 doubles per entry, ZE = 4 for expanded operands
   int one = 0;                  // aci_options.concurrent: single-cluster prrLU launches
@@ -999,6 +1032,7 @@ static size_t carve(Run &R, char *base) {
   R.epoch = c.take<unsigned>(1);
   R.counter = c.take<unsigned>(1);
   R.dtrsm = c.take<TrsmArgs>(L);
+  R.binfo = c.take<int>((size_t)8 * std::max(L - 1, 1));
   R.UJ.assign(L, nullptr);
   size_t nblk = 0;
   for (int b = 0; b < L - 1; ++b) {
@@ -1247,9 +1281,26 @@ static void launch_update(Run &R, int b, int dir, int logslot, const BondStatic 
   U.step = logslot;
   U.per_iter = 2 * (R.L - 1);
   U.cap_piv = R.log_cap_piv;
+  U.info = R.binfo + 8 * b;
   size_t work = (size_t)R.rmax[b] * 256;
   int blocks = (int)std::min<size_t>(592, std::max<size_t>(1, (work + 255) / 256));
   update_bond_kernel<<<blocks, 256, 0, st>>>(U);
+}
+
+static void launch_index(Run &R, int b, int dir, int logslot, cudaStream_t st) {
+  IndexArgs U = {};
+  U.b = b; U.dir = dir; U.L = R.L; U.db = R.d[b];
+  U.rows = R.prow[b]; U.cols = R.pcol[b]; U.info = R.binfo + 8 * b; U.eps_in = R.epsb + b;
+  U.Iprev = b > 0 ? R.Imi[b - 1] : nullptr;
+  U.Inew = R.Imi[b];
+  U.Jnext = b + 2 < R.L ? R.Jmi[b + 2] : nullptr;
+  U.Jnew = R.Jmi[b + 1];
+  U.maxeps_bits = R.maxeps;
+  U.log_info = R.log_info; U.log_es = R.log_es; U.log_rows = R.log_rows; U.log_cols = R.log_cols;
+  U.iter = R.iter; U.step = logslot; U.per_iter = 2 * (R.L - 1); U.cap_piv = R.log_cap_piv;
+  const size_t work = (size_t)R.rmax[b] * (size_t)std::max(b + 1, R.L - b - 1);
+  const int blocks = (int)std::min<size_t>(148, std::max<size_t>(1, (work + 255) / 256));
+  index_bond_kernel<<<blocks, 256, 0, st>>>(U);
 }
 
 // Static description of every bond update (both directions), built once per call on the host
@@ -1329,8 +1380,8 @@ static void pre_launch(Run &R, cudaStream_t st) {
 // Created by side_stream_init() at the start of every call, before any stream capture (creating
 // streams or events inside a capture is refused, which left null events behind).
 struct SideStream {
-  cudaStream_t st = nullptr;
-  cudaEvent_t started = nullptr, done = nullptr;
+  cudaStream_t st = nullptr, ix = nullptr;  // look-ahead GEMMs; index/log kernels
+  cudaEvent_t started = nullptr, done = nullptr, upd = nullptr, ix_done = nullptr;
 };
 static SideStream &side_stream() {
   static thread_local SideStream s;
@@ -1338,13 +1389,14 @@ static SideStream &side_stream() {
 }
 static bool side_stream_init() {
   SideStream &s = side_stream();
-  if (s.st && s.started && s.done) return true;
+  if (s.st && s.ix && s.started && s.done && s.upd && s.ix_done) return true;
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   if (!s.st && cudaStreamCreateWithPriority(&s.st, cudaStreamNonBlocking, lo) != cudaSuccess) s.st = nullptr;
-  if (!s.started && cudaEventCreateWithFlags(&s.started, cudaEventDisableTiming) != cudaSuccess) s.started = nullptr;
-  if (!s.done && cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming) != cudaSuccess) s.done = nullptr;
-  return s.st && s.started && s.done;
+  if (!s.ix && cudaStreamCreateWithPriority(&s.ix, cudaStreamNonBlocking, lo) != cudaSuccess) s.ix = nullptr;
+  for (cudaEvent_t *e : {&s.started, &s.done, &s.upd, &s.ix_done})
+    if (!*e && cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) *e = nullptr;
+  return s.st && s.ix && s.started && s.done && s.upd && s.ix_done;
 }
 
 // One 2-site update (Alg. 1): [plan] -> a3+a4 -> a5 (|| look-ahead GEMM) -> a6/a7 (+ the
@@ -1399,6 +1451,22 @@ static void bond_update(Run &R, double tol, int tol_mode, int b, int dir, int lo
   R.P->begin(ACI_PROF_UPDATE);
   launch_update(R, b, dir, logslot, next, st);
   R.P->end(1);
+  cudaEventRecord(sd.upd, st);
+  cudaStreamWaitEvent(sd.ix, sd.upd, 0);
+  cudaStream_t mine = R.P->st;
+  R.P->st = sd.ix;
+  R.P->begin(ACI_PROF_UPDATE);
+  launch_index(R, b, dir, logslot, sd.ix);
+  R.P->end(1);
+  R.P->st = mine;
+}
+
+// End of an iteration's sweeps: the index/log stream joins the main stream (the convergence test
+// reads the error bookkeeping).
+static void index_join(cudaStream_t st) {
+  SideStream &sd = side_stream();
+  cudaEventRecord(sd.ix_done, sd.ix);
+  cudaStreamWaitEvent(st, sd.ix_done, 0);
 }
 
 static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st) {
@@ -1646,6 +1714,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
       bond_update(R, tol, o.tol_mode, b, 0, step++, b == 0, b + 1 < L - 1 ? dstat(R, 0, b + 1) : dstat(R, 1, L - 2), strm);
     for (int b = L - 2; b >= 0; --b)
       bond_update(R, tol, o.tol_mode, b, 1, step++, false, b > 0 ? dstat(R, 1, b - 1) : nullptr, strm);
+    index_join(strm);
     prof.begin(ACI_PROF_CONV);
     converge_kernel<<<1, 32, 0, strm>>>(R.rk, R.prev, L, R.maxeps, R.scale, tol, o.tol_mode, R.conv, R.err,
                                         R.iter);

@@ -1491,10 +1491,6 @@ static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st)
   R.P->begin(ACI_PROF_CANON);
   plan_canon_kernel<<<1, 1, 0, st>>>(C, R.rk);
   FOp dummy = {};
-  if (tm > 0) {
-    if (R.cplx) launch_gemm_z(R.dT, N, tm, 2 * tn, 0, 1, dummy, nullptr, nullptr, st);
-    else launch_gemm(R.dT, N, tm, tn, 1, false, dummy, nullptr, nullptr, st);
-  }
   const int max_m = R.yr[s], max_n = R.nmax[s - 1];
   LuArgs a = {};
   a.M = C.M; a.dims = R.dLu; a.tol = tol; a.thr_mode = tol_mode == ACI_TOL_RELATIVE ? 1 : 2;
@@ -1502,8 +1498,18 @@ static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st)
   a.rows = R.prow[s - 1]; a.cols = R.pcol[s - 1]; a.r_out = R.rout + (s - 1); a.eps_out = R.epsb + (s - 1);
   a.U = nullptr;
   a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter; a.epoch = R.epoch;
-  const cudaError_t le = launch_prrlu(a, max_m, max_n, st, R.cplx != 0, R.one != 0);
+  // the R-frame product T^n = X^n_s R^n_{s+1} is only gathered after the factorisation: it runs on
+  // the side stream beside the prrLU (forked off its launch-completion event, as in the sweep)
+  SideStream &sd = side_stream();
+  const cudaError_t le = launch_prrlu(a, max_m, max_n, st, R.cplx != 0, R.one != 0, tm > 0 ? sd.started : nullptr);
   if (le != cudaSuccess && R.launch_err == cudaSuccess) R.launch_err = le;
+  if (tm > 0) {
+    cudaStreamWaitEvent(sd.st, sd.started, 0);
+    if (R.cplx) launch_gemm_z(R.dT, N, tm, 2 * tn, 0, 1, dummy, nullptr, nullptr, sd.st);
+    else launch_gemm(R.dT, N, tm, tn, 1, false, dummy, nullptr, nullptr, sd.st);
+    cudaEventRecord(sd.done, sd.st);
+    cudaStreamWaitEvent(st, sd.done, 0);
+  }
   CanonUpd U = {};
   U.s = s; U.L = L; U.N = N; U.ds = R.d[s]; U.yr_s = R.yr[s]; U.yr_prev_rows = R.yr[s - 1] * R.d[s - 1];
   U.cols = R.pcol[s - 1]; U.r_in = R.rout + (s - 1);

@@ -3,6 +3,14 @@
 // The GEMMs are in gemm.cu, the prrLU in prrlu.cu. The host code below only computes static
 // capacities and enqueues kernels: live ranks chi'_l never leave the device during a sweep
 // (one word per iteration is read back for the convergence test).
+//
+// Streams per call: the caller's stream carries the critical path of every bond (Pi GEMM ->
+// prrLU -> update kernel); a side stream runs the look-ahead GEMM that produces the next bond's
+// operand beside the prrLU (forked off the prrLU's launch-completion event, joined by the
+// update); a third stream runs the index-set / log kernel of each bond (joined before the
+// convergence test). One iteration of all three is captured as one CUDA graph and cached.
+// Memory: a persistent per-stream workspace (stable address -> graph-cache hits) and a
+// stream-ordered pool for TT cores.
 #include <cuda_runtime.h>
 
 #include <algorithm>

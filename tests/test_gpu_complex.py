@@ -180,3 +180,21 @@ def test_complex_absolute_tolerance_mode(aci):
     assert _pivots_identical_or_tie(ex, ref) >= 20
     exact = _fourier_values(cf["inputs"][0], cf["samples"]) * _fourier_values(cf["inputs"][1], cf["samples"])
     assert np.abs(out.evaluate(cf["samples"]) - exact).max() <= 10 * tau
+
+
+def test_complex_cluster_tiers_vs_oracle(aci):
+    """Complex blocks large enough for the multi-CTA complex prrLU tiers (up to 384 live rows in
+    512-row static blocks): pivots identical to the complex oracle (or diverging only at a
+    roundoff-level tie), and the output equal to the exact product within 10 tol."""
+    L, tol = 16, 1e-10
+    a = _complex_tt(L, 2, 48, 301)
+    b = _complex_tt(L, 2, 4, 302)
+    y0 = random_init([a, b], 256, _rng(303, 2))
+    op = {"coef": [1.0], "expo": [[1, 1]]}
+    out, st, rep, ex = aci.aci_elementwise(op, [aci.TensorTrain.from_cores(a), aci.TensorTrain.from_cores(b)], tol,
+                                           256, 4, y_init=aci.TensorTrain.from_cores(y0), log=True)
+    assert max(out.shape()[1]) > 128  # the grid tiers were used
+    ref = oracle.aci_z([a, b], op, y0, tol, 256, 4)
+    _pivots_identical_or_tie(ex, ref)  # any divergence only at a roundoff-level tie
+    exact = oracle.tt_dense(a) * oracle.tt_dense(b)
+    assert np.abs(oracle.tt_dense(out.cores()) - exact).max() <= 10 * tol * np.abs(exact).max()

@@ -486,3 +486,41 @@ def test_edge_shapes_vs_oracle(aci):
     Dz = [oracle.tt_dense(x) for x in xz]
     exactz = sum(c * np.prod([Dz[n] ** e for n, e in enumerate(ex_)], axis=0) for c, ex_ in zip(op["coef"], op["expo"]))
     assert _rel(oracle.tt_dense(outz.cores()), exactz) <= 1e-10
+
+
+_TIER_SCRIPT = r"""
+import hashlib, sys
+sys.path.insert(0, ".")
+import numpy as np
+import paper_2604_00037_b200 as aci
+from workloads import make_config
+aci.load()
+cf = make_config(int(sys.argv[1]), int(sys.argv[2]), npts=0)
+xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+y0 = aci.TensorTrain.from_cores(cf["y_init"])
+out, st, rep, ex = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0, log=True)
+h = hashlib.sha256()
+for e in ex["log"]:
+    h.update(np.asarray(e["rows"], np.int32).tobytes()); h.update(np.asarray(e["cols"], np.int32).tobytes())
+print(h.hexdigest(), len(ex["log"]))
+"""
+
+
+@pytest.mark.parametrize("cfg,chi", [(3, 64), (1, 32), (3, 256)])
+def test_prrlu_tiers_identical_pivots(aci, cfg, chi):
+    """Every prrLU tier takes the same decisions (same keys, tie-break and arithmetic, R3/R4):
+    the default tiers, the L2 grid tier (no clusters), 8-CTA clusters, no push tier, and direct
+    launches instead of the CUDA graph give bit-identical pivot logs (subprocesses: the switches
+    are read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = {}
+    for name, env in [("default", {}), ("l2_grid", {"ACI_PRRLU_CLUSTER": "0"}), ("cluster8", {"ACI_PRRLU_CLUSTER": "8"}),
+                      ("no_push", {"ACI_PRRLU_PUSH": "0"}), ("no_graph", {"ACI_NO_GRAPH": "1"})]:
+        r = subprocess.run([sys.executable, "-c", _TIER_SCRIPT, str(cfg), str(chi)], cwd=root, capture_output=True,
+                           text=True, timeout=300, env={**os.environ, **env})
+        assert r.returncode == 0, (name, r.stderr[-2000:])
+        runs[name] = r.stdout.split()
+    assert len({tuple(v) for v in runs.values()}) == 1, runs

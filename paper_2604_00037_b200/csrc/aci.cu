@@ -347,9 +347,8 @@ __device__ __forceinline__ GemmDesc desc_b(const BondStatic &S, const InBond &I,
 //   R->L: B^n_{b-1} = X^n_b R^n_{b+1} = (X^n_b B^n_b)[:, J_{b+1} cols]     (R^n_{b+1} = B^n_b[:, J])
 // so no GEMM sits between the update of one bond and the Pi of the next. An L->R bond reads B^n_b
 // of the previous R->L half-sweep and an R->L bond A^n_b of this iteration's L->R (R20).
-__device__ void plan_bond(const BondStatic &S, const int *rk, GemmDesc *ab, GemmDesc *pi, LuDims *lu) {
+__device__ void plan_bond_r(const BondStatic &S, int rl, int rr, GemmDesc *ab, GemmDesc *pi, LuDims *lu) {
   const int b = S.b;
-  const int rl = rk[b], rr = rk[b + 2];
   const int m = rl * S.db, n = S.db1 * rr;
   const int z = S.Z;
   GemmDesc P = {};
@@ -382,6 +381,10 @@ __device__ void plan_bond(const BondStatic &S, const int *rk, GemmDesc *ab, Gemm
   D.kmax = min(S.maxrank, min(m, n));
   D.ldu = S.ldu;
   *lu = D;
+}
+
+__device__ __forceinline__ void plan_bond(const BondStatic &S, const int *rk, GemmDesc *ab, GemmDesc *pi, LuDims *lu) {
+  plan_bond_r(S, rk[S.b], rk[S.b + 2], ab, pi, lu);
 }
 
 __global__ void plan_bond_kernel(const BondStatic *S, const int *rk, GemmDesc *ab, GemmDesc *pi, LuDims *lu) {
@@ -431,6 +434,7 @@ struct UpdateArgs {
   GemmDesc *ab, *pi;
   LuDims *lu;
   int *info;                  // 8 ints: this bond's (rl, rr, r, -, s bits) for index_bond_kernel
+  int next_b;                 // bond index of `next` (-1: none)
 };
 
 // Index-set update (a6, R21) and frame update (a7: the rows/columns of A^n / B^n the
@@ -451,9 +455,13 @@ __global__ void update_bond_kernel(UpdateArgs U) {
     for (int t = threadIdx.x; t < (int)(sizeof(BondStatic) / 8); t += 32) dst[t] = src[t];
     __syncwarp();
   }
+  // the next bond's ranks, loaded together with r (rk[b+1], which this kernel writes, is r)
+  const int nb = U.next_b;
+  const int rl2 = nb >= 0 ? (nb == b + 1 ? r : U.rk[nb]) : 0;
+  const int rr2 = nb >= 0 ? (nb + 2 == b + 1 ? r : U.rk[nb + 2]) : 0;
   if (gt == 0) {
-    U.rk[b + 1] = r;  // no thread of this kernel reads rk[b+1]
-    if (U.next) plan_bond(s_next, U.rk, U.ab, U.pi, U.lu);  // reads the rank just written
+    U.rk[b + 1] = r;
+    if (U.next) plan_bond_r(s_next, rl2, rr2, U.ab, U.pi, U.lu);
     // sizes and s as this bond saw them, for index_bond_kernel (which may trail the sweep while
     // later bonds rewrite rk and s)
     U.info[0] = rl; U.info[1] = rr; U.info[2] = r;
@@ -1261,6 +1269,7 @@ namespace {
 static void launch_update(Run &R, int b, int dir, int logslot, const BondStatic *next, cudaStream_t st) {
   UpdateArgs U = {};
   U.next = next; U.ab = R.dAB; U.pi = R.dPi; U.lu = R.dLu;
+  U.next_b = next ? (int)((next - R.dStat) % (R.L - 1)) : -1;
   U.b = b; U.dir = dir; U.L = R.L; U.N = R.N; U.db = R.d[b]; U.db1 = R.d[b + 1];
   U.rows = R.prow[b]; U.cols = R.pcol[b]; U.r_in = R.rout + b; U.eps_in = R.epsb + b;
   U.rk = R.rk;

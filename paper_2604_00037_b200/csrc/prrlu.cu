@@ -23,9 +23,14 @@
 //     (st.async + mbarrier), the candidate column published to L2 as tagged packets (each
 //     8-byte word carries epoch|step, so no release/acquire fence is needed); several clusters
 //     exchange cluster winners through L2 (one poller per cluster + DSMEM broadcast).
+//   * push tier (XM = 3, prrlu_kernel_push, real blocks of <= 128 static rows): one 8-CTA cluster;
+//     every CTA pushes its candidate column with its key into every peer's shared memory
+//     (cp.async.bulk over DSMEM), so the winner's column is local when the keys are in.
 //   * L2 grid tier (XM = 1): cooperative launch, tagged key packets with a key-poll or counter
 //     barrier — used only when 16- and 8-CTA clusters cannot all be co-resident.
 //   * single-cluster mode (prrlu_kernel_one, aci_options.concurrent): at most one cluster.
+// All tiers use the same keys, tie-break and arithmetic, so they take identical decisions
+// (tests/test_gpu_parity.py::test_prrlu_tiers_identical_pivots).
 #include <cstdlib>
 
 #include "aci_common.cuh"

@@ -206,6 +206,32 @@ int aci_elementwise(aci_op op, const tt_t *const *inputs, int n_inputs, double t
 int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_inputs, double tol, int maxrank,
                        int max_sweeps, tt_t **out, aci_report *rep, const aci_options *opts);
 
+/* One product of a batch (aci_elementwise_batch). */
+typedef struct {
+  aci_op op;
+  const tt_t *const *inputs;
+  int n_inputs;
+  double tol;
+  int maxrank;
+  int max_sweeps;
+  const aci_options *options; /* nullable; `concurrent` is forced on and `stream`/`workspace` are
+                               * ignored: every product runs on a library stream of its worker */
+  tt_t **out;                  /* out: new TT owned by the caller */
+  aci_report *rep;             /* out, nullable */
+  int status;                  /* out: this product's return code (ACI_OK, ACI_NOT_CONVERGED, < 0) */
+} aci_job;
+
+/*
+ * aci_elementwise_batch — several independent products (concurrent products
+ * on one GPU, P:74 time stepping, several nonlinear terms) run concurrently: min(n_jobs,
+ * max_parallel) library threads (max_parallel <= 0: 8) each take the next job and run it with
+ * aci_options.concurrent on their own stream, so the products overlap on the GPU (every prrLU
+ * launch stays within one thread-block cluster). Each job's result is exactly what the
+ * corresponding aci_elementwise_ex call returns. Returns ACI_OK if every job returned >= 0,
+ * else the first negative status in job order (the other jobs still ran; see jobs[i].status).
+ */
+int aci_elementwise_batch(aci_job *jobs, int n_jobs, int max_parallel);
+
 /* Device workspace (bytes) aci_elementwise_ex needs for these inputs and maxrank. */
 int aci_workspace_query(const tt_t *const *inputs, int n_inputs, int maxrank, const tt_t *y_init,
                         size_t *bytes);

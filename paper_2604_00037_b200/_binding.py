@@ -22,7 +22,7 @@ MAX_INPUTS, MAX_TERMS, MAX_EXPO = 4, 8, 4
 # every symbol include/aci.h declares (tests check the library exports all of them)
 EXPORTS = ["tt_create", "tt_create_z", "tt_create_device", "tt_create_device_z", "tt_is_complex", "tt_destroy",
            "tt_shape", "tt_get_cores", "tt_device_cores", "tt_evaluate", "tt_evaluate_device", "aci_elementwise",
-           "aci_elementwise_ex", "aci_workspace_query", "aci_limits", "aci_last_error", "aci_version"]
+           "aci_elementwise_ex", "aci_elementwise_batch", "aci_workspace_query", "aci_limits", "aci_last_error", "aci_version"]
 
 
 class AciError(RuntimeError):
@@ -98,6 +98,7 @@ def load(path: str = LIB_PATH):
                                     C.POINTER(aci_report)]
     lib.aci_elementwise_ex.argtypes = [aci_op, C.POINTER(vp), C.c_int, C.c_double, C.c_int, C.c_int,
                                        C.POINTER(vp), C.POINTER(aci_report), C.POINTER(aci_options)]
+    lib.aci_elementwise_batch.argtypes = [C.POINTER(aci_job), C.c_int, C.c_int]
     lib.aci_workspace_query.argtypes = [C.POINTER(vp), C.c_int, C.c_int, vp, C.POINTER(C.c_size_t)]
     lib.aci_limits.argtypes = [ip, ip]
     lib.aci_last_error.restype = C.c_char_p
@@ -274,6 +275,54 @@ def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, t
         extras["I"] = [Ibufs[b][:rk[b + 1]].copy() for b in range(L - 1)]
         extras["J"] = {s: Jbufs[s][:rk[s]].copy() for s in range(1, L)}
     return res, st, rep.as_dict(), extras
+
+
+class aci_job(C.Structure):
+    _fields_ = [("op", aci_op), ("inputs", C.POINTER(C.c_void_p)), ("n_inputs", C.c_int), ("tol", C.c_double),
+                ("maxrank", C.c_int), ("max_sweeps", C.c_int), ("options", C.POINTER(aci_options)),
+                ("out", C.POINTER(C.c_void_p)), ("rep", C.POINTER(aci_report)), ("status", C.c_int)]
+
+
+def aci_elementwise_batch(jobs, max_parallel=0):
+    """Run aci_elementwise_batch: ``jobs`` is a list of dicts with the aci_elementwise arguments
+    (op, inputs, tol, maxrank, max_sweeps; optional y_init, seed, tol_mode). The products run
+    concurrently on library threads and streams. Returns a list of (TensorTrain, status, report)
+    in job order; raises AciError if any job failed."""
+    lib = load()
+    n = len(jobs)
+    arr = (aci_job * n)()
+    keep, outs, reps, opts = [], [], [], []
+    for i, j in enumerate(jobs):
+        ins = j["inputs"]
+        cop, k = _make_op(j["op"], len(ins))
+        hs = (C.c_void_p * len(ins))(*[x.handle.value for x in ins])
+        o = aci_options()
+        o.seed = j.get("seed", 0)
+        o.y_init = j["y_init"].handle.value if j.get("y_init") is not None else None
+        o.tol_mode = j.get("tol_mode", TOL_RELATIVE)
+        out = C.c_void_p()
+        rep = aci_report()
+        keep += [cop, k, hs]
+        outs.append(out)
+        reps.append(rep)
+        opts.append(o)
+        arr[i].op = cop
+        arr[i].inputs = C.cast(hs, C.POINTER(C.c_void_p))
+        arr[i].n_inputs = len(ins)
+        arr[i].tol = float(j["tol"])
+        arr[i].maxrank = int(j["maxrank"])
+        arr[i].max_sweeps = int(j["max_sweeps"])
+        arr[i].options = C.pointer(o)
+        arr[i].out = C.pointer(out)
+        arr[i].rep = C.pointer(rep)
+    st = lib.aci_elementwise_batch(arr, n, int(max_parallel))
+    res = [(TensorTrain(outs[i]) if outs[i].value else None, int(arr[i].status), reps[i].as_dict()) for i in range(n)]
+    if st < 0:
+        for r in res:
+            if r[0] is not None:
+                r[0].free()
+    _check(st)
+    return res
 
 
 def workspace_query(inputs, maxrank, y_init=None) -> int:

@@ -21,6 +21,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <atomic>
 #include <vector>
 
 #include "../../include/aci.h"
@@ -1994,6 +1996,31 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
 extern "C" int aci_elementwise(aci_op op, const tt_t *const *inputs, int n_inputs, double tol, int maxrank,
                                int max_sweeps, tt_t **out, aci_report *rep) {
   return aci_elementwise_ex(op, inputs, n_inputs, tol, maxrank, max_sweeps, out, rep, nullptr);
+}
+
+extern "C" int aci_elementwise_batch(aci_job *jobs, int n_jobs, int max_parallel) {
+  if (n_jobs < 0 || (n_jobs > 0 && !jobs)) return fail(ACI_ERR_INVALID, "aci_elementwise_batch: null jobs");
+  if (n_jobs == 0) return ACI_OK;
+  const int nt = std::max(1, std::min(n_jobs, max_parallel > 0 ? max_parallel : 8));
+  std::atomic<int> next{0};
+  auto worker = [&]() {
+    for (int j = next.fetch_add(1); j < n_jobs; j = next.fetch_add(1)) {
+      aci_job &J = jobs[j];
+      aci_options o = J.options ? *J.options : aci_options{};
+      o.concurrent = 1;
+      o.stream = nullptr;  // the worker thread's library stream
+      o.workspace = nullptr;
+      o.workspace_bytes = 0;
+      J.status = aci_elementwise_ex(J.op, J.inputs, J.n_inputs, J.tol, J.maxrank, J.max_sweeps, J.out, J.rep, &o);
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(worker);
+  worker();
+  for (auto &t : th) t.join();
+  for (int j = 0; j < n_jobs; ++j)
+    if (jobs[j].status < 0) return fail(jobs[j].status, "aci_elementwise_batch: job " + std::to_string(j) + " failed");
+  return ACI_OK;
 }
 
 extern "C" int aci_workspace_query(const tt_t *const *inputs, int n_inputs, int maxrank, const tt_t *y_init,

@@ -524,3 +524,24 @@ def test_prrlu_tiers_identical_pivots(aci, cfg, chi):
         assert r.returncode == 0, (name, r.stderr[-2000:])
         runs[name] = r.stdout.split()
     assert len({tuple(v) for v in runs.values()}) == 1, runs
+
+
+def test_batch_api_matches_single_products(aci):
+    """aci_elementwise_batch (NEXT-2): several independent products on library threads/streams give
+    bitwise the outputs and reports of the same products run one by one; a failing job reports its
+    own status while the others complete."""
+    jobs, refs = [], []
+    for cfg, chi in [(0, None), (1, None), (3, 64), (0, None), (1, None), (3, 64)]:
+        cf = make_config(cfg, chi, npts=0) if chi else make_config(cfg, npts=0)
+        xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+        y0 = aci.TensorTrain.from_cores(cf["y_init"])
+        jobs.append({"op": cf["op"], "inputs": xs, "tol": cf["tol"], "maxrank": cf["maxrank"],
+                     "max_sweeps": cf["max_sweeps"], "y_init": y0})
+        refs.append(aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0))
+    res = aci.aci_elementwise_batch(jobs, max_parallel=4)
+    for (tt, st, rep), (rtt, rst, rrep, _) in zip(res, refs):
+        assert st == rst and rep["pivot_steps"] == rrep["pivot_steps"] and rep["iterations"] == rrep["iterations"]
+        assert all(np.array_equal(a, b) for a, b in zip(tt.cores(), rtt.cores()))
+    bad = dict(jobs[0], tol=-1.0)
+    with pytest.raises(aci.AciError):
+        aci.aci_elementwise_batch([jobs[0], bad])

@@ -10,6 +10,10 @@ using C32 = Cfg<32, 32, 16, 16, 16, 3, 4>;
 using C3264 = Cfg<32, 64, 16, 32, 16, 3, 4>;
 using C6432 = Cfg<64, 32, 32, 16, 16, 3, 4>;
 using C32b = Cfg<32, 32, 16, 16, 32, 3, 4>;
+using C32w8 = Cfg<32, 64, 16, 16, 16, 3, 4>;   // 8 warps of 16x16
+using C64w8s4 = Cfg<64, 64, 32, 16, 16, 4, 2>;
+using C32s4 = Cfg<32, 32, 16, 16, 16, 4, 4>;
+using C32x16 = Cfg<32, 32, 16, 8, 16, 3, 4>;  // 8 warps of 16x8
 
 __global__ void empty_kernel(int *p) { if (p && threadIdx.x == 1023) *p = 0; }
 
@@ -30,6 +34,10 @@ int main() {
   set_attr<C3264, 1, 1, EPI_F>();
   set_attr<C6432, 1, 1, EPI_F>();
   set_attr<C32b, 1, 1, EPI_F>();
+  set_attr<C32w8, 1, 1, EPI_F>();
+  set_attr<C64w8s4, 1, 1, EPI_F>();
+  set_attr<C32s4, 1, 1, EPI_F>();
+  set_attr<C32x16, 1, 1, EPI_F>();
   cudaStream_t st; cudaStreamCreate(&st);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   auto timeit = [&](auto fn, int n) {
@@ -66,8 +74,12 @@ int main() {
     const float t3264 = timeit([&] { launch<C3264, 1, 1, EPI_F>(dd, 1, sz[0], sz[1], op, sb, nf, st); }, 100);
     const float t6432 = timeit([&] { launch<C6432, 1, 1, EPI_F>(dd, 1, sz[0], sz[1], op, sb, nf, st); }, 100);
     const float t32b = timeit([&] { launch<C32b, 1, 1, EPI_F>(dd, 1, sz[0], sz[1], op, sb, nf, st); }, 100);
-    printf("Pi %4d x %4d x %3d: 64x64 static %7.2f fitted %7.2f | 32x32 %7.2f | 32x64 %7.2f | 64x32 %7.2f | 32x32bk32 %7.2f us | %s\n",
-           sz[0], sz[1], sz[2], tstat, tfit, t32, t3264, t6432, t32b, cudaGetErrorString(cudaGetLastError()));
+    const float ta = timeit([&] { launch<C32w8, 1, 1, EPI_F>(dd, 1, sz[0], sz[1], op, sb, nf, st); }, 100);
+    const float tb = timeit([&] { launch<C64w8s4, 1, 1, EPI_F>(dd, 1, sz[0], sz[1], op, sb, nf, st); }, 100);
+    const float tc = timeit([&] { launch<C32s4, 1, 1, EPI_F>(dd, 1, sz[0], sz[1], op, sb, nf, st); }, 100);
+    const float td = timeit([&] { launch<C32x16, 1, 1, EPI_F>(dd, 1, sz[0], sz[1], op, sb, nf, st); }, 100);
+    printf("Pi %4d x %4d x %3d: 64x64 %7.2f | 32x32 %7.2f | 32x64 %7.2f | 64x32 %7.2f | 32x32bk32 %7.2f | 32x64w8 %7.2f | 64x64s4 %7.2f | 32x32s4 %7.2f | 32x32w8 %7.2f us | %s\n",
+           sz[0], sz[1], sz[2], tfit, t32, t3264, t6432, t32b, ta, tb, tc, td, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }

@@ -28,19 +28,47 @@ METRIC = "ACI Hadamard-product wall time (ms) and FP64 TFLOP/s vs χ; fraction o
 UNIT = "TFLOP/s (FP64, contraction model)"
 
 
-def _peaks():
-    """Roofline denominators: MEASURED_PEAKS.json has no FP64 entry, so the FP64 peaks are the
-    ones measured on this pool by tools/probe (profiles/r01_probe_sync_dmma.txt,
-    profiles/r01_dgemm_peak.json): DMMA 37.1 TF/s, DFMA 34.0 TF/s, cuBLAS DGEMM 35.5 TF/s."""
-    p = {"dmma_tflops": 37.13, "dfma_tflops": 33.97, "dgemm_tflops": 35.46, "source": "measured (tools/probe)"}
+def _file_peaks():
+    """HBM copy bandwidth from the driver-written MEASURED_PEAKS.json (it has no FP64 entry)."""
     try:
         m = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        p["hbm_gbs"] = m.get("hbm_gbs")
-        for k in ("fp64_tflops", "dgemm_tflops"):
-            if k in m:
-                p["dgemm_tflops"] = m[k]
+        return {"hbm_gbs": m.get("hbm_gbs"), "hbm_source": "MEASURED_PEAKS.json"}
     except Exception:
-        p["hbm_gbs"] = 6539.9
+        return {"hbm_gbs": 6650.0, "hbm_source": "fallback (B200_PROFILING.md)"}
+
+
+def measure_peaks(stream=None):
+    """FP64 roofline denominators measured IN THIS RUN on this GPU (MEASURED_PEAKS.json has no FP64
+    entry): cuBLAS DGEMM 8192^3 through torch.matmul (best of 5 after a warm-up, CUDA events), the
+    DMMA register loop and the DFMA register loop of libaci_peak.so (paper_2604_00037_b200/csrc/
+    peak_probe.cu; best of 5 launches over all SMs)."""
+    import ctypes
+    import torch
+    from paper_2604_00037_b200 import _build
+    p = _file_peaks()
+    lib = ctypes.CDLL(_build.build_peak())
+    lib.aci_peak_fp64.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    for kind, key in ((0, "dmma_tflops"), (1, "dfma_tflops")):
+        v = ctypes.c_double(0.0)
+        rc = lib.aci_peak_fp64(kind, 5, ctypes.byref(v))
+        p[key] = v.value if rc == 0 else None
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    c = torch.matmul(a, b)
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b, out=c)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, 2.0 * n ** 3 / (e0.elapsed_time(e1) * 1e9))
+    del a, b, c
+    torch.cuda.empty_cache()
+    p["dgemm_tflops"] = best
+    p["source"] = ("measured in this bench run: cuBLAS DGEMM 8192^3 (torch.matmul float64), DMMA / DFMA "
+                   "register loops over all SMs (csrc/peak_probe.cu); best of 5")
     return p
 
 
@@ -117,17 +145,31 @@ def _dist():
     return ws, rank, local
 
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def run_reference(args):
-    """The oracle (CPU, single thread) on a bounded sample of the workload."""
+    """The oracle (CPU, single thread) as the reference arm: every TIMED step is the whole
+    workload (configs[3] at --chi, all 4 iterations: the same config as our arm); the untimed
+    warm-up steps run iteration 1 only (a CPU program has no warm-up effect worth a 27 s product),
+    so --steps K --warmup W costs about K whole products."""
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
     import oracle
     from workloads import make_config
     cf = make_config(3, args.chi, npts=0)
-    sweeps = args.ref_arm_sweeps  # bounded per-step sample, so W + K oracle runs end within minutes
     times, flops = [], []
     for i in range(args.warmup + args.steps):
+        sweeps = cf["max_sweeps"] if i >= args.warmup else 1
         t0 = time.perf_counter()
         res = oracle.aci(cf["inputs"], cf["op"], cf["y_init"], cf["tol"], cf["maxrank"], sweeps)
         dt = time.perf_counter() - t0
@@ -137,16 +179,18 @@ def run_reference(args):
         res.free()
     tot_t, tot_f = sum(times), sum(flops)
     value = tot_f / tot_t / 1e12
-    sample = (f"configs[3] chi={args.chi}: oracle ACI with max_sweeps={sweeps} (first {sweeps} of "
-              f"{cf['max_sweeps']} iterations), contraction-model flops / wall time")
+    sample = (f"configs[3] chi={args.chi}: the whole product (all {cf['max_sweeps']} iterations) per timed step, "
+              f"naive-loop C oracle on 1 thread of {os.cpu_count()} host cores ({_cpu_model()}); "
+              f"contraction-model flops / wall time")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / len(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
+            "impl": "reference", "same_config": True,
             "config": {"workload": cf["name"], "chi": args.chi, "L": 40, "d": 2, "maxrank": cf["maxrank"],
-                       "tol": cf["tol"], "iterations": sweeps, "parallelism": "replicas",
+                       "tol": cf["tol"], "iterations": cf["max_sweeps"], "parallelism": "replicas",
                        "l2": "n/a (CPU)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "host_cores": os.cpu_count(),
+                             "cpu_model": _cpu_model(), "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -190,9 +234,67 @@ def cpu_baseline(chi, sweeps):
     dt = time.perf_counter() - t0
     v = res.report["flops_contraction"] / dt / 1e12
     res.free()
-    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+    return {"value": v, "unit": UNIT, "cores": 1, "host_cores": os.cpu_count(), "cpu_model": _cpu_model(),
+            "kind": "oracle",
             "sample": f"configs[3] chi={chi}, {sweeps} of 4 iterations (4 = the whole product), single-thread naive C oracle, "
-                      f"{dt:.1f} s on {os.cpu_count()} host cores (1 used)"}
+                      f"{dt:.1f} s on 1 of {os.cpu_count()} host cores ({_cpu_model()})"}
+
+
+def _free_port():
+    import socket
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    return port
+
+
+def launch_ranks(n, argv):
+    """`bench.py --gpus N` outside torchrun: re-launch this script as N ranks (one process per GPU)
+    under torch.distributed.run on 127.0.0.1; the ranks assert WORLD_SIZE == N. NCCL's
+    communicator log stays on (NCCL_DEBUG=INFO unless set)."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args):
+    """--dry-run: the multi-rank plumbing on CPU (gloo), for tests: every rank times the CPU oracle
+    on configs[0] as its 'product', the line aggregates over ranks exactly as the GPU path does
+    (max time, summed work) and reports n_gpus = the ranks that ran."""
+    import torch.distributed as tdist
+    ws, rank, _ = _dist()
+    dist = None
+    if ws > 1:
+        tdist.init_process_group("gloo")
+        dist = tdist
+    import oracle
+    from workloads import make_config
+    cf = make_config(0, npts=0)
+    tot, fl = 0.0, 0.0
+    for i in range(args.warmup + args.steps):
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        r = oracle.aci(cf["inputs"], cf["op"], cf["y_init"], cf["tol"], cf["maxrank"], cf["max_sweeps"])
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            tot += 1e3 * dt
+            fl += r.report["flops_contraction"]
+        r.free()
+    t_max, f_sum, _ = reduce_over_ranks(tot, fl, 0.0, dist, "cpu")
+    world = dist.get_world_size() if dist is not None else 1
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": f_sum / t_max / 1e9, "unit": UNIT, "n_gpus": world,
+                          "ranks_ran": world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": t_max / args.steps, "dry_run": True, "scaling": "weak",
+                          "config": {"workload": cf["name"], "parallelism": f"replicas x{world}"}}), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
 
 
 def main():
@@ -203,13 +305,26 @@ def main():
     ap.add_argument("--chi", type=int, default=256)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-sweeps", type=int, default=4, help="cpu_baseline sample: oracle iterations (4 = whole)")
-    ap.add_argument("--ref-arm-sweeps", type=int, default=3, help="--impl reference: oracle iterations per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="CPU/gloo multi-rank plumbing check (tests)")
     ap.add_argument("--no-chi-sweep", action="store_true", help="skip the chi = 64, 128 products")
     ap.add_argument("--no-complex", action="store_true", help="skip the complex Fourier-series sweep")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    ws, rank, local = _dist()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        if not args.dry_run:
+            import torch
+            if torch.cuda.device_count() < args.gpus:
+                print(json.dumps({"error": f"--gpus {args.gpus} but {torch.cuda.device_count()} visible GPUs"}))
+                return 2
+        return launch_ranks(args.gpus, sys.argv[1:])
+    if "WORLD_SIZE" in os.environ and args.impl == "ours" and ws != args.gpus:
+        print(json.dumps({"error": f"WORLD_SIZE={ws} but --gpus {args.gpus}"}), flush=True)
+        return 2
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -217,7 +332,6 @@ def main():
     import paper_2604_00037_b200 as aci
     from workloads import make_config
 
-    ws, rank, local = _dist()
     torch.cuda.set_device(local)
     dist = None
     if ws > 1:
@@ -500,8 +614,8 @@ def main():
     t_max, f_sum, e2e_sum = reduce_over_ranks(tot_ms, tot_flops, e2e["value"] if e2e else 0.0, dist, "cuda")
     if e2e is not None:
         e2e["value"] = e2e_sum
+    pk = measure_peaks()  # after the timed regions: the same process, clocks and GPU
     if rank == 0:
-        pk = _peaks()
         value = f_sum / t_max / 1e9  # GFLOP/ms -> TFLOP/s
         steps = args.steps
         r0 = reps[-1]
@@ -526,12 +640,15 @@ def main():
                                           "for the winner's column (~800 cycles at 1965 MHz = 0.41 us); the "
                                           "rank-1 update itself is ALU-issue bound (DESIGN.md §5)"},
                       "note": "latency-bound: one cluster/L2 exchange per pivot (DESIGN.md §5); 'frac' above is "
-                              "against the measured DFMA rate, 'latency.frac' against the exchange floor"}
+                              "against the DFMA register loop measured in this run (peaks.dfma_tflops), "
+                              "'latency.frac' against the exchange floor"}
         roof_pi = {"kernel": "gemm_dmma_kernel<fused f> (a3+a4) + a1/a2", "bound": "tensor",
                    "achieved": pi_flops / ((pi["ms"] + prof["gemm_ab"]["ms"]) * 1e9),
                    "peak": pk["dmma_tflops"], "unit": "TFLOP/s",
                    "frac": pi_flops / ((pi["ms"] + prof["gemm_ab"]["ms"]) * 1e9) / pk["dmma_tflops"],
-                   "traffic": None, "note": "FP64 DMMA (mma.sync m8n8k4); peak = measured DMMA microbenchmark"}
+                   "traffic": None, "note": "FP64 DMMA (mma.sync m8n8k4); peak = the DMMA register loop measured "
+                                            "in this run (peaks.dmma_tflops); peaks.dgemm_tflops = cuBLAS DGEMM "
+                                            "8192^3 in this run"}
         tr = _ncu_traffic()
         if "prrlu" in tr:
             roof_prrlu["traffic"] = tr["prrlu"]["bytes"]
@@ -541,7 +658,7 @@ def main():
             roof_pi["traffic_source"] = tr["contraction"]["source"] + ": " + tr["contraction"]["kernel"]
         roof = roof_prrlu if dom == "prrlu" else roof_pi
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": steps,
             "warmup": args.warmup, "ms_per_step": t_max / steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cf["name"], "chi": args.chi, "L": 40, "d": 2, "maxrank": cf["maxrank"],

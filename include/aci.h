@@ -165,8 +165,14 @@ typedef struct {
   const tt_t *y_init;        /* initial guess; ranks are capped at maxrank */
   int tol_mode;              /* ACI_TOL_RELATIVE | ACI_TOL_ABSOLUTE */
   aci_pivot_log *log;        /* optional */
-  void *stream;              /* cudaStream_t; NULL = library stream */
-  void *workspace;           /* optional caller device memory (e.g. a torch tensor) */
+  void *stream;              /* cudaStream_t; NULL = the calling thread's library stream. A stream
+                              * carries one call at a time: a call on a stream another call is
+                              * still using returns ACI_ERR_INVALID (concurrent calls: one stream
+                              * each) */
+  void *workspace;           /* optional caller device memory (e.g. a torch tensor), >= the bytes
+                              * aci_workspace_query returns, 256-byte aligned (else ACI_ERR_INVALID;
+                              * cudaMalloc and the torch caching allocator return 512-byte aligned
+                              * blocks). The library owns it for the duration of the call. */
   size_t workspace_bytes;
   /* optional: multi-indices of the final index sets, host buffers:
    * I_sets[b] must hold (>= out rank of bond b) x (b+1) bytes; J_sets[s] (>= rank) x (L-s). */
@@ -232,8 +238,12 @@ typedef struct {
  */
 int aci_elementwise_batch(aci_job *jobs, int n_jobs, int max_parallel);
 
-/* Device workspace (bytes) aci_elementwise_ex needs for these inputs and maxrank. */
-int aci_workspace_query(const tt_t *const *inputs, int n_inputs, int maxrank, const tt_t *y_init,
+/* Device workspace (bytes) aci_elementwise_ex needs for these inputs, maxrank and max_sweeps (the
+ * per-update pivot log holds max_sweeps iterations; a call with more sweeps than the query was
+ * made for returns ACI_ERR_OOM "caller workspace too small"). y_init: nullable (the default
+ * initial guess's ranks are assumed). Errors: ACI_ERR_INVALID (null, maxrank < 1, max_sweeps < 1),
+ * ACI_ERR_SHAPE, ACI_ERR_UNSUPPORTED. */
+int aci_workspace_query(const tt_t *const *inputs, int n_inputs, int maxrank, int max_sweeps, const tt_t *y_init,
                         size_t *bytes);
 
 /* Compiled envelope: the largest Pi block (rows, cols) the prrLU kernels accept. */

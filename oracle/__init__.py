@@ -562,11 +562,3 @@ def tt_norm(cores) -> float:
         _, R = np.linalg.qr(c.reshape(r0 * d, r1))
     return float(np.linalg.norm(R))
 
-
-def tt_inner(a, b) -> float:
-    """<a, b> = sum_sigma a_sigma b_sigma, by transfer matrices."""
-    a, b = _cores_of(a), _cores_of(b)
-    E = np.ones((1, 1))
-    for x, y in zip(a, b):
-        E = np.einsum("ab,asc,bsd->cd", E, x, y)
-    return float(E[0, 0])

@@ -99,7 +99,7 @@ def load(path: str = LIB_PATH):
     lib.aci_elementwise_ex.argtypes = [aci_op, C.POINTER(vp), C.c_int, C.c_double, C.c_int, C.c_int,
                                        C.POINTER(vp), C.POINTER(aci_report), C.POINTER(aci_options)]
     lib.aci_elementwise_batch.argtypes = [C.POINTER(aci_job), C.c_int, C.c_int]
-    lib.aci_workspace_query.argtypes = [C.POINTER(vp), C.c_int, C.c_int, vp, C.POINTER(C.c_size_t)]
+    lib.aci_workspace_query.argtypes = [C.POINTER(vp), C.c_int, C.c_int, C.c_int, vp, C.POINTER(C.c_size_t)]
     lib.aci_limits.argtypes = [ip, ip]
     lib.aci_last_error.restype = C.c_char_p
     lib.aci_version.restype = C.c_char_p
@@ -205,6 +205,33 @@ def _make_op(op, n_inputs):
     return aci_op(len(coef), _dptr(coef), expo.ctypes.data_as(C.POINTER(C.c_int))), (coef, expo)
 
 
+def _make_log(L, maxrank, max_sweeps):
+    """An aci_pivot_log sized for max_sweeps iterations, and a reader returning
+    {"log": [per-update dicts], "canon_cols": {s: columns}} once the call has returned."""
+    cap_u = 2 * (L - 1) * max_sweeps
+    cap_p = maxrank
+    info = np.zeros((cap_u, 5), np.int32)
+    es = np.zeros((cap_u, 2))
+    rows = np.zeros((cap_u, cap_p), np.int32)
+    cols = np.zeros((cap_u, cap_p), np.int32)
+    cn = np.zeros(L + 1, np.int32)
+    cc = np.zeros((L + 1, cap_p), np.int32)
+    lg = aci_pivot_log(cap_u, cap_p, info.ctypes.data_as(C.POINTER(C.c_int)), _dptr(es),
+                       rows.ctypes.data_as(C.POINTER(C.c_int)), cols.ctypes.data_as(C.POINTER(C.c_int)), 0,
+                       cn.ctypes.data_as(C.POINTER(C.c_int)), cc.ctypes.data_as(C.POINTER(C.c_int)))
+
+    def read():
+        nw = lg.n_written
+        return {"log": [{"bond": int(info[u, 0]), "dir": int(info[u, 1]), "rl": int(info[u, 2]),
+                         "rr": int(info[u, 3]), "r": int(info[u, 4]), "eps": float(es[u, 0]),
+                         "scale": float(es[u, 1]), "rows": rows[u, :info[u, 4]].copy(),
+                         "cols": cols[u, :info[u, 4]].copy()} for u in range(nw)],
+                "canon_cols": {s: cc[s, :cn[s]].copy() for s in range(1, L)}}
+
+    read.keep = (info, es, rows, cols, cn, cc)
+    return lg, read
+
+
 def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, tol_mode=TOL_RELATIVE,
                     log=False, stream=0, workspace=None, index_sets=False, profile=False, iter_times=False,
                     concurrent=False):
@@ -235,17 +262,7 @@ def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, t
         opts.iter_ms = iter_ms.ctypes.data_as(C.POINTER(C.c_float))
     L = len(inputs[0].shape()[0])
     if log:
-        cap_u = 2 * (L - 1) * max_sweeps
-        cap_p = maxrank
-        info = np.zeros((cap_u, 5), np.int32)
-        es = np.zeros((cap_u, 2))
-        rows = np.zeros((cap_u, cap_p), np.int32)
-        cols = np.zeros((cap_u, cap_p), np.int32)
-        cn = np.zeros(L + 1, np.int32)
-        cc = np.zeros((L + 1, cap_p), np.int32)
-        lg = aci_pivot_log(cap_u, cap_p, info.ctypes.data_as(C.POINTER(C.c_int)), _dptr(es),
-                           rows.ctypes.data_as(C.POINTER(C.c_int)), cols.ctypes.data_as(C.POINTER(C.c_int)), 0,
-                           cn.ctypes.data_as(C.POINTER(C.c_int)), cc.ctypes.data_as(C.POINTER(C.c_int)))
+        lg, read_log = _make_log(L, maxrank, max_sweeps)
         opts.log = C.pointer(lg)
     if index_sets:
         Ibufs = [np.zeros((maxrank, b + 1), np.uint8) for b in range(L - 1)]
@@ -264,12 +281,7 @@ def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, t
     if iter_times:
         extras["iter_ms"] = [float(x) for x in iter_ms[:rep.iterations]]
     if log:
-        nw = lg.n_written
-        extras["log"] = [{"bond": int(info[u, 0]), "dir": int(info[u, 1]), "rl": int(info[u, 2]),
-                          "rr": int(info[u, 3]), "r": int(info[u, 4]), "eps": float(es[u, 0]),
-                          "scale": float(es[u, 1]), "rows": rows[u, :info[u, 4]].copy(),
-                          "cols": cols[u, :info[u, 4]].copy()} for u in range(nw)]
-        extras["canon_cols"] = {s: cc[s, :cn[s]].copy() for s in range(1, L)}
+        extras.update(read_log())
     if index_sets:
         _, rk = res.shape()
         extras["I"] = [Ibufs[b][:rk[b + 1]].copy() for b in range(L - 1)]
@@ -285,13 +297,14 @@ class aci_job(C.Structure):
 
 def aci_elementwise_batch(jobs, max_parallel=0):
     """Run aci_elementwise_batch: ``jobs`` is a list of dicts with the aci_elementwise arguments
-    (op, inputs, tol, maxrank, max_sweeps; optional y_init, seed, tol_mode). The products run
+    (op, inputs, tol, maxrank, max_sweeps; optional y_init, seed, tol_mode, log). The products run
     concurrently on library threads and streams. Returns a list of (TensorTrain, status, report)
-    in job order; raises AciError if any job failed."""
+    in job order — (TensorTrain, status, report, extras) for jobs with log=True — and raises
+    AciError if any job failed."""
     lib = load()
     n = len(jobs)
     arr = (aci_job * n)()
-    keep, outs, reps, opts = [], [], [], []
+    keep, outs, reps, opts, readers = [], [], [], [], []
     for i, j in enumerate(jobs):
         ins = j["inputs"]
         cop, k = _make_op(j["op"], len(ins))
@@ -300,6 +313,13 @@ def aci_elementwise_batch(jobs, max_parallel=0):
         o.seed = j.get("seed", 0)
         o.y_init = j["y_init"].handle.value if j.get("y_init") is not None else None
         o.tol_mode = j.get("tol_mode", TOL_RELATIVE)
+        if j.get("log"):
+            lg, rd = _make_log(len(ins[0].shape()[0]), int(j["maxrank"]), int(j["max_sweeps"]))
+            o.log = C.pointer(lg)
+            keep += [lg, rd]
+            readers.append(rd)
+        else:
+            readers.append(None)
         out = C.c_void_p()
         rep = aci_report()
         keep += [cop, k, hs]
@@ -316,7 +336,8 @@ def aci_elementwise_batch(jobs, max_parallel=0):
         arr[i].out = C.pointer(out)
         arr[i].rep = C.pointer(rep)
     st = lib.aci_elementwise_batch(arr, n, int(max_parallel))
-    res = [(TensorTrain(outs[i]) if outs[i].value else None, int(arr[i].status), reps[i].as_dict()) for i in range(n)]
+    res = [(TensorTrain(outs[i]) if outs[i].value else None, int(arr[i].status), reps[i].as_dict())
+           + ((readers[i](),) if readers[i] is not None else ()) for i in range(n)]
     if st < 0:
         for r in res:
             if r[0] is not None:
@@ -325,11 +346,11 @@ def aci_elementwise_batch(jobs, max_parallel=0):
     return res
 
 
-def workspace_query(inputs, maxrank, y_init=None) -> int:
+def workspace_query(inputs, maxrank, y_init=None, max_sweeps=64) -> int:
     n = len(inputs)
     hs = (C.c_void_p * n)(*[x.handle.value for x in inputs])
     b = C.c_size_t()
-    _check(load().aci_workspace_query(hs, n, maxrank, y_init.handle.value if y_init is not None else None,
+    _check(load().aci_workspace_query(hs, n, maxrank, max_sweeps, y_init.handle.value if y_init is not None else None,
                                       C.byref(b)))
     return b.value
 

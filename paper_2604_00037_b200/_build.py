@@ -19,6 +19,23 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in SRC + HDR)
 
 
+PEAK_SRC = os.path.join(HERE, "csrc", "peak_probe.cu")
+PEAK_LIB = os.path.join(HERE, "libaci_peak.so")
+
+
+def build_peak(force: bool = False) -> str:
+    """libaci_peak.so: the FP64 DMMA / DFMA loops bench.py measures its roofline peaks with."""
+    if force or not os.path.exists(PEAK_LIB) or os.path.getmtime(PEAK_SRC) > os.path.getmtime(PEAK_LIB):
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-shared",
+               "-Xcompiler", "-fPIC", "-o", PEAK_LIB, PEAK_SRC, "-lcudart"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            if os.path.exists(PEAK_LIB):
+                os.remove(PEAK_LIB)
+            raise RuntimeError("nvcc failed (peak probe):\n" + r.stderr[-2000:])
+    return PEAK_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
         cmd = [NVCC] + FLAGS + ["-o", LIB] + SRC + ["-lcudart"]
@@ -50,4 +67,5 @@ def build_example() -> str:
 
 if __name__ == "__main__":
     build(force=True, verbose=False)
+    build_peak(force=True)
     print(LIB)

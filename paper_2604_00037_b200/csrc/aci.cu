@@ -901,7 +901,11 @@ struct Prof {
 
 struct Run {
   Prof *P = nullptr;
-  int *binfo = nullptr;         // 8 ints per bond: the update's snapshot for index_bond_kernel
+  // Per-bond pivot outputs are kept PER SWEEP DIRECTION (index dir * L + b): the index/log kernel of
+  // an L->R update trails the sweep on a side stream, and the first R->L update is the same bond
+  // (L-2); with one buffer per direction nothing on the main stream overwrites what it still reads
+  // (the iteration joins the side stream before the next iteration reuses them).
+  int *binfo = nullptr;         // 8 ints per (dir, bond): the update's snapshot for index_bond_kernel
   cudaError_t launch_err = cudaSuccess;  // first rejected prrLU launch (eager launches)
   int cplx = 0, Z = 1, ZE = 1;  // complex run: Z = 2 doubles per entry, ZE = 4 for expanded operands
   int one = 0;                  // aci_options.concurrent: single-cluster prrLU launches
@@ -969,20 +973,21 @@ static size_t carve(Run &R, char *base) {
   const int L = R.L, N = R.N;
   R.rk = c.take<int>(L + 1);
   R.prev = c.take<int>(L);
-  R.rout = c.take<int>(L);
+  R.rout = c.take<int>(2 * L);
   R.nonfinite = c.take<int>(1);
   R.conv = c.take<int>(1);
   R.iter = c.take<int>(1);
-  R.epsb = c.take<double>(L);
+  R.epsb = c.take<double>(2 * L);
   R.err = c.take<double>(1);
   R.scale = c.take<unsigned long long>(1);
   R.maxeps = c.take<unsigned long long>(1);
-  R.prow.resize(L);
-  R.pcol.resize(L);
-  for (int s = 0; s < L; ++s) {  // bonds 0..L-2 ; index L-1 unused; canon uses bond s-1 arrays
+  R.prow.resize(2 * L);
+  R.pcol.resize(2 * L);
+  for (int t = 0; t < 2 * L; ++t) {  // [dir * L + b], bonds 0..L-2; canon uses the dir-0 arrays of bond s-1
+    const int s = t % L;
     int cap = s < L - 1 ? R.rmax[s] : 1;
-    R.prow[s] = c.take<int>(cap + 1);
-    R.pcol[s] = c.take<int>(cap + 1);
+    R.prow[t] = c.take<int>(cap + 1);
+    R.pcol[t] = c.take<int>(cap + 1);
   }
   R.Rf.assign(N, std::vector<double *>(L + 1, nullptr));
   R.Abuf.assign(N, nullptr);
@@ -1050,7 +1055,7 @@ static size_t carve(Run &R, char *base) {
   R.epoch = c.take<unsigned>(1);
   R.counter = c.take<unsigned>(1);
   R.dtrsm = c.take<TrsmArgs>(L);
-  R.binfo = c.take<int>((size_t)8 * std::max(L - 1, 1));
+  R.binfo = c.take<int>((size_t)16 * std::max(L - 1, 1));
   R.UJ.assign(L, nullptr);
   size_t nblk = 0;
   for (int b = 0; b < L - 1; ++b) {
@@ -1142,10 +1147,18 @@ static std::vector<WsEntry> g_ws;
 static uint64_t g_ws_clock = 0;
 constexpr size_t kWsCap = 16;
 
-static char *stream_workspace_acquire(cudaStream_t st, size_t need) {
+// A stream carries one call at a time: a second call on a stream whose workspace is in use (a
+// concurrent-mode call and a default-tier call from two host threads on one stream) is refused
+// (*busy = true) instead of sharing — or reallocating under — the running call's workspace.
+static char *stream_workspace_acquire(cudaStream_t st, size_t need, bool *busy) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
+  *busy = false;
   for (auto &e : g_ws)
     if (e.st == st) {
+      if (e.inuse > 0) {
+        *busy = true;
+        return nullptr;
+      }
       if (e.size < need) {
         cudaFree(e.ptr);
         e.ptr = nullptr;
@@ -1273,7 +1286,8 @@ static void launch_update(Run &R, int b, int dir, int logslot, const BondStatic 
   U.next = next; U.ab = R.dAB; U.pi = R.dPi; U.lu = R.dLu;
   U.next_b = next ? (int)((next - R.dStat) % (R.L - 1)) : -1;
   U.b = b; U.dir = dir; U.L = R.L; U.N = R.N; U.db = R.d[b]; U.db1 = R.d[b + 1];
-  U.rows = R.prow[b]; U.cols = R.pcol[b]; U.r_in = R.rout + b; U.eps_in = R.epsb + b;
+  const int pv = dir * R.L + b;  // per-direction pivot buffers (Run::binfo)
+  U.rows = R.prow[pv]; U.cols = R.pcol[pv]; U.r_in = R.rout + pv; U.eps_in = R.epsb + pv;
   U.rk = R.rk;
   U.Iprev = b > 0 ? R.Imi[b - 1] : nullptr;
   U.Inew = R.Imi[b];
@@ -1300,7 +1314,7 @@ static void launch_update(Run &R, int b, int dir, int logslot, const BondStatic 
   U.step = logslot;
   U.per_iter = 2 * (R.L - 1);
   U.cap_piv = R.log_cap_piv;
-  U.info = R.binfo + 8 * b;
+  U.info = R.binfo + 8 * (dir * (R.L - 1) + b);
   size_t work = (size_t)R.rmax[b] * 256;
   int blocks = (int)std::min<size_t>(592, std::max<size_t>(1, (work + 255) / 256));
   update_bond_kernel<<<blocks, 256, 0, st>>>(U);
@@ -1309,7 +1323,8 @@ static void launch_update(Run &R, int b, int dir, int logslot, const BondStatic 
 static void launch_index(Run &R, int b, int dir, int logslot, cudaStream_t st) {
   IndexArgs U = {};
   U.b = b; U.dir = dir; U.L = R.L; U.db = R.d[b];
-  U.rows = R.prow[b]; U.cols = R.pcol[b]; U.info = R.binfo + 8 * b; U.eps_in = R.epsb + b;
+  const int pv = dir * R.L + b;
+  U.rows = R.prow[pv]; U.cols = R.pcol[pv]; U.info = R.binfo + 8 * (dir * (R.L - 1) + b); U.eps_in = R.epsb + pv;
   U.Iprev = b > 0 ? R.Imi[b - 1] : nullptr;
   U.Inew = R.Imi[b];
   U.Jnext = b + 2 < R.L ? R.Jmi[b + 2] : nullptr;
@@ -1443,7 +1458,8 @@ static void bond_update(Run &R, double tol, int tol_mode, int b, int dir, int lo
   LuArgs a = {};
   a.M = R.Pi; a.dims = R.dLu; a.tol = tol; a.thr_mode = tol_mode == ACI_TOL_RELATIVE ? 0 : 2;
   a.scale_bits = R.scale;
-  a.rows = R.prow[b]; a.cols = R.pcol[b]; a.r_out = R.rout + b; a.eps_out = R.epsb + b;
+  const int pv = dir * L + b;
+  a.rows = R.prow[pv]; a.cols = R.pcol[pv]; a.r_out = R.rout + pv; a.eps_out = R.epsb + pv;
   a.U = dir == 1 ? R.Ust[b] : nullptr;
   a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter; a.epoch = R.epoch;
   SideStream &sd = side_stream();
@@ -1671,12 +1687,20 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   bool own_ws = false;
   if (o.workspace) {
     if (o.workspace_bytes < need) { tt_destroy(ygen); return fail(ACI_ERR_OOM, "aci: caller workspace too small"); }
+    // 16-byte packet stores/loads and cp.async tiles need aligned carve offsets: the carver aligns
+    // offsets to 256 bytes, so the base must be 256-byte aligned too (aci.h)
+    if (reinterpret_cast<uintptr_t>(o.workspace) & 255u) {
+      tt_destroy(ygen);
+      return fail(ACI_ERR_INVALID, "aci: caller workspace must be 256-byte aligned");
+    }
     ws = (char *)o.workspace;
   } else {
-    ws = stream_workspace_acquire(strm, need);  // pinned until cleanup()
+    bool busy = false;
+    ws = stream_workspace_acquire(strm, need, &busy);  // pinned until cleanup()
     own_ws = ws != nullptr;
     if (!ws) {
       tt_destroy(ygen);
+      if (busy) return fail(ACI_ERR_INVALID, "aci: another call is running on this stream (use one stream per concurrent call)");
       return fail(ACI_ERR_OOM, "aci: workspace allocation failed");
     }
   }
@@ -1839,7 +1863,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
     std::vector<ZTrsmArgs> za(L - 1);
     int nmx = 1, rmx = 1;
     for (int b = 0; b < L - 1; ++b) {
-      za[b] = ZTrsmArgs{R.Ust[b], R.nmax[b], R.pcol[b], res->dcores + res->off[b + 1], rk[b + 1], R.d[b + 1] * rk[b + 2]};
+      za[b] = ZTrsmArgs{R.Ust[b], R.nmax[b], R.pcol[L + b], res->dcores + res->off[b + 1], rk[b + 1], R.d[b + 1] * rk[b + 2]};
       nmx = std::max(nmx, za[b].n);
       rmx = std::max(rmx, za[b].r);
     }
@@ -1864,7 +1888,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
     std::vector<TrsmArgs> ta(L - 1);
     int nmx = 1, nsteps = 0;
     for (int b = 0; b < L - 1; ++b) {
-      ta[b].U = R.Ust[b]; ta[b].ldu = R.nmax[b]; ta[b].cols = R.pcol[b]; ta[b].b = b; ta[b].d1 = R.d[b + 1];
+      ta[b].U = R.Ust[b]; ta[b].ldu = R.nmax[b]; ta[b].cols = R.pcol[L + b];  // the last R->L half-sweep's pivots ta[b].b = b; ta[b].d1 = R.d[b + 1];
       ta[b].UJ = R.UJ[b]; ta[b].ldj = R.rmax[b];
       ta[b].out = res->dcores + res->off[b + 1];
       nmx = std::max(nmx, R.d[b + 1] * rk[b + 2]);
@@ -2023,9 +2047,10 @@ extern "C" int aci_elementwise_batch(aci_job *jobs, int n_jobs, int max_parallel
   return ACI_OK;
 }
 
-extern "C" int aci_workspace_query(const tt_t *const *inputs, int n_inputs, int maxrank, const tt_t *y_init,
-                                   size_t *bytes) {
-  if (!bytes || !inputs || n_inputs < 1 || maxrank < 1) return fail(ACI_ERR_INVALID, "aci_workspace_query: bad args");
+extern "C" int aci_workspace_query(const tt_t *const *inputs, int n_inputs, int maxrank, int max_sweeps,
+                                   const tt_t *y_init, size_t *bytes) {
+  if (!bytes || !inputs || n_inputs < 1 || maxrank < 1 || max_sweeps < 1)
+    return fail(ACI_ERR_INVALID, "aci_workspace_query: bad args");
   std::vector<double> coef(1, 1.0);
   std::vector<int> expo(n_inputs, 1);
   aci_op op = {1, coef.data(), expo.data()};
@@ -2046,7 +2071,7 @@ extern "C" int aci_workspace_query(const tt_t *const *inputs, int n_inputs, int 
     y_init = &tmp;
   }
   Run R;
-  st = build_run(I, y_init, maxrank, 64, R);
+  st = build_run(I, y_init, maxrank, max_sweeps, R);  // the pivot log holds max_sweeps iterations
   if (st) return st;
   *bytes = carve(R, nullptr);
   return ACI_OK;
@@ -2057,7 +2082,7 @@ extern "C" int tt_evaluate_device(const tt_t *t, int64_t npts, const uint8_t *de
                                   void *stream) {
   if (!t || npts < 0 || (npts > 0 && (!dev_idx || !dev_out))) return fail(ACI_ERR_INVALID, "tt_evaluate: bad args");
   if (npts == 0) return ACI_OK;
-  cudaStream_t st = (cudaStream_t)stream;
+  cudaStream_t st = stream ? (cudaStream_t)stream : lib_stream();  // never the legacy stream
   const int L = t->L;
   // complex TTs: the same real pipeline on interleaved vectors (ranks x 2) against 2x2-block
   // expanded cores
@@ -2112,18 +2137,25 @@ extern "C" int tt_evaluate(const tt_t *t, int64_t npts, const uint8_t *idx, doub
   for (int64_t p = 0; p < npts; ++p)
     for (int s = 0; s < L; ++s)
       if (idx[p * L + s] >= t->d[s]) return fail(ACI_ERR_INVALID, "tt_evaluate: index >= d_s");
+  // stream-ordered on the library stream (a legacy-stream cudaMalloc/cudaMemcpy would synchronise
+  // with, and break, stream captures running in other host threads)
+  cudaStream_t st = lib_stream();
   uint8_t *di = nullptr;
   double *dout = nullptr;
   const size_t nout = (size_t)npts * (t->cplx ? 2 : 1);
-  CUDA_TRY(cudaMalloc(&di, (size_t)npts * L));
-  if (cudaMalloc(&dout, sizeof(double) * nout) != cudaSuccess) { cudaFree(di); return fail(ACI_ERR_OOM, "tt_evaluate"); }
-  cudaMemcpy(di, idx, (size_t)npts * L, cudaMemcpyHostToDevice);
-  int st = tt_evaluate_device(t, npts, di, dout, nullptr);
-  if (st == ACI_OK) {
-    cudaError_t e = cudaMemcpy(out, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) st = fail(ACI_ERR_CUDA, cudaGetErrorString(e));
+  if (cudaMallocAsync((void **)&di, (size_t)npts * L, st) != cudaSuccess ||
+      cudaMallocAsync((void **)&dout, sizeof(double) * nout, st) != cudaSuccess) {
+    cudaGetLastError();
+    if (di) cudaFreeAsync(di, st);
+    cudaStreamSynchronize(st);
+    return fail(ACI_ERR_OOM, "tt_evaluate: device buffers");
   }
-  cudaFree(di);
-  cudaFree(dout);
-  return st;
+  cudaMemcpyAsync(di, idx, (size_t)npts * L, cudaMemcpyHostToDevice, st);
+  int rc = tt_evaluate_device(t, npts, di, dout, st);
+  if (rc == ACI_OK) cudaMemcpyAsync(out, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(di, st);
+  cudaFreeAsync(dout, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (rc == ACI_OK && e != cudaSuccess) rc = fail(ACI_ERR_CUDA, std::string("tt_evaluate: ") + cudaGetErrorString(e));
+  return rc;
 }

@@ -246,8 +246,11 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB)
               y += p;
             }
           }
-          bad |= !isfinite(y);
-          vmax = fmax(vmax, fabs(y));
+          // padded lanes hold f(0) (nonzero for a constant term): never part of s or the NaN check
+          if (row < M && col0 + e < N) {
+            bad |= !isfinite(y);
+            vmax = fmax(vmax, fabs(y));
+          }
           y2[e] = y;
         }
         if (row < M) {
@@ -293,9 +296,9 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB)
             yi += pi;
           }
         }
-        bad |= !isfinite(yr) || !isfinite(yi);
-        vmax = fmax(vmax, __dsqrt_rn(__dadd_rn(__dmul_rn(yr, yr), __dmul_rn(yi, yi))));
-        if (row < M && col0 + 1 < N) {
+        if (row < M && col0 + 1 < N) {  // real entries only (padding holds f(0))
+          bad |= !isfinite(yr) || !isfinite(yi);
+          vmax = fmax(vmax, __dsqrt_rn(__dadd_rn(__dmul_rn(yr, yr), __dmul_rn(yi, yi))));
           double *dst = D.C + (size_t)row * D.ldc + col0;
           dst[0] = yr;
           dst[1] = yi;

@@ -1,0 +1,102 @@
+// libaci_peak.so — FP64 roofline denominators measured in the same process as the bench
+// (measurement infrastructure, not part of the ACI path; MEASURED_PEAKS.json has no FP64 entry).
+//   kind 0: DMMA (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4) register-only loop, 4 x 2 independent
+//           accumulator tiles per warp, 8 warps per CTA, 2 CTAs per SM: the FP64 tensor-pipe peak
+//           the contraction kernels (a1-a4) are held against;
+//   kind 1: DFMA register-only loop (8 independent chains per thread): the FP64 ALU peak the
+//           prrLU's rank-1 updates (a5) are held against.
+// Each launch covers every SM (148 x 2 CTAs); the result is the best of `reps` CUDA-event-timed
+// launches after one warm-up launch, in TFLOP/s (2 flops per FMA).
+#include <cuda_runtime.h>
+
+namespace {
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+constexpr int kMI = 4, kNI = 2, kKS = 4;
+
+__global__ void __launch_bounds__(256) dmma_loop(double *out, int iters) {
+  double acc[kMI][kNI][2] = {};
+  double a[kKS][kMI], b[kKS][kNI];
+  for (int k = 0; k < kKS; ++k) {
+    for (int i = 0; i < kMI; ++i) a[k][i] = 1e-3 * (threadIdx.x + i + k);
+    for (int j = 0; j < kNI; ++j) b[k][j] = 1e-3 * (blockIdx.x + j + k);
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < kKS; ++k)
+#pragma unroll
+      for (int i = 0; i < kMI; ++i)
+#pragma unroll
+        for (int j = 0; j < kNI; ++j) dmma(acc[i][j], a[k][i], b[k][j]);
+  }
+  double s = 0;
+  for (int i = 0; i < kMI; ++i)
+    for (int j = 0; j < kNI; ++j) s += acc[i][j][0] + acc[i][j][1];
+  if (s == 12345.0) out[0] = s;  // keeps the loop; never true
+}
+
+constexpr int kChains = 8;
+
+__global__ void __launch_bounds__(256) dfma_loop(double *out, int iters) {
+  double x[kChains];
+  const double y = 1.0 + 1e-9 * threadIdx.x, z = 1e-12 * blockIdx.x;
+  for (int c = 0; c < kChains; ++c) x[c] = 1e-3 * (threadIdx.x + c);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int c = 0; c < kChains; ++c) x[c] = fma(x[c], y, z);
+  }
+  double s = 0;
+  for (int c = 0; c < kChains; ++c) s += x[c];
+  if (s == 12345.0) out[0] = s;
+}
+
+}  // namespace
+
+extern "C" int aci_peak_fp64(int kind, int reps, double *tflops) {
+  if (!tflops || (kind != 0 && kind != 1)) return -1;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -5;
+  double *out = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess || cudaMallocAsync(&out, 64, st) != cudaSuccess ||
+      cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
+    return -5;
+  const int grid = 2 * sms, threads = 256;
+  const int iters = kind == 0 ? 4000 : 20000;
+  // flops per launch: DMMA 8x8x4 = 256 FMA per warp instruction; DFMA 1 FMA per thread
+  const double fl = kind == 0 ? 2.0 * 256 * kMI * kNI * kKS * (double)iters * (threads / 32) * grid
+                              : 2.0 * 8 * kChains * (double)iters * threads * grid;
+  auto launch = [&](int it) {
+    if (kind == 0) dmma_loop<<<grid, threads, 0, st>>>(out, it);
+    else dfma_loop<<<grid, threads, 0, st>>>(out, it);
+  };
+  launch(iters);
+  double best = 0.0;
+  for (int r = 0; r < (reps > 0 ? reps : 5); ++r) {
+    cudaEventRecord(e0, st);
+    launch(iters);
+    cudaEventRecord(e1, st);
+    if (cudaEventSynchronize(e1) != cudaSuccess) break;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms > 0.f && fl / (ms * 1e9) > best) best = fl / (ms * 1e9);
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(out, st);
+  cudaStreamSynchronize(st);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(st);
+  if (e != cudaSuccess) return -5;
+  *tflops = best;
+  return 0;
+}

@@ -110,8 +110,12 @@ def test_cfg1_vs_oracle_and_exact(aci):
     assert _pivot_agreement(ex, ref) == len(ref.log)
 
 
-def test_cfg3_chi64_vs_oracle(aci):
-    cf = make_config(3, 64, npts=20_000)
+@pytest.mark.parametrize("chi", [64, 128])
+def test_cfg3_vs_oracle(aci, chi):
+    """configs[3] at chi = 64 and 128 (two points of the metric's chi sweep, B:2, B:10): identical
+    ordered pivots on every update, <= 10 tol on 10^5 seeded samples against the oracle and the
+    exact product, Frobenius against the oracle's output."""
+    cf = make_config(3, chi, npts=100_000)
     out, st, rep, ex, ref = _run_both(aci, cf)
     s = cf["samples"]
     y = out.evaluate(s)
@@ -119,7 +123,8 @@ def test_cfg3_chi64_vs_oracle(aci):
     assert _rel(y, oracle.tt_evaluate(ref.cores, s)) <= 10 * cf["tol"]
     assert _rel(y, exact) <= 10 * cf["tol"]
     assert _frob_rel(out.cores(), ref.cores) <= 10 * cf["tol"]
-    assert max(out.shape()[1]) == 128
+    assert max(out.shape()[1]) == 2 * chi
+    assert (rep["iterations"], rep["converged"]) == (ref.report["iterations"], ref.report["converged"])
     agree = _pivot_agreement(ex, ref)
     assert agree == len(ref.log), f"pivots identical for {agree}/{len(ref.log)} updates"
 
@@ -258,12 +263,16 @@ def test_cfg2_psi_cubed(aci):
     assert agree == len(ref.log), f"pivots identical for {agree}/{len(ref.log)} updates"
 
 
-def test_cfg4_planewave_two_iterations(aci):
-    """configs[4] (f = ab + a^2, d = 4, 1024 x 1024 blocks, rank cap 256), bounded to two
-    iterations for the oracle: identical pivots and agreement on 10^5 samples. The exact-error
-    floor of the rank-capped output is reported, not gated."""
+@pytest.mark.slow
+def test_cfg4_planewave_all_iterations(aci):
+    """configs[4] (f = ab + a^2, d = 4, 1024 x 1024 blocks, rank cap 256) at all 8 iterations the
+    bench runs (the oracle takes minutes): identical pivots on every update and agreement on 10^5
+    samples and in the Frobenius norm. The exact-error floor of the rank-capped output is
+    reported, not gated."""
     cf = make_config(4, npts=100_000)
-    out, st, rep, ex, ref = _run_both(aci, cf, sweeps=2)
+    assert cf["max_sweeps"] == 8
+    out, st, rep, ex, ref = _run_both(aci, cf)
+    assert len(ex["log"]) == len(ref.log) == 8 * 2 * 19
     s = cf["samples"]
     y = out.evaluate(s)
     yo = oracle.tt_evaluate(ref.cores, s)
@@ -276,8 +285,8 @@ def test_cfg4_planewave_two_iterations(aci):
 
 def test_cfg3_chi256_full_size(aci):
     """configs[3] at chi = 256 in the bench's configuration (4 iterations, ranks reach 2 chi):
-    GPU vs oracle on 10^4 sampled outputs and vs the exact Kronecker product (rank 512)."""
-    cf = make_config(3, 256, npts=10_000)
+    GPU vs oracle on 10^5 sampled outputs and vs the exact Kronecker product (rank 512)."""
+    cf = make_config(3, 256, npts=100_000)
     out, st, rep, ex, ref = _run_both(aci, cf)
     s = cf["samples"]
     y = out.evaluate(s)
@@ -545,3 +554,66 @@ def test_batch_api_matches_single_products(aci):
     bad = dict(jobs[0], tol=-1.0)
     with pytest.raises(aci.AciError):
         aci.aci_elementwise_batch([jobs[0], bad])
+
+
+def test_concurrent_and_batch_paths_match_oracle_pivots(aci):
+    """The concurrent path (aci_options.concurrent, single-cluster prrLU tiers) and the batch API
+    compared with the ORACLE itself: identical ordered pivot lists on every update, and outputs
+    within 10 tol of the oracle's, for configs[3] chi = 64 and configs[1]."""
+    cfgs = [make_config(3, 64, npts=20_000), make_config(1, npts=20_000)]
+    refs = [oracle.aci(cf["inputs"], cf["op"], cf["y_init"], cf["tol"], cf["maxrank"], cf["max_sweeps"]) for cf in cfgs]
+    jobs = []
+    for cf, ref in zip(cfgs, refs):
+        xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+        y0 = aci.TensorTrain.from_cores(cf["y_init"])
+        out, st, rep, ex = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0,
+                                               log=True, concurrent=True)
+        assert _pivot_agreement(ex, ref) == len(ref.log) == len(ex["log"])
+        s = cf["samples"]
+        assert _rel(out.evaluate(s), oracle.tt_evaluate(ref.cores, s)) <= 10 * cf["tol"]
+        jobs.append({"op": cf["op"], "inputs": xs, "tol": cf["tol"], "maxrank": cf["maxrank"],
+                     "max_sweeps": cf["max_sweeps"], "y_init": y0, "log": True})
+    res = aci.aci_elementwise_batch(jobs + jobs, max_parallel=4)
+    for i, (tt, st, rep, ex) in enumerate(res):
+        cf, ref = cfgs[i % 2], refs[i % 2]
+        assert _pivot_agreement(ex, ref) == len(ref.log) == len(ex["log"]), i
+        assert _rel(tt.evaluate(cf["samples"]), oracle.tt_evaluate(ref.cores, cf["samples"])) <= 10 * cf["tol"]
+
+
+def test_constant_term_op_vs_oracle(aci):
+    """f = 1 - a^2 b^2 (a constant term): every real entry of Pi is < 1, while padded
+    tile lanes of the Pi epilogue hold f(0) = 1, which must not enter s = max |Pi| (R1) —
+    identical pivots and scale to the oracle's."""
+    rng = np.random.default_rng(31)
+    for L, chi in [(9, 3), (12, 6)]:
+        xs = [G.random_tt(L, 2, chi, rng), G.random_tt(L, 2, 2, rng)]
+        op = {"coef": [1.0, -1.0], "expo": [[0, 0], [2, 2]]}
+        y0 = G.random_init(xs, 64, rng)
+        hs = [aci.TensorTrain.from_cores(x) for x in xs]
+        out, st, rep, ex = aci.aci_elementwise(op, hs, 1e-10, 64, 10, y_init=aci.TensorTrain.from_cores(y0), log=True)
+        ref = oracle.aci(xs, op, y0, 1e-10, 64, 10)
+        assert _pivot_agreement(ex, ref) == len(ref.log)
+        for g, o in zip(ex["log"], ref.log):
+            assert g["scale"] == pytest.approx(o["scale"], rel=1e-14)
+        D = [oracle.tt_dense(x) for x in xs]
+        assert _rel(oracle.tt_dense(out.cores()), 1.0 - D[0] ** 2 * D[1] ** 2) <= 1e-9
+
+
+def test_workspace_alignment_and_query_sweeps(aci):
+    """A caller workspace must be 256-byte aligned (ACI_ERR_INVALID otherwise); aci_workspace_query
+    sizes the pivot log for the max_sweeps it is given."""
+    import torch
+    cf = make_config(0, npts=0)
+    xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+    y0 = aci.TensorTrain.from_cores(cf["y_init"])
+    n20 = aci.workspace_query(xs, cf["maxrank"], y0, max_sweeps=20)
+    n80 = aci.workspace_query(xs, cf["maxrank"], y0, max_sweeps=80)
+    assert n80 > n20
+    ws = torch.empty(n80 + 512, dtype=torch.uint8, device="cuda")
+    with pytest.raises(aci.AciError) as e:
+        aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], 20, y_init=y0, workspace=(ws.data_ptr() + 8, n80))
+    assert "INVALID" in str(e.value)
+    out, st, rep, _ = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], 20, y_init=y0,
+                                          workspace=(ws.data_ptr(), n20))
+    ref, *_ = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], 20, y_init=y0)
+    assert all(np.array_equal(a, b) for a, b in zip(out.cores(), ref.cores()))

@@ -295,3 +295,93 @@ def test_aci_cfg3_chi64_saturates_to_exact_product():
     s = cf["samples"]
     ref = oracle.tt_evaluate(cf["inputs"][0], s) * oracle.tt_evaluate(cf["inputs"][1], s)
     assert _rel_max(oracle.tt_evaluate(res.cores, s), ref) <= 10 * cf["tol"]
+
+
+def _generic_rank_model(d, true_ranks, yr, maxrank, maxiter):
+    """Closed-form rank recursion of Alg. 1 on GENERIC data (exact arithmetic), independent of the
+    oracle's code. Canonicalisation: |J_s| = min(r^y_s, d_s |J_{s+1}|, chi-hat,
+    full bound). An update at bond b sees the block Pi of size (d_b |I_{b-1}|) x (d_{b+1} |J_{b+2}|)
+    (Alg. 4) whose rank is generically min(m, n, true rank of the bond); prrLU with a tolerance
+    above roundoff takes exactly that many pivots (capped at chi-hat) and its error eps is ~0 unless
+    the cap binds. So rank at most multiplies by d per half-sweep from the J sets ("rank doubling"
+    for d = 2), and eps alone would stop the loop after iteration 1 — only P:497's clause "the
+    chi_l have not increased" keeps it running. Returns (iterations, converged, final ranks)."""
+    L = len(d)
+
+    def full(b):
+        return min(int(np.prod([float(x) for x in d[:b + 1]])), int(np.prod([float(x) for x in d[b + 1:]])))
+
+    Jn = [0] * (L + 1)
+    Jn[L] = 1
+    for s in range(L - 1, 0, -1):
+        Jn[s] = min(yr[s], d[s] * Jn[s + 1], maxrank, full(s - 1))
+    chi = [Jn[b + 1] for b in range(L - 1)]
+    prev = list(chi)
+    for it in range(1, maxiter + 1):
+        eps_ok = True
+        for bonds in (range(L - 1), range(L - 2, -1, -1)):
+            for b in bonds:
+                rl = 1 if b == 0 else chi[b - 1]
+                rr = 1 if b + 2 == L else Jn[b + 2]
+                rank_pi = min(rl * d[b], d[b + 1] * rr, true_ranks[b])
+                chi[b] = Jn[b + 1] = min(rank_pi, maxrank)
+                eps_ok &= chi[b] == rank_pi
+        grew = any(c > p for c, p in zip(chi, prev))
+        prev = list(chi)
+        if not grew and eps_ok:
+            return it, True, chi
+    return maxiter, False, chi
+
+
+def _product_true_ranks(inputs):
+    """rank(A (.) B) = rank(A) rank(B) for generic inputs (B:5), capped by the full bound."""
+    d = inputs[0].d
+    L = len(d)
+    out = []
+    for b in range(L - 1):
+        full = min(int(np.prod([float(x) for x in d[:b + 1]])), int(np.prod([float(x) for x in d[b + 1:]])))
+        p = 1
+        for t in inputs:
+            p *= min(t.ranks[b + 1], full)
+        out.append(min(p, full))
+    return out
+
+
+@pytest.mark.parametrize("cfg,chi", [(1, 0), (3, 64), (3, 128)])
+def test_aci_convergence_rank_clause_matches_rank_doubling_model(cfg, chi):
+    """P:497 (R10): an iteration converges only if no chi_l grew AND max eps <= tau s. On these
+    generic random-TT products every block is exactly interpolated (eps ~ 1e-16 s) from the first
+    iteration on, so the rank clause alone decides: the oracle's iteration count, flag and final
+    ranks must equal the closed-form rank-doubling model (configs[3]
+    at chi = 64 saturates in half-sweep 6 and converges at iteration 4; at chi = 128 the rank 2 chi
+    is first reached in half-sweep 7, so iteration 4 still grows and the run ends unconverged).
+    Dropping the clause would report convergence at iteration 1."""
+    cf = make_config(cfg, chi, npts=0)
+    d = cf["inputs"][0].d
+    it, conv, ranks = _generic_rank_model(d, _product_true_ranks(cf["inputs"]), cf["y_init"].ranks, cf["maxrank"],
+                                          cf["max_sweeps"])
+    res = oracle.aci(cf["inputs"], cf["op"], cf["y_init"], cf["tol"], cf["maxrank"], cf["max_sweeps"])
+    assert (res.report["iterations"], bool(res.report["converged"])) == (it, conv)
+    assert [res.chi(b) for b in range(len(d) - 1)] == ranks
+    L = len(d)
+    first = res.log[:2 * (L - 1)]
+    assert max(e["eps"] for e in first) <= cf["tol"] * first[-1]["scale"]  # eps alone would stop here
+    if cfg == 3:
+        assert (it, conv) == ((4, True) if chi == 64 else (4, False))
+
+
+def test_aci_convergence_model_small_random_cases():
+    """The same model on small random products (d in {2, 3}, rank caps that bind or not): equal
+    iteration counts, flags and ranks. A binding cap (chi-hat < true rank) leaves eps > tau s, so
+    those runs never converge."""
+    rng = np.random.default_rng(497)
+    for trial in range(12):
+        L = int(rng.integers(4, 9))
+        d = 3 if trial % 3 == 2 else 2
+        xs = [G.random_tt(L, d, int(rng.integers(1, 5)), rng) for _ in range(2)]
+        maxrank = int(rng.integers(3, 10)) if trial % 4 == 1 else 64
+        y0 = G.random_init(xs, maxrank, rng)
+        it, conv, ranks = _generic_rank_model(xs[0].d, _product_true_ranks(xs), y0.ranks, maxrank, 12)
+        res = oracle.aci(xs, {"coef": [1.0], "expo": [[1, 1]]}, y0, 1e-10, maxrank, 12)
+        assert (res.report["iterations"], bool(res.report["converged"])) == (it, conv), trial
+        assert [res.chi(b) for b in range(L - 1)] == ranks, trial

@@ -1050,7 +1050,7 @@ static size_t carve(Run &R, char *base) {
   R.log_cols = c.take<int>((size_t)R.log_cap_upd * R.log_cap_piv);
   R.canon_n = c.take<int>(L + 1);
   R.canon_cols = c.take<int>((size_t)(L + 1) * R.log_cap_piv);
-  R.colpub = c.take<unsigned long long>((size_t)2 * 148 * R.colcap * 2);
+  R.colpub = c.take<unsigned long long>((size_t)2 * 148 * R.colcap * 2 * prrlu_col_spread());
   R.keys = c.take<unsigned long long>(2 * 148 * 4);
   R.epoch = c.take<unsigned>(1);
   R.counter = c.take<unsigned>(1);
@@ -1733,7 +1733,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   cudaMemsetAsync(R.iter, 0, sizeof(int), strm);
   // tags in the exchange buffers must never match stale data: clear them once per call
   cudaMemsetAsync(R.keys, 0, sizeof(unsigned long long) * 2 * 148 * 4, strm);
-  cudaMemsetAsync(R.colpub, 0, sizeof(unsigned long long) * 2 * 148 * R.colcap * 2, strm);
+  cudaMemsetAsync(R.colpub, 0, sizeof(unsigned long long) * 2 * 148 * R.colcap * 2 * prrlu_col_spread(), strm);
   cudaMemsetAsync(R.epoch, 0, sizeof(unsigned), strm);
   for (int s = 0; s < L; ++s)
     cudaMemcpyAsync(R.Yin[s], y->dcores + y->off[s], sizeof(double) * (y->off[s + 1] - y->off[s]),
@@ -1888,7 +1888,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
     std::vector<TrsmArgs> ta(L - 1);
     int nmx = 1, nsteps = 0;
     for (int b = 0; b < L - 1; ++b) {
-      ta[b].U = R.Ust[b]; ta[b].ldu = R.nmax[b]; ta[b].cols = R.pcol[L + b];  // the last R->L half-sweep's pivots ta[b].b = b; ta[b].d1 = R.d[b + 1];
+      ta[b].U = R.Ust[b]; ta[b].ldu = R.nmax[b]; ta[b].cols = R.pcol[L + b]; ta[b].b = b; ta[b].d1 = R.d[b + 1];  // last R->L pivots
       ta[b].UJ = R.UJ[b]; ta[b].ldj = R.rmax[b];
       ta[b].out = res->dcores + res->off[b + 1];
       nmx = std::max(nmx, R.d[b + 1] * rk[b + 2]);

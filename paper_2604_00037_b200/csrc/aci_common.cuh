@@ -53,7 +53,7 @@ struct LuArgs {
   double *U;                  // optional U rows out (r x n, ld = dims->ldu), U_k = S_k[p,:]/c
   // grid tier exchange: every published word carries a tag (epoch << 12 | step + 1) in its
   // upper 32 bits, so readers validate data without release/acquire fences
-  unsigned long long *colpub; // 2 x G x colcap x 2 words: (tag|lo32, tag|hi32) per element
+  unsigned long long *colpub; // 2 x G x colcap x 2 x prrlu_col_spread() words: (tag|lo32, tag|hi32) per element
   int colcap;
   unsigned long long *keys;   // 2 x G x 4 words: tag|hi, tag|lo, tag|id, pad
   unsigned int *counter;      // zeroed before launch
@@ -91,3 +91,5 @@ bool prrlu_supported_one(int m, int n, bool cplx);
 // Chooses the prrLU exchange tier (cluster size) once; call before any stream capture.
 void prrlu_init();
 void prrlu_envelope(int *max_rows, int *max_cols);
+// Column-slot stride factor of the exchange buffer: a slot holds colcap * 2 * factor u64 words.
+int prrlu_col_spread();

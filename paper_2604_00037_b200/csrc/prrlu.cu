@@ -189,6 +189,13 @@ __device__ __forceinline__ double key_abs(const Key &k) {
   return __longlong_as_double((long long)(((unsigned long long)k.hi << 32) | k.lo));
 }
 
+// Paired shared-memory layout of per-row values (l_i, the raw pivot column): row i = lane + 32 a
+// sits at (a / 2) * 64 + 2 lane + a % 2, so a thread reads the values of its rows a and a + 1 with
+// one LDS.128 (a warp reads 512 contiguous bytes: conflict-free), and the rank-1 update keeps
+// several pairs in flight instead of a LDS -> DFMA -> LDS chain through one register (the SASS of
+// the previous layout reloaded every l_i into the same register pair).
+__device__ __forceinline__ int lpair(int i) { return ((i >> 6) << 6) | ((i & 31) << 1) | ((i >> 5) & 1); }
+
 // columns per warp of the 8-warp grid tiers, measured (tools/prrlu_bench.cu): 16 CTAs with the
 // key-poll barrier beat more CTAs with the counter barrier up to 512 rows
 #ifndef ACI_W8_EB128
@@ -202,6 +209,27 @@ __device__ __forceinline__ double key_abs(const Key &k) {
 #endif
 #ifndef ACI_BIG_EB
 #define ACI_BIG_EB 2  // columns per warp for the 1024-row grid tier (64 CTAs for 1024 columns)
+#endif
+#ifndef ACI_SCAN_CHAINS
+#define ACI_SCAN_CHAINS 4  // independent max chains per thread in the candidate scan
+#endif
+#ifndef ACI_SCAN_DMNMX
+#define ACI_SCAN_DMNMX 0
+#endif
+#ifndef ACI_COL_SPREAD
+#define ACI_COL_SPREAD 0  // 1: one 128-byte line of column packets per 1 KB (spreads a column over L2 slices)
+#endif
+#ifndef ACI_PUB_WINNER
+#define ACI_PUB_WINNER 0  // 1: several-cluster grids publish only the cluster winners' columns
+#endif
+constexpr int kColSpread = ACI_COL_SPREAD ? 8 : 1;
+// u64 offset of packet i (two u64 words per element) within a CTA's column slot
+__device__ __forceinline__ int cpk(int i) { return ACI_COL_SPREAD ? (((i >> 3) << 7) | ((i & 7) << 1)) : 2 * i; }
+#ifndef ACI_LPAIR_PD
+#define ACI_LPAIR_PD 4  // l_i pairs loaded per group in the rank-1 update
+#endif
+#ifndef ACI_LPAIR
+#define ACI_LPAIR 1  // paired l_i layout + prefetched rank-1 update (lpair); 0 = one LDS per row
 #endif
 constexpr int kMaxRows = 1024;   // 32 * EA_max
 constexpr int kMaxCTAs = 148;
@@ -277,7 +305,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   int be = 0;
   auto scan = [&]() {
     constexpr int NE = EA * EB;
-    constexpr int NCH = NE < 4 ? NE : 4;
+    constexpr int NCH = NE < ACI_SCAN_CHAINS ? NE : ACI_SCAN_CHAINS;
     // chains keep the SIGNED value and compare magnitudes (|.| operand modifiers of DSETP), so
     // no FP64-pipe instruction is spent materialising |v|
     double cx[NCH];
@@ -287,6 +315,19 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       const double *x = v[e / EB][e % EB];
       return CPLX ? __dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[Z - 1], x[Z - 1])) : x[0];
     };
+#if ACI_SCAN_DMNMX
+    // chains hold |x|: DMNMX for the value, DSETP against the old max for the slot (3 instructions
+    // per entry instead of DSETP + 2 FSEL + SEL)
+#pragma unroll
+    for (int t = 0; t < NCH; ++t) { cx[t] = fabs(mag(t)); ce[t] = t; }
+#pragma unroll
+    for (int e = NCH; e < NE; ++e) {
+      const double x = mag(e);
+      const bool take = fabs(x) > cx[e % NCH];
+      cx[e % NCH] = fmax(cx[e % NCH], fabs(x));
+      ce[e % NCH] = take ? e : ce[e % NCH];
+    }
+#else
 #pragma unroll
     for (int t = 0; t < NCH; ++t) { cx[t] = mag(t); ce[t] = t; }
 #pragma unroll
@@ -296,6 +337,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       cx[e % NCH] = take ? x : cx[e % NCH];
       ce[e % NCH] = take ? e : ce[e % NCH];
     }
+#endif
     double bm = cx[0];
     int bi = ce[0];
 #pragma unroll
@@ -312,6 +354,47 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     const int a = be / EB, b = be % EB;
     const unsigned flat = (unsigned)(lane + 32 * a) * NC + (unsigned)(c0 + w + NW * b);
     return Key{(unsigned)(bits >> 32), (unsigned)bits, flat};
+  };
+  // v[a][b] = fma(mul(a, r_a), ub[b], v[a][b]) for this thread's rows, with r_a the per-row value
+  // (l_i or the raw column entry) read from `base` in the lpair layout, several LDS.128 in flight
+  auto rank1_update = [&](const double *base, const double (&ub)[EB], auto mul) {
+#if ACI_LPAIR
+    // groups of PD pairs: the group's LDS.128 are issued back to back and pinned (the empty asm
+    // needs every value), so one shared-memory latency covers 4 * EB DFMAs per pair; ptxas would
+    // otherwise reload every pair into one register quad right before its DFMAs
+    constexpr int NP = (EA + 1) / 2;
+    constexpr int PD = NP < ACI_LPAIR_PD ? NP : ACI_LPAIR_PD;
+#pragma unroll
+    for (int g = 0; g < NP; g += PD) {
+      double2 c[PD];
+#pragma unroll
+      for (int j = 0; j < PD; ++j)
+        if (g + j < NP) c[j] = *reinterpret_cast<const double2 *>(base + (g + j) * 64 + 2 * lane);
+#pragma unroll
+      for (int j = 0; j < PD; ++j)
+        if (g + j < NP) asm volatile("" : "+d"(c[j].x), "+d"(c[j].y));
+#pragma unroll
+      for (int j = 0; j < PD; ++j) {
+        if (g + j >= NP) continue;
+        const int a0 = 2 * (g + j), a1 = a0 + 1 < EA ? a0 + 1 : a0;
+        const double m0 = mul(a0, c[j].x);
+#pragma unroll
+        for (int b = 0; b < EB; ++b) v[a0][b][0] = fma(m0, ub[b], v[a0][b][0]);
+        if (a0 + 1 < EA) {
+          const double m1 = mul(a1, c[j].y);
+#pragma unroll
+          for (int b = 0; b < EB; ++b) v[a1][b][0] = fma(m1, ub[b], v[a1][b][0]);
+        }
+      }
+    }
+#else
+#pragma unroll
+    for (int a = 0; a < EA; ++a) {
+      const double ma = mul(a, base[lpair(lane + 32 * a)]);
+#pragma unroll
+      for (int b = 0; b < EB; ++b) v[a][b][0] = fma(ma, ub[b], v[a][b][0]);
+    }
+#endif
   };
   scan();
   if constexpr (XM == 3) {
@@ -372,7 +455,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         for (int b = 0; b < EB; ++b)
           if (b == bc)
 #pragma unroll
-            for (int a = 0; a < EA; ++a) stg[lane + 32 * a] = v[a][b][0];
+            for (int a = 0; a < EA; ++a) stg[lpair(lane + 32 * a)] = v[a][b][0];
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane < (int)CS) {
@@ -405,9 +488,9 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
           st_async_key(mapa_u32(smem_u32(&S.ck[par][cluster_rank()]), (unsigned)lane), ck.hi, ck.lo, ck.id,
                        mapa_u32(smem_u32(&S.mb[par]), (unsigned)lane));
       }
-      if (w == pw) {
+      auto publish_col = [&]() {
         const int bc = jc / NW;
-        unsigned long long *dst = A.colpub + (((size_t)par * G + g) * A.colcap) * 2;
+        unsigned long long *dst = A.colpub + (((size_t)par * G + g) * A.colcap) * 2 * kColSpread;
 #pragma unroll
         for (int b = 0; b < EB; ++b)
           if (b == bc)
@@ -417,9 +500,13 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
 #pragma unroll
                 for (int z = 0; z < Z; ++z) {
                   const unsigned long long bits = (unsigned long long)__double_as_longlong(v[a][b][z]);
-                  st_pkt(dst + 2 * (Z * (lane + 32 * a) + z), tagged(tag, (unsigned)bits),
+                  st_pkt(dst + cpk(Z * (lane + 32 * a) + z), tagged(tag, (unsigned)bits),
                          tagged(tag, (unsigned)(bits >> 32)));
                 }
+      };
+      const bool late_pub = ACI_PUB_WINNER && XM == 2 && G > (int)cluster_size();
+      if (w == pw) {
+        if (!late_pub) publish_col();
         if (XM == 1 && lane == 0) {
           unsigned long long *kd = A.keys + ((size_t)par * G + g) * 4;
           st_pkt(kd, tagged(tag, ck.hi), tagged(tag, ck.lo));
@@ -438,6 +525,8 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         const uint4 q4 = S.ck[par][lane < (int)CS ? lane : 0];
         const Key cw = warp_argmax(lane < (int)CS ? Key{q4.x, q4.y, q4.z} : Key{0u, 0u, BAD_ID});
         const int NCL = G / (int)CS;
+        // late publication: only the cluster winner's column goes to L2 (its candidate is ck)
+        if (late_pub && w == pw && (int)((cw.id % NC) / CB) == g) publish_col();
         if (NCL == 1) {
           win = cw;
         } else {
@@ -591,7 +680,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     if constexpr (XM == 3) {
       // the winner's column is already in this CTA's shared memory (pushed with its key)
       const double *col = push_dyn + ((size_t)(k & 1) * kPushCS + q / CB) * kPushRows;
-      const bool neg = col[p] < 0.0;
+      const bool neg = col[lpair(p)] < 0.0;
       inv = neg ? -inv_abs : inv_abs;
       __syncthreads();  // S3: pivot row in smem
       PHASE(5);
@@ -602,26 +691,24 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         }
 #pragma unroll
       for (int b = 0; b < EB; ++b) ub[b] = s_u[w + NW * b];
-#pragma unroll
-      for (int a = 0; a < EA; ++a) {
+      // multiplier -l_i (exact negation: fma(-l_i, u, v) as R4); padding rows hold 0
+      rank1_update(col, ub, [&](int a, double r) -> double {
         const int i = lane + 32 * a;
-        const double li = i < m ? ((i == p) ? 1.0 : col[i] * inv) : 0.0;
-#pragma unroll
-        for (int b = 0; b < EB; ++b) v[a][b][0] = fma(-li, ub[b], v[a][b][0]);
-      }
+        return -(i < m ? ((i == p) ? 1.0 : r * inv) : 0.0);
+      });
     } else if (GRID) {
       const unsigned tag = (ep << 12) | (unsigned)(k + 1);
-      const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2;
+      const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2 * kColSpread;
       constexpr int PPT = (MROWS + T - 1) / T;  // column packets per thread
       unsigned long long cw[PPT + 1][2];
 #pragma unroll
       for (int t = 0; t < PPT; ++t) {
         const int i = tid + T * t;
-        if (i < m) ld_pkt(src + 2 * i, cw[t][0], cw[t][1]);
+        if (i < m) ld_pkt(src + cpk(i), cw[t][0], cw[t][1]);
       }
-      ld_pkt(src + 2 * p, cw[PPT][0], cw[PPT][1]);  // the pivot itself, for its sign
+      ld_pkt(src + cpk(p), cw[PPT][0], cw[PPT][1]);  // the pivot itself, for its sign
       while ((unsigned)(cw[PPT][0] >> 32) != tag || (unsigned)(cw[PPT][1] >> 32) != tag)
-        ld_pkt(src + 2 * p, cw[PPT][0], cw[PPT][1]);
+        ld_pkt(src + cpk(p), cw[PPT][0], cw[PPT][1]);
       const bool neg = (cw[PPT][1] & 0x80000000ull) != 0;
       inv = neg ? -inv_abs : inv_abs;
 #pragma unroll
@@ -629,8 +716,8 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         const int i = tid + T * t;
         if (i < m) {
           while ((unsigned)(cw[t][0] >> 32) != tag || (unsigned)(cw[t][1] >> 32) != tag)
-            ld_pkt(src + 2 * i, cw[t][0], cw[t][1]);
-          s_l[i] = (i == p) ? 1.0 : pkt_double(cw[t][0], cw[t][1]) * inv;
+            ld_pkt(src + cpk(i), cw[t][0], cw[t][1]);
+          s_l[lpair(i)] = (i == p) ? 1.0 : pkt_double(cw[t][0], cw[t][1]) * inv;
         }
       }
       __syncthreads();  // S3
@@ -642,12 +729,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         }
 #pragma unroll
       for (int b = 0; b < EB; ++b) ub[b] = s_u[w + NW * b];
-#pragma unroll
-      for (int a = 0; a < EA; ++a) {
-        const double li = s_l[lane + 32 * a];
-#pragma unroll
-        for (int b = 0; b < EB; ++b) v[a][b][0] = fma(-li, ub[b], v[a][b][0]);
-      }
+      rank1_update(s_l, ub, [](int, double l) -> double { return -l; });  // fma(-l_i, u_j, S_ij) (R4)
     } else {
       const int jq = q - c0;
       if ((jq % NW) == w) {
@@ -656,10 +738,10 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         for (int b = 0; b < EB; ++b)
           if (b == bq)
 #pragma unroll
-            for (int a = 0; a < EA; ++a) s_raw[lane + 32 * a] = v[a][b][0];
+            for (int a = 0; a < EA; ++a) s_raw[lpair(lane + 32 * a)] = v[a][b][0];
       }
       __syncthreads();  // S2 (CTA tier): raw pivot column and pivot row in smem
-      const bool neg = s_raw[p] < 0.0;
+      const bool neg = s_raw[lpair(p)] < 0.0;
       inv = neg ? -inv_abs : inv_abs;
 #pragma unroll
       for (int b = 0; b < EB; ++b) ub[b] = neg ? s_u[w + NW * b] : -s_u[w + NW * b];
@@ -670,20 +752,16 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
           if (j < n) A.U[(size_t)k * ldu + j] = (j == q) ? 1.0 : s_u[jj] * inv;
         }
       // every thread forms its own l'_i (no third barrier)
-#pragma unroll
-      for (int a = 0; a < EA; ++a) {
-        const int i = lane + 32 * a;
-        const double li = (i == p) ? (neg ? -1.0 : 1.0) : s_raw[i] * inv_abs;
-#pragma unroll
-        for (int b = 0; b < EB; ++b) v[a][b][0] = fma(li, ub[b], v[a][b][0]);
-      }
+      rank1_update(s_raw, ub, [&](int a, double r) -> double {
+        return (lane + 32 * a == p) ? (neg ? -1.0 : 1.0) : r * inv_abs;
+      });
     }
     } else {
     // ---- complex (RZ2-RZ4): inv = conj(c) / w with w the key's |c|^2
     double cr, ci;
     if (GRID) {
       const unsigned tag = (ep << 12) | (unsigned)(k + 1);
-      const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2;
+      const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2 * kColSpread;
       constexpr int PPT = (MROWS + T - 1) / T;  // column entries per thread (2 packets each)
       unsigned long long cw[PPT + 1][2][2];
 #pragma unroll
@@ -691,13 +769,13 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         const int i = tid + T * t;
         if (i < m)
 #pragma unroll
-          for (int z = 0; z < 2; ++z) ld_pkt(src + 2 * (2 * i + z), cw[t][z][0], cw[t][z][1]);
+          for (int z = 0; z < 2; ++z) ld_pkt(src + cpk(2 * i + z), cw[t][z][0], cw[t][z][1]);
       }
 #pragma unroll
       for (int z = 0; z < 2; ++z) {
-        ld_pkt(src + 2 * (2 * p + z), cw[PPT][z][0], cw[PPT][z][1]);
+        ld_pkt(src + cpk(2 * p + z), cw[PPT][z][0], cw[PPT][z][1]);
         while ((unsigned)(cw[PPT][z][0] >> 32) != tag || (unsigned)(cw[PPT][z][1] >> 32) != tag)
-          ld_pkt(src + 2 * (2 * p + z), cw[PPT][z][0], cw[PPT][z][1]);
+          ld_pkt(src + cpk(2 * p + z), cw[PPT][z][0], cw[PPT][z][1]);
       }
       cr = pkt_double(cw[PPT][0][0], cw[PPT][0][1]);
       ci = pkt_double(cw[PPT][1][0], cw[PPT][1][1]);
@@ -709,7 +787,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
 #pragma unroll
           for (int z = 0; z < 2; ++z)
             while ((unsigned)(cw[t][z][0] >> 32) != tag || (unsigned)(cw[t][z][1] >> 32) != tag)
-              ld_pkt(src + 2 * (2 * i + z), cw[t][z][0], cw[t][z][1]);
+              ld_pkt(src + cpk(2 * i + z), cw[t][z][0], cw[t][z][1]);
           const double xr = pkt_double(cw[t][0][0], cw[t][0][1]), xi = pkt_double(cw[t][1][0], cw[t][1][1]);
           double lr = 1.0, li = 0.0;
           if (i != p) {  // RZ3
@@ -1045,6 +1123,8 @@ void prrlu_envelope(int *max_rows, int *max_cols) {
   *max_rows = kMaxRows;
   *max_cols = kMaxCTAs * 8;
 }
+
+int prrlu_col_spread() { return kColSpread; }
 
 size_t prrlu_exchange_bytes(int max_m, int max_n) {
   (void)max_n;

@@ -24,8 +24,8 @@ int main(int argc, char **argv) {
   long long *ddbg;
   cudaMalloc(&dM, sizeof(double) * 1024 * 1024);
   cudaMalloc(&dU, sizeof(double) * 1024 * 1024);
-  cudaMalloc(&dcol, 16 * 2 * 148 * 1024);
-  cudaMemset(dcol, 0, 16 * 2 * 148 * 1024);
+  cudaMalloc(&dcol, (size_t)16 * 2 * 148 * 1024 * kColSpread);
+  cudaMemset(dcol, 0, (size_t)16 * 2 * 148 * 1024 * kColSpread);
   cudaMalloc(&depoch, 4);
   cudaMemset(depoch, 0, 4);
   cudaMalloc(&deps, 8);
@@ -87,10 +87,16 @@ int main(int argc, char **argv) {
       cudaMemcpy(&r, dr, 4, cudaMemcpyDeviceToHost);
       cudaMemcpy(dbg, ddbg, 64, cudaMemcpyDeviceToHost);
       if (rep == 2) {
+        // FNV-1a over the ordered pivots: variants must take identical decisions
+        std::vector<int> hr(r), hc(r);
+        cudaMemcpy(hr.data(), drows, 4 * r, cudaMemcpyDeviceToHost);
+        cudaMemcpy(hc.data(), dcols, 4 * r, cudaMemcpyDeviceToHost);
+        unsigned long long hsh = 1469598103934665603ull;
+        for (int t = 0; t < r; ++t) hsh = (hsh ^ (unsigned)(hr[t] * 4099 + hc[t])) * 1099511628211ull;
         printf("%4dx%4d (static %4d) r=%4d: %8.1f us total, %6.3f us/pivot | cycles/pivot:", m, n, stat, r, ms * 1e3,
                ms * 1e3 / r);
         for (int t = 0; t < 7; ++t) printf(" p%d=%lld", t, dbg[t] / (r > 0 ? r : 1));
-        printf("\n");
+        printf(" | piv %016llx\n", hsh);
       }
     }
   }

@@ -78,6 +78,10 @@ def _load():
         lib.oracle_Rframe.argtypes = [vp, C.c_int, C.c_int, dp]
         lib.oracle_ldu.argtypes = [C.c_int, C.c_int, dp, C.c_double, C.c_int, C.c_int, ip, ip, ip, dp, dp, dp,
                                    C.c_int, dp]
+        lib.oracle_ldu_p.argtypes = [C.c_int, C.c_int, dp, C.c_double, C.c_int, C.c_int, C.c_int, ip, ip, ip, dp,
+                                     dp, dp, C.c_int, dp]
+        lib.oracle_aci_p.restype = vp
+        lib.oracle_aci_p.argtypes = lib.oracle_aci.argtypes[:-1] + [C.c_int, ip]
         lib.oracle_ci_right.argtypes = [C.c_int, C.c_int, dp, C.c_double, C.c_int, C.c_int, ip, ip, ip, dp, dp,
                                         C.c_int, dp]
         lib.oracle_assemble_pi.argtypes = [C.c_int, ip, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(dp),
@@ -114,8 +118,12 @@ def _cores_of(x):
 # --------------------------------------------------------------------------
 # Alg. 2 / Alg. 3 / Eq. pifromframes (pin-test entry points)
 # --------------------------------------------------------------------------
-def ldu(M, thr: float, maxrank: int, relative_to_own_max: bool = False) -> dict:
-    """Alg. 2 with R2-R4/R17. Returns rows, cols, D, U (r x n), L (m x r), eps."""
+PIVOTING = {"full": 0, "rook": 1}
+
+
+def ldu(M, thr: float, maxrank: int, relative_to_own_max: bool = False, pivoting: str = "full") -> dict:
+    """Alg. 2 (P:504-545) with R2-R4/R17; pivoting "full" (P:529) or "rook" (R23, NEXT-4).
+    Returns rows, cols, D, U (r x n), L (m x r), eps."""
     lib = _load()
     M = np.ascontiguousarray(M, dtype=np.float64)
     m, n = M.shape
@@ -127,8 +135,8 @@ def ldu(M, thr: float, maxrank: int, relative_to_own_max: bool = False) -> dict:
     D = np.zeros(maxr)
     U = np.zeros((maxr, n))
     Lc = np.zeros((m, maxr))
-    st = lib.oracle_ldu(m, n, _dptr(M), thr, 1 if relative_to_own_max else 0, maxrank, C.byref(r), _iptr(rows),
-                        _iptr(cols), _dptr(D), _dptr(U), _dptr(Lc), maxr, C.byref(eps))
+    st = lib.oracle_ldu_p(m, n, _dptr(M), thr, 1 if relative_to_own_max else 0, maxrank, PIVOTING[pivoting],
+                          C.byref(r), _iptr(rows), _iptr(cols), _dptr(D), _dptr(U), _dptr(Lc), maxr, C.byref(eps))
     if st != 0:
         raise ValueError(f"oracle_ldu: {STATUS.get(st, st)}")
     k = r.value
@@ -276,8 +284,9 @@ class AciResult:
             pass
 
 
-def aci(inputs, op, y_init, tol, maxrank, max_sweeps, relative=True) -> AciResult:
-    """Run Alg. 1. ``inputs`` are distinct TTs; ``op`` = {coef, expo} over them."""
+def aci(inputs, op, y_init, tol, maxrank, max_sweeps, relative=True, pivoting="full") -> AciResult:
+    """Run Alg. 1 (P:402-502). ``inputs`` are distinct TTs; ``op`` = {coef, expo} over them;
+    ``pivoting`` "full" or "rook" (R23) for every prrLU of the run."""
     lib = _load()
     ins = [_cores_of(x) for x in inputs]
     N = len(ins)
@@ -302,8 +311,9 @@ def aci(inputs, op, y_init, tol, maxrank, max_sweeps, relative=True) -> AciResul
     expo = np.ascontiguousarray(op["expo"], dtype=np.int32)
     dd = np.array(d, np.int32)
     st = C.c_int()
-    h = lib.oracle_aci(L, _iptr(dd), N, _iptr(xr), cp, len(coef), _dptr(coef), _iptr(expo), _iptr(yr), yp,
-                       float(tol), 0 if relative else 1, int(maxrank), int(max_sweeps), C.byref(st))
+    h = lib.oracle_aci_p(L, _iptr(dd), N, _iptr(xr), cp, len(coef), _dptr(coef), _iptr(expo), _iptr(yr), yp,
+                         float(tol), 0 if relative else 1, int(maxrank), int(max_sweeps), PIVOTING[pivoting],
+                         C.byref(st))
     if not h:
         raise ValueError(f"oracle_aci: {STATUS.get(st.value, st.value)}")
     return AciResult(h, L, N, d, [list(map(int, r)) for r in xr])

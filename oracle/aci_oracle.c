@@ -79,7 +79,51 @@ static void ldu_free(ldu_t *f) {
  * thr_mode: 0 = absolute thr; 1 = thr * |first candidate| (relative to own max, R8).
  * Returns ORC_ERR_NONFINITE if M contains NaN/Inf.
  */
+/*
+ * Rook pivot search (SURVEY 8(f) NEXT-4, B:5 "full/rook"; reading R23 of DESIGN.md §2 — the paper
+ * only uses full pivoting, and does not define rook). Textbook rook pivoting (Neal & Poole):
+ * start at the smallest active column c; r = argmax over active rows of |S[i][c]|; then alternate
+ * row and column maxima until an entry is the largest in both its row and its column. Ties go to
+ * the smallest index (R3); an alternation stops as soon as the new extremum does not exceed the
+ * current entry, so the accepted (p, q) is maximal in its active row AND its active column.
+ */
+static int col_argmax(int m, int n, const double *S, const char *rowdone, int c) {
+  int r = -1;
+  double best = -1.0;
+  for (int i = 0; i < m; ++i)
+    if (!rowdone[i] && fabs(S[(size_t)i * n + c]) > best) { best = fabs(S[(size_t)i * n + c]); r = i; }
+  return r;
+}
+static int row_argmax(int n, const double *S, const char *coldone, int r) {
+  int c = -1;
+  double best = -1.0;
+  for (int j = 0; j < n; ++j)
+    if (!coldone[j] && fabs(S[(size_t)r * n + j]) > best) { best = fabs(S[(size_t)r * n + j]); c = j; }
+  return c;
+}
+static void rook_search(int m, int n, const double *S, const char *rowdone, const char *coldone, int *pp, int *pq) {
+  int c = 0;
+  while (coldone[c]) ++c;
+  int r = col_argmax(m, n, S, rowdone, c);
+  for (;;) {
+    int c2 = row_argmax(n, S, coldone, r);
+    if (fabs(S[(size_t)r * n + c2]) <= fabs(S[(size_t)r * n + c])) break; /* (r,c): max of its column and row */
+    c = c2;
+    int r2 = col_argmax(m, n, S, rowdone, c);
+    if (fabs(S[(size_t)r2 * n + c]) <= fabs(S[(size_t)r * n + c])) break; /* (r,c): max of its row and column */
+    r = r2;
+  }
+  *pp = r;
+  *pq = c;
+}
+
+static int ldu_p(int m, int n, const double *M, double thr, int thr_mode, int maxrank, int pivoting, ldu_t *out);
 static int ldu(int m, int n, const double *M, double thr, int thr_mode, int maxrank, ldu_t *out) {
+  return ldu_p(m, n, M, thr, thr_mode, maxrank, 0, out);
+}
+
+/* pivoting: 0 = full, 1 = rook (R23); everything else (stop rule, eps, elimination) as Alg. 2 */
+static int ldu_p(int m, int n, const double *M, double thr, int thr_mode, int maxrank, int pivoting, ldu_t *out) {
   memset(out, 0, sizeof(*out));
   for (size_t t = 0; t < (size_t)m * n; ++t)
     if (!isfinite(M[t])) return ORC_ERR_NONFINITE;
@@ -99,13 +143,17 @@ static int ldu(int m, int n, const double *M, double thr, int thr_mode, int maxr
   for (;;) {
     if (k == mn) { out->eps = 0.0; break; }
     int p = -1, q = -1;
-    double best = -1.0;
-    for (int i = 0; i < m; ++i) {
-      if (rowdone[i]) continue;
-      for (int j = 0; j < n; ++j) {
-        if (coldone[j]) continue;
-        double a = fabs(S[(size_t)i * n + j]);
-        if (a > best) { best = a; p = i; q = j; } /* strict '>' keeps the smallest (row, col) on ties */
+    if (pivoting == 1) {
+      rook_search(m, n, S, rowdone, coldone, &p, &q);
+    } else {
+      double best = -1.0;
+      for (int i = 0; i < m; ++i) {
+        if (rowdone[i]) continue;
+        for (int j = 0; j < n; ++j) {
+          if (coldone[j]) continue;
+          double a = fabs(S[(size_t)i * n + j]);
+          if (a > best) { best = a; p = i; q = j; } /* strict '>' keeps the smallest (row, col) on ties */
+        }
       }
     }
     double c = S[(size_t)p * n + q];
@@ -144,13 +192,13 @@ static int ldu(int m, int n, const double *M, double thr, int thr_mode, int maxr
   return ORC_OK;
 }
 
-/* Exported for the pin tests: prrLU of a dense row-major m x n matrix. */
-int oracle_ldu(int m, int n, const double *M, double thr, int thr_mode, int maxrank,
-               int *r, int *rows, int *cols, double *D, double *U /* maxr x n */,
-               double *Lc /* m x maxr */, int maxr, double *eps) {
-  if (m < 1 || n < 1 || maxrank < 1 || thr < 0) return ORC_ERR_INVALID;
+/* Exported for the pin tests: prrLU of a dense row-major m x n matrix (pivoting 0 full, 1 rook). */
+int oracle_ldu_p(int m, int n, const double *M, double thr, int thr_mode, int maxrank, int pivoting,
+                 int *r, int *rows, int *cols, double *D, double *U /* maxr x n */,
+                 double *Lc /* m x maxr */, int maxr, double *eps) {
+  if (m < 1 || n < 1 || maxrank < 1 || thr < 0 || pivoting < 0 || pivoting > 1) return ORC_ERR_INVALID;
   ldu_t f;
-  int st = ldu(m, n, M, thr, thr_mode, maxrank, &f);
+  int st = ldu_p(m, n, M, thr, thr_mode, maxrank, pivoting, &f);
   if (st != ORC_OK) return st;
   int kcap = (m < n ? m : n);
   if (maxrank < kcap) kcap = maxrank;
@@ -163,6 +211,11 @@ int oracle_ldu(int m, int n, const double *M, double thr, int thr_mode, int maxr
   }
   ldu_free(&f);
   return ORC_OK;
+}
+
+int oracle_ldu(int m, int n, const double *M, double thr, int thr_mode, int maxrank,
+               int *r, int *rows, int *cols, double *D, double *U, double *Lc, int maxr, double *eps) {
+  return oracle_ldu_p(m, n, M, thr, thr_mode, maxrank, 0, r, rows, cols, D, U, Lc, maxr, eps);
 }
 
 /* ------------------------------------------------------------------ */
@@ -255,6 +308,7 @@ typedef struct {
   unsigned char **canon_J;
   int *canon_cols_log_n;
   int **canon_cols_log;
+  int pivoting;     /* 0 full, 1 rook (R23): every prrLU of the run */
 } aci_t;
 
 static void log_push(aci_t *S, int b, int dir, int rl, int rr, const ldu_t *f, double scale) {
@@ -386,13 +440,17 @@ void oracle_free(void *h) { aci_free((aci_t *)h); }
  * tol, tol_mode (0 relative (R1), 1 absolute), maxrank, maxiter.
  * Returns a handle (NULL on allocation failure); *status receives the code.
  */
-void *oracle_aci(int L, const int *d, int N, const int *xranks, const double *const *xcores,
-                 int T, const double *coef, const int *expo, const int *yr0, const double *const *ycores,
-                 double tol, int tol_mode, int maxrank, int maxiter, int *status) {
+void *oracle_aci_p(int L, const int *d, int N, const int *xranks, const double *const *xcores,
+                   int T, const double *coef, const int *expo, const int *yr0, const double *const *ycores,
+                   double tol, int tol_mode, int maxrank, int maxiter, int pivoting, int *status) {
   *status = ORC_OK;
-  if (L < 2 || N < 1 || T < 1 || maxrank < 1 || maxiter < 1 || tol < 0) { *status = ORC_ERR_INVALID; return NULL; }
+  if (L < 2 || N < 1 || T < 1 || maxrank < 1 || maxiter < 1 || tol < 0 || pivoting < 0 || pivoting > 1) {
+    *status = ORC_ERR_INVALID;
+    return NULL;
+  }
   aci_t *S = (aci_t *)calloc(1, sizeof(aci_t));
   S->L = L; S->N = N;
+  S->pivoting = pivoting;
   S->d = (int *)malloc(sizeof(int) * L); memcpy(S->d, d, sizeof(int) * L);
   S->xr = (int *)malloc(sizeof(int) * N * (L + 1)); memcpy(S->xr, xranks, sizeof(int) * N * (L + 1));
   double *cf = (double *)malloc(sizeof(double) * T); memcpy(cf, coef, sizeof(double) * T);
@@ -444,7 +502,7 @@ void *oracle_aci(int L, const int *d, int N, const int *xranks, const double *co
       for (int t = 0; t < s && pl < cap; ++t) pl *= d[t];
       if (pl < cap) cap = (int)pl;
     }
-    int st = ldu(rows_, cols_, Y[s], tol, tol_mode == 0 ? 1 : 0, cap, &f);
+    int st = ldu_p(rows_, cols_, Y[s], tol, tol_mode == 0 ? 1 : 0, cap, S->pivoting, &f);
     if (st != ORC_OK) { *status = st; aci_free(S); return NULL; }
     /* J_s[k] = (sigma, J_{s+1}[j]) */
     unsigned char *Js = (unsigned char *)malloc((size_t)f.r * (L - s));
@@ -503,7 +561,7 @@ void *oracle_aci(int L, const int *d, int N, const int *xranks, const double *co
         }
         double thr = tol_mode == 0 ? tol * scale : tol;
         ldu_t f;
-        ldu(m, n, Pi, thr, 0, maxrank, &f);
+        ldu_p(m, n, Pi, thr, 0, maxrank, S->pivoting, &f);
         for (int k = 0; k < f.r; ++k) S->flops_prrlu += 2.0 * (m - k - 1) * (n - k - 1);
         S->pivot_steps += f.r;
         if (f.eps > maxeps) maxeps = f.eps;
@@ -555,6 +613,12 @@ void *oracle_aci(int L, const int *d, int N, const int *xranks, const double *co
   S->yr[0] = 1; S->yr[L] = 1;
   S->scale = scale;
   return S;
+}
+
+void *oracle_aci(int L, const int *d, int N, const int *xranks, const double *const *xcores,
+                 int T, const double *coef, const int *expo, const int *yr0, const double *const *ycores,
+                 double tol, int tol_mode, int maxrank, int maxiter, int *status) {
+  return oracle_aci_p(L, d, N, xranks, xcores, T, coef, expo, yr0, ycores, tol, tol_mode, maxrank, maxiter, 0, status);
 }
 
 /* ---- accessors (ctypes) ---- */

@@ -164,3 +164,115 @@ def test_nonfinite_rejected():
     M[1, 2] = np.nan
     with pytest.raises(ValueError):
         oracle.ldu(M, 0.0, 3)
+
+
+# ---------------------------------------------------------------------------------------------
+# Rook pivoting (reading R23; SURVEY 8(f) NEXT-4, B:5 "full/rook")
+# ---------------------------------------------------------------------------------------------
+ROOK_GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "prrlu_rook_hand.json")
+
+
+def test_rook_golden_hand_worked_cases():
+    for case in json.load(open(ROOK_GOLDEN))["cases"]:
+        M = np.array(case["M"], dtype=np.float64)
+        f = oracle.ldu(M, case["tol_abs"], case["maxrank"], pivoting="rook")
+        assert list(f["rows"]) == case["rows"], case["name"]
+        assert list(f["cols"]) == case["cols"], case["name"]
+        assert np.allclose(f["D"], case["D"], rtol=1e-15, atol=0), case["name"]
+        assert f["eps"] == case["eps"], case["name"]
+
+
+def _residual_closed_form(M, I, J):
+    """S = M - M[:, J] M[I, J]^{-1} M[I, :] (the Schur complement after pivots I, J)."""
+    if not I:
+        return M.copy()
+    return M - M[:, J] @ np.linalg.solve(M[np.ix_(I, J)], M[I, :])
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_rook_pivot_is_max_of_its_row_and_column(seed):
+    """Definition of a rook pivot: every accepted (p, q) is the largest |.| of its active row and
+    of its active column in the residual recomputed in closed form (independent of the oracle's
+    elimination); eps is the magnitude of such an entry of the final residual (or 0)."""
+    rng = np.random.default_rng(seed)
+    m, n = int(rng.integers(3, 12)), int(rng.integers(3, 12))
+    M = rng.standard_normal((m, n))
+    f = oracle.ldu(M, 0.0, min(m, n), pivoting="rook")
+    I, J = [], []
+    for p, q in zip(f["rows"], f["cols"]):
+        S = _residual_closed_form(M, I, J)
+        ar = [i for i in range(m) if i not in I]
+        ac = [j for j in range(n) if j not in J]
+        v = abs(S[p, q])
+        assert v >= np.abs(S[p, ac]).max() * (1 - 1e-12)
+        assert v >= np.abs(S[ar, q]).max() * (1 - 1e-12)
+        I.append(int(p))
+        J.append(int(q))
+    assert len(I) == min(m, n) and f["eps"] == 0.0
+
+
+def _rook_exact(M, maxrank):
+    """Textbook rook pivoting (Neal & Poole) in exact rational arithmetic: start at the smallest
+    active column, alternate column / row maxima (strictly larger only, ties -> smallest index)."""
+    m, n = len(M), len(M[0])
+    S = [[Fraction(int(x)) for x in row] for row in M]
+    rd, cd = set(), set()
+    piv, D = [], []
+    for _ in range(min(m, n, maxrank)):
+        ar = [i for i in range(m) if i not in rd]
+        ac = [j for j in range(n) if j not in cd]
+        c = ac[0]
+        r = max(ar, key=lambda i: (abs(S[i][c]), -i))
+        while True:
+            c2 = max(ac, key=lambda j: (abs(S[r][j]), -j))
+            if abs(S[r][c2]) <= abs(S[r][c]):
+                break
+            c = c2
+            r2 = max(ar, key=lambda i: (abs(S[i][c]), -i))
+            if abs(S[r2][c]) <= abs(S[r][c]):
+                break
+            r = r2
+        if S[r][c] == 0:
+            break
+        piv.append((r, c))
+        D.append(S[r][c])
+        for i in ar:
+            if i == r:
+                continue
+            li = S[i][c] / S[r][c]
+            for j in ac:
+                if j != c:
+                    S[i][j] -= li * S[r][j]
+        rd.add(r)
+        cd.add(c)
+    return piv, D
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_rook_matches_exact_rational_rook_elimination(seed):
+    """Integer matrices with distinct magnitudes (no near-ties): the oracle's rook pivots equal
+    exact rational rook pivoting, and its pivot values match to roundoff."""
+    rng = np.random.default_rng(100 + seed)
+    m, n = int(rng.integers(3, 8)), int(rng.integers(3, 8))
+    vals = rng.permutation(np.arange(1, m * n + 1)) * rng.choice([-1, 1], size=m * n)
+    M = vals.reshape(m, n).astype(np.float64)
+    piv, D = _rook_exact(M.astype(int).tolist(), min(m, n))
+    f = oracle.ldu(M, 0.0, min(m, n), pivoting="rook")
+    k = len(piv)
+    assert f["r"] == k
+    assert [tuple(x) for x in zip(f["rows"][:k], f["cols"][:k])] == piv[:k]
+    assert np.allclose(f["D"][:k], [float(x) for x in D[:k]], rtol=1e-13)
+
+
+def test_rook_full_rank_reconstruction_and_interpolation():
+    """Rook LDU reproduces M at full rank (L D U = M), and the cross interpolation of its pivots
+    is exact on the pivot rows and columns — the identities hold for any pivot order."""
+    rng = np.random.default_rng(7)
+    M = rng.standard_normal((9, 7))
+    f = oracle.ldu(M, 0.0, 7, pivoting="rook")
+    assert f["r"] == 7
+    R = f["L"] @ np.diag(f["D"]) @ f["U"]
+    assert np.abs(R - M).max() <= 1e-12 * np.abs(M).max()
+    I, J = list(f["rows"]), list(f["cols"])
+    A = M[:, J] @ np.linalg.inv(M[np.ix_(I, J)]) @ M[I, :]
+    assert np.abs(A[I, :] - M[I, :]).max() <= 1e-12 and np.abs(A[:, J] - M[:, J]).max() <= 1e-12

@@ -190,7 +190,19 @@ typedef struct {
                               * else ACI_ERR_UNSUPPORTED. 0 (default): the fastest tiers, which may
                               * span several clusters; such calls from several host threads are
                               * serialised by the library (a process-wide lock). */
+  int pivoting;              /* ACI_PIVOT_FULL (default): full pivoting, Alg. 2 as written.
+                              * ACI_PIVOT_ROOK: rook pivoting in every prrLU of the call (B:5
+                              * "full/rook"; reading R23 of DESIGN.md §2): the pivot is an entry that
+                              * is the largest of its active row and column, found from the smallest
+                              * active column by alternating column / row maxima; eps is the magnitude
+                              * of the first rejected rook candidate. Pivots (hence outputs) differ
+                              * from full pivoting. Real values only and blocks within the
+                              * `concurrent` envelope (one CTA or one 16-CTA cluster), else
+                              * ACI_ERR_UNSUPPORTED. */
 } aci_options;
+
+#define ACI_PIVOT_FULL 0
+#define ACI_PIVOT_ROOK 1
 
 /*
  * aci_elementwise — Alg. 1: y ~ f(x^1, ..., x^N) with ||y - f(x)||_inf ~ tau

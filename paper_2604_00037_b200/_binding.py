@@ -17,6 +17,8 @@ ACI_OK, ACI_NOT_CONVERGED = 0, 1
 ERRORS = {-1: "ACI_ERR_INVALID", -2: "ACI_ERR_SHAPE", -3: "ACI_ERR_NONFINITE", -4: "ACI_ERR_OOM",
           -5: "ACI_ERR_CUDA", -6: "ACI_ERR_UNSUPPORTED"}
 TOL_RELATIVE, TOL_ABSOLUTE = 0, 1
+PIVOT_FULL, PIVOT_ROOK = 0, 1
+_PIVOTING = {"full": PIVOT_FULL, "rook": PIVOT_ROOK}
 MAX_INPUTS, MAX_TERMS, MAX_EXPO = 4, 8, 4
 
 # every symbol include/aci.h declares (tests check the library exports all of them)
@@ -67,7 +69,7 @@ class aci_options(C.Structure):
                 ("log", C.POINTER(aci_pivot_log)), ("stream", C.c_void_p), ("workspace", C.c_void_p),
                 ("workspace_bytes", C.c_size_t), ("I_sets", C.POINTER(C.POINTER(C.c_uint8))),
                 ("J_sets", C.POINTER(C.POINTER(C.c_uint8))), ("profile", C.POINTER(aci_profile)),
-                ("iter_ms", C.POINTER(C.c_float)), ("concurrent", C.c_int)]
+                ("iter_ms", C.POINTER(C.c_float)), ("concurrent", C.c_int), ("pivoting", C.c_int)]
 
 
 _lib = None
@@ -234,7 +236,7 @@ def _make_log(L, maxrank, max_sweeps):
 
 def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, tol_mode=TOL_RELATIVE,
                     log=False, stream=0, workspace=None, index_sets=False, profile=False, iter_times=False,
-                    concurrent=False):
+                    concurrent=False, pivoting="full"):
     """Run aci_elementwise_ex. ``inputs`` are TensorTrain handles (aliases allowed).
 
     Returns (TensorTrain, status, report dict, extras dict).
@@ -251,6 +253,7 @@ def aci_elementwise(op, inputs, tol, maxrank, max_sweeps, y_init=None, seed=0, t
     opts.tol_mode = tol_mode
     opts.stream = stream or None
     opts.concurrent = 1 if concurrent else 0
+    opts.pivoting = _PIVOTING[pivoting]
     extras = {}
     if workspace is not None:
         opts.workspace, opts.workspace_bytes = workspace
@@ -313,6 +316,7 @@ def aci_elementwise_batch(jobs, max_parallel=0):
         o.seed = j.get("seed", 0)
         o.y_init = j["y_init"].handle.value if j.get("y_init") is not None else None
         o.tol_mode = j.get("tol_mode", TOL_RELATIVE)
+        o.pivoting = _PIVOTING[j.get("pivoting", "full")]
         if j.get("log"):
             lg, rd = _make_log(len(ins[0].shape()[0]), int(j["maxrank"]), int(j["max_sweeps"]))
             o.log = C.pointer(lg)

@@ -909,6 +909,7 @@ struct Run {
   cudaError_t launch_err = cudaSuccess;  // first rejected prrLU launch (eager launches)
   int cplx = 0, Z = 1, ZE = 1;  // complex run: Z = 2 doubles per entry, ZE = 4 for expanded operands
   int one = 0;                  // aci_options.concurrent: single-cluster prrLU launches
+  int rook = 0;                 // aci_options.pivoting == ACI_PIVOT_ROOK (R23, NEXT-4)
   int L = 0, N = 0, maxrank = 0, max_sweeps = 0, log_cap_upd = 0, log_cap_piv = 0, colcap = 0;
   std::vector<int> d, yr;
   std::vector<std::vector<int>> xr;      // [n][s], s = 0..L
@@ -1264,7 +1265,7 @@ static std::vector<uint64_t> graph_key(const Run &R, const FOp &op, double tol, 
     u(b);
   };
   u((uint64_t)(uintptr_t)ws); u(need); u((uint64_t)(uintptr_t)st);
-  u(R.L); u(R.N); u(R.maxrank); u(R.log_cap_upd); u(R.log_cap_piv); u(R.colcap); u(R.cplx); u(R.one);
+  u(R.L); u(R.N); u(R.maxrank); u(R.log_cap_upd); u(R.log_cap_piv); u(R.colcap); u(R.cplx); u(R.one); u(R.rook);
   dbl(tol); u(tol_mode);
   for (int x : R.d) u(x);
   for (int x : R.yr) u(x);
@@ -1462,6 +1463,7 @@ static void bond_update(Run &R, double tol, int tol_mode, int b, int dir, int lo
   a.rows = R.prow[pv]; a.cols = R.pcol[pv]; a.r_out = R.rout + pv; a.eps_out = R.epsb + pv;
   a.U = dir == 1 ? R.Ust[b] : nullptr;
   a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter; a.epoch = R.epoch;
+  a.rook = R.rook;
   SideStream &sd = side_stream();
   const bool look = la_m > 0 && la_n > 0;
   R.P->begin(ACI_PROF_PRRLU);
@@ -1533,6 +1535,7 @@ static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st)
   a.rows = R.prow[s - 1]; a.cols = R.pcol[s - 1]; a.r_out = R.rout + (s - 1); a.eps_out = R.epsb + (s - 1);
   a.U = nullptr;
   a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter; a.epoch = R.epoch;
+  a.rook = R.rook;
   // the R-frame product T^n = X^n_s R^n_{s+1} is only gathered after the factorisation: it runs on
   // the side stream beside the prrLU (forked off its launch-completion event, as in the sweep)
   SideStream &sd = side_stream();
@@ -1581,7 +1584,8 @@ extern "C" int aci_limits(int *max_rows, int *max_cols) {
   return ACI_OK;
 }
 
-static int build_run(const Inputs &I, const tt_s *y, int maxrank, int max_sweeps, Run &R, int one = 0) {
+static int build_run(const Inputs &I, const tt_s *y, int maxrank, int max_sweeps, Run &R, int one = 0,
+                     int rook = 0) {
   const tt_s *t0 = I.tts[0];
   R.L = t0->L;
   R.N = (int)I.tts.size();
@@ -1608,9 +1612,14 @@ static int build_run(const Inputs &I, const tt_s *y, int maxrank, int max_sweeps
   for (int b = 0; b < R.L - 1; ++b) R.colcap = std::max(R.colcap, R.mmax[b]);
   for (int s = 0; s < R.L; ++s) R.colcap = std::max(R.colcap, R.yr[s]);
   R.colcap *= R.Z;
-  // envelope
+  // envelope (rook mode: the single-cluster envelope, real values)
   R.one = one;
-  auto ok = [&](int m, int n) { return one ? prrlu_supported_one(m, n, R.cplx != 0) : prrlu_supported(m, n, R.cplx != 0); };
+  R.rook = rook;
+  if (rook && R.cplx) return fail(ACI_ERR_UNSUPPORTED, "aci: rook pivoting is implemented for real values only");
+  auto ok = [&](int m, int n) {
+    if (rook) return prrlu_supported_rook(m, n);
+    return one ? prrlu_supported_one(m, n, R.cplx != 0) : prrlu_supported(m, n, R.cplx != 0);
+  };
   for (int b = 0; b < R.L - 1; ++b)
     if (!ok(R.mmax[b], R.nmax[b]))
       return fail(ACI_ERR_UNSUPPORTED, "aci: 2-site block " + std::to_string(R.mmax[b]) + "x" +
@@ -1680,7 +1689,11 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   }
 
   Run R;
-  st = build_run(I, y, maxrank, max_sweeps, R, o.concurrent ? 1 : 0);
+  if (o.pivoting != ACI_PIVOT_FULL && o.pivoting != ACI_PIVOT_ROOK) {
+    tt_destroy(ygen);
+    return fail(ACI_ERR_INVALID, "aci: bad pivoting mode");
+  }
+  st = build_run(I, y, maxrank, max_sweeps, R, o.concurrent ? 1 : 0, o.pivoting == ACI_PIVOT_ROOK ? 1 : 0);
   if (st) { tt_destroy(ygen); return st; }
   size_t need = carve(R, nullptr);
   char *ws = nullptr;

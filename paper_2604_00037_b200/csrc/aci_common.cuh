@@ -59,6 +59,7 @@ struct LuArgs {
   unsigned int *counter;      // zeroed before launch
   unsigned int *epoch;        // incremented by every grid-tier launch (tags stay unique)
   long long *dbg;             // development timing (ACI_PRRLU_TIMING builds only)
+  int rook;                   // 1: rook pivoting (R23, NEXT-4; one-CTA / one-cluster envelope, real)
 };
 
 // ---- launchers (defined in gemm.cu / prrlu.cu / sweep.cu) ----
@@ -88,6 +89,7 @@ size_t prrlu_exchange_bytes(int max_m, int max_n);
 cudaError_t launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx = false, bool one = false,
                          cudaEvent_t started = nullptr);
 bool prrlu_supported_one(int m, int n, bool cplx);
+bool prrlu_supported_rook(int m, int n);
 // Chooses the prrLU exchange tier (cluster size) once; call before any stream capture.
 void prrlu_init();
 void prrlu_envelope(int *max_rows, int *max_cols);

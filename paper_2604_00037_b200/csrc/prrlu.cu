@@ -161,6 +161,18 @@ __device__ __forceinline__ void bulk_push(unsigned rdst, unsigned src, unsigned 
                : "memory");
 }
 
+// cluster tier with ACI_COL_TMA: the winner's column, as its tagged packets (16 B per row), lands
+// here in every CTA of the cluster by one cp.async.bulk ... .multicast::cluster (dynamic shared memory
+// of prrlu_kernel<8, 2, false>)
+constexpr size_t kColTmaSmem = (size_t)16 * 1024;  // kMaxRows packets
+__device__ __forceinline__ void bulk_multicast(unsigned dst, const void *src, unsigned bytes, unsigned mbar,
+                                               unsigned short mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(mbar), "h"(mask)
+      : "memory");
+}
+
 // push tier (XM = 3): one 8-CTA cluster; every CTA's candidate column is pushed into every
 // cluster CTA's shared memory (dynamic: [2 parities][8 ranks][kPushRows] + 2 staging columns)
 constexpr int kPushCS = 8;
@@ -219,6 +231,9 @@ __device__ __forceinline__ int lpair(int i) { return ((i >> 6) << 6) | ((i & 31)
 #ifndef ACI_COL_SPREAD
 #define ACI_COL_SPREAD 0  // 1: one 128-byte line of column packets per 1 KB (spreads a column over L2 slices)
 #endif
+#ifndef ACI_COL_TMA
+#define ACI_COL_TMA 1  // cluster tier (real): the winner's column reaches every CTA by one TMA multicast per cluster
+#endif
 #ifndef ACI_PUB_WINNER
 #define ACI_PUB_WINNER 0  // 1: several-cluster grids publish only the cluster winners' columns
 #endif
@@ -244,7 +259,8 @@ struct PrrluSmem {
   unsigned win[4];  // grid winner broadcast (key-poll mode)
   uint4 ck[2][16];                // cluster tier: CTA keys pushed by the cluster's CTAs (by parity)
   uint4 gw[2];                    // cluster tier, several clusters: global winner pushed by rank 0
-  unsigned long long mb[4];       // cluster tier: key mbarrier and winner mbarrier per parity
+  unsigned long long mb[5];       // cluster tier: key mbarrier and winner mbarrier per parity; [4] column multicast
+  unsigned cdone[48];             // rook mode: eliminated columns (bitmap, up to 1536 columns)
 };
 
 // One factorisation, register tile EA x EB per thread, NW warps per CTA. GRID: G CTAs (this is
@@ -265,6 +281,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   constexpr int MROWS = 32 * EA;
   constexpr int CB = NW * EB;  // columns per CTA
   static_assert(MROWS <= kMaxRows && CB <= kMaxCB, "tile exceeds the shared scratch");
+  constexpr bool kColTma = ACI_COL_TMA && XM == 2 && !CPLX && ACI_COL_SPREAD == 0;
   double *s_l = S.l, *s_raw = S.raw, *s_u = S.u;
   unsigned *s_hi = S.hi, *s_lo = S.lo, *s_id = S.id;
   const int tid = threadIdx.x;
@@ -303,6 +320,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   // strict '>' within a chain; chains merged with the slot (== flat-index) tie-break.
   double bx = 0.0;
   int be = 0;
+  int k = 0;  // pivots accepted so far
   auto scan = [&]() {
     constexpr int NE = EA * EB;
     constexpr int NCH = NE < ACI_SCAN_CHAINS ? NE : ACI_SCAN_CHAINS;
@@ -354,6 +372,19 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     const int a = be / EB, b = be % EB;
     const unsigned flat = (unsigned)(lane + 32 * a) * NC + (unsigned)(c0 + w + NW * b);
     return Key{(unsigned)(bits >> 32), (unsigned)bits, flat};
+  };
+  // ACI_COL_TMA: whether the candidate `c` will be accepted as pivot k (the stop rule R2, evaluated
+  // early by the thread that issues the column multicast), and the multicast of CTA gsrc's
+  // published column into every CTA of this cluster
+  auto will_accept = [&](const Key &c) -> bool {
+    const double wk = key_abs(c);
+    if (k == kmax) return false;
+    if (k == 0) return wk != 0.0;
+    return !(wk <= thr);
+  };
+  auto issue_col_multicast = [&](int gsrc) {
+    const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + gsrc) * A.colcap) * 2;
+    bulk_multicast(smem_u32(push_dyn), src, (unsigned)m * 16u, smem_u32(&S.mb[4]), (unsigned short)0xffffu);
   };
   // v[a][b] = fma(mul(a, r_a), ub[b], v[a][b]) for this thread's rows, with r_a the per-row value
   // (l_i or the raw column entry) read from `base` in the lpair layout, several LDS.128 in flight
@@ -419,12 +450,16 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       mbar_arm(smem_u32(&S.mb[1]), CS * 16u);
       mbar_arm(smem_u32(&S.mb[2]), 16u);
       mbar_arm(smem_u32(&S.mb[3]), 16u);
+      if (kColTma) {
+        mbar_init(smem_u32(&S.mb[4]), 1u);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_arm(smem_u32(&S.mb[4]), (unsigned)m * 16u);
+      }
     }
     cluster_sync_all();
   }
 
   double first = 0.0, eps = 0.0;
-  int k = 0;
 #ifdef ACI_PRRLU_TIMING
   long long ph_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long ph_t_ = clock64();
@@ -503,6 +538,12 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
                   st_pkt(dst + cpk(Z * (lane + 32 * a) + z), tagged(tag, (unsigned)bits),
                          tagged(tag, (unsigned)(bits >> 32)));
                 }
+        // the column is multicast from L2 by the async proxy: order these generic stores before
+        // it (the tags still catch a stale read)
+        if (kColTma) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __syncwarp();  // lane 0 may issue the multicast of these packets
+        }
       };
       const bool late_pub = ACI_PUB_WINNER && XM == 2 && G > (int)cluster_size();
       if (w == pw) {
@@ -529,6 +570,9 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         if (late_pub && w == pw && (int)((cw.id % NC) / CB) == g) publish_col();
         if (NCL == 1) {
           win = cw;
+          // the winner's owner warp (it wrote the packets) multicasts them into every CTA
+          if (kColTma && w == pw && lane == 0 && (int)((cw.id % NC) / CB) == g && will_accept(cw))
+            issue_col_multicast(g);
         } else {
           // cluster winners through L2: warp 0 of each cluster's rank-0 CTA publishes its
           // cluster's winner (slots 256 B apart), polls the NCL tagged keys and pushes the
@@ -579,6 +623,8 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
             const Key gw = warp_argmax(gk);
             if (lane < (int)CS)
               st_async_key(mapa_u32(smem_u32(&S.gw[par]), (unsigned)lane), gw.hi, gw.lo, gw.id, mapa_u32(mwp, (unsigned)lane));
+            // each cluster's leader multicasts the global winner's column into its cluster
+            if (kColTma && lane == 0 && will_accept(gw)) issue_col_multicast((int)((gw.id % NC) / CB));
           }
           mbar_wait(mwp, (unsigned)(k >> 1) & 1u);
           if (tid == 0) mbar_arm(mwp, 16u);
@@ -701,12 +747,32 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2 * kColSpread;
       constexpr int PPT = (MROWS + T - 1) / T;  // column packets per thread
       unsigned long long cw[PPT + 1][2];
+      if constexpr (kColTma) {
+        // the packets arrive by the cluster's multicast (one per accepted pivot: phase k & 1); a
+        // stale packet (tag mismatch) is re-read from L2 below
+        mbar_wait(smem_u32(&S.mb[4]), (unsigned)k & 1u);
+        if (tid == 0) mbar_arm(smem_u32(&S.mb[4]), (unsigned)m * 16u);
+        const unsigned long long *cs = reinterpret_cast<const unsigned long long *>(push_dyn);
 #pragma unroll
-      for (int t = 0; t < PPT; ++t) {
-        const int i = tid + T * t;
-        if (i < m) ld_pkt(src + cpk(i), cw[t][0], cw[t][1]);
+        for (int t = 0; t < PPT; ++t) {
+          const int i = tid + T * t;
+          if (i < m) {
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(cs + 2 * i);
+            cw[t][0] = x.x;
+            cw[t][1] = x.y;
+          }
+        }
+        const ulonglong2 xp = *reinterpret_cast<const ulonglong2 *>(cs + 2 * p);
+        cw[PPT][0] = xp.x;
+        cw[PPT][1] = xp.y;
+      } else {
+#pragma unroll
+        for (int t = 0; t < PPT; ++t) {
+          const int i = tid + T * t;
+          if (i < m) ld_pkt(src + cpk(i), cw[t][0], cw[t][1]);
+        }
+        ld_pkt(src + cpk(p), cw[PPT][0], cw[PPT][1]);  // the pivot itself, for its sign
       }
-      ld_pkt(src + cpk(p), cw[PPT][0], cw[PPT][1]);  // the pivot itself, for its sign
       while ((unsigned)(cw[PPT][0] >> 32) != tag || (unsigned)(cw[PPT][1] >> 32) != tag)
         ld_pkt(src + cpk(p), cw[PPT][0], cw[PPT][1]);
       const bool neg = (cw[PPT][1] & 0x80000000ull) != 0;
@@ -893,6 +959,39 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   if (XM >= 2) cluster_sync_all();  // no CTA leaves while a cluster peer may still push to it
 }
 
+#include "prrlu_rook.cuh"
+
+// Rook mode (LuArgs::rook): the prrlu_kernel_one envelope (one CTA or one 16-CTA cluster), real
+// values; the same variant list as prrlu_kernel_one.
+template <int NWT>
+__global__ void __launch_bounds__(NWT * 32) prrlu_kernel_rook(LuArgs A) {
+  __shared__ PrrluSmem S;
+  const int m = A.dims->m, n = A.dims->n;
+  const int g = blockIdx.x;
+#define ACI_CTA_VARIANT(EA, EB)                                        \
+  if (m <= 32 * (EA) && n <= NWT * (EB)) {                              \
+    if (g == 0) prrlu_body_rook<(EA), (EB), NWT, 0>(A, S, 1, 0);       \
+    return;                                                            \
+  }
+#define ACI_ONE_VARIANT(EA, EB)                                        \
+  if (m <= 32 * (EA) && n <= 16 * NWT * (EB)) {                         \
+    prrlu_body_rook<(EA), (EB), NWT, 2>(A, S, 16, g);                  \
+    return;                                                            \
+  }
+  ACI_CTA_VARIANT(1, 4)
+  ACI_CTA_VARIANT(2, 8)
+  ACI_CTA_VARIANT(4, 4)
+  ACI_CTA_VARIANT(1, 16)
+  ACI_CTA_VARIANT(4, 16)
+  ACI_CTA_VARIANT(8, 8)
+  ACI_CTA_VARIANT(2, 32)
+  ACI_ONE_VARIANT(4, 8)    //  128 x 1024
+  ACI_ONE_VARIANT(8, 4)    //  256 x  512
+  ACI_ONE_VARIANT(16, 4)   //  512 x  512
+#undef ACI_CTA_VARIANT
+#undef ACI_ONE_VARIANT
+}
+
 // Runtime tier selection from the LIVE sizes (device-resident ranks): the launch is sized for
 // the static capacity, and CTAs beyond what the live block needs exit immediately. 8 warps per
 // CTA (up to 255 registers, so the 32-row-slot tiles do not spill; measured faster than 16).
@@ -1064,6 +1163,10 @@ static int cluster_choice_once() {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c * 8);
     cfg.blockDim = dim3(kNWT * 32);
+    if (ACI_COL_TMA && kern == (const void *)prrlu_kernel<kNWT, 2, false>) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kColTmaSmem);
+      cfg.dynamicSmemBytes = kColTmaSmem;
+    }
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = c;
@@ -1113,6 +1216,21 @@ bool prrlu_supported_one(int m, int n, bool cplx) {
   return false;
 }
 
+// rook envelope: prrlu_kernel_rook's variants (one CTA, or one 16-CTA cluster up to 512 rows)
+static bool rook_fits_cta(int m, int n) {
+  const int cta[][2] = {{32, 32}, {64, 64}, {128, 32}, {32, 128}, {128, 128}, {256, 64}, {64, 256}};
+  for (auto &e : cta)
+    if (m <= e[0] && n <= e[1]) return true;
+  return false;
+}
+bool prrlu_supported_rook(int m, int n) {
+  if (rook_fits_cta(m, n)) return true;
+  const int one[][2] = {{128, 1024}, {256, 512}, {512, 512}};
+  for (auto &e : one)
+    if (m <= e[0]) return n <= e[1];
+  return false;
+}
+
 bool prrlu_supported(int max_m, int max_n, bool cplx) {
   if (fits_one_cta(max_m, max_n, cplx)) return true;
   if (cplx) return max_m <= 512 && (max_n + 15) / 16 <= 64;
@@ -1137,9 +1255,12 @@ size_t prrlu_exchange_bytes(int max_m, int max_n) {
 static int attr_once() {
   cudaFuncSetAttribute((const void *)prrlu_kernel_push<kNWT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kPushSmem);
+  cudaFuncSetAttribute((const void *)prrlu_kernel<kNWT, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kColTmaSmem);
   // 16-CTA clusters are a non-portable size
   const void *k16[] = {(const void *)prrlu_kernel<kNWT, 2, false>, (const void *)prrlu_kernel<kNWT, 2, true>,
-                       (const void *)prrlu_kernel_one<kNWT, false>, (const void *)prrlu_kernel_one<kNWT, true>};
+                       (const void *)prrlu_kernel_one<kNWT, false>, (const void *)prrlu_kernel_one<kNWT, true>,
+                       (const void *)prrlu_kernel_rook<kNWT>};
   for (const void *f : k16) cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return 0;
 }
@@ -1175,6 +1296,14 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
     ++na;
   }
   cfg.attrs = at;
+  if (a.rook) {  // NEXT-4: one CTA or one 16-CTA cluster (prrlu_supported_one), real values
+    if (CPLX || !prrlu_supported_rook(max_m, max_n)) return cudaErrorNotSupported;
+    const bool cta = rook_fits_cta(max_m, max_n);
+    cfg.gridDim = dim3(cta ? 1 : 16);
+    if (!cta) cluster(16);
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, prrlu_kernel_rook<kNWT>, args);
+  }
   if (!CPLX && !fits_one_cta(max_m, max_n, CPLX) && max_m <= kPushRows && max_n <= kPushCS * kNWT * 4 &&
       push_enabled()) {
     cfg.gridDim = dim3(kPushCS);
@@ -1199,6 +1328,7 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
   if (cs > 0) {
     G = (G + cs - 1) / cs * cs;
     cfg.gridDim = dim3(G);
+    if (!CPLX && ACI_COL_TMA) cfg.dynamicSmemBytes = kColTmaSmem;
     cluster(cs);
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 2, CPLX>, args);

@@ -617,3 +617,43 @@ def test_workspace_alignment_and_query_sweeps(aci):
                                           workspace=(ws.data_ptr(), n20))
     ref, *_ = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], 20, y_init=y0)
     assert all(np.array_equal(a, b) for a, b in zip(out.cores(), ref.cores()))
+
+
+@pytest.mark.parametrize("cfg,chi", [(0, 0), (1, 0), (3, 64)])
+def test_rook_pivoting_vs_rook_oracle(aci, cfg, chi):
+    """Rook pivoting (aci_options.pivoting = ACI_PIVOT_ROOK; R23) against the
+    oracle's rook mode on the same seeded inputs: identical ordered pivots on every update (and the
+    canonicalisation), equal iteration counts, and <= 10 tol against the oracle and the exact
+    product on seeded samples."""
+    cf = make_config(cfg, chi, npts=20_000) if chi else make_config(cfg, npts=20_000)
+    xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+    y0 = aci.TensorTrain.from_cores(cf["y_init"])
+    out, st, rep, ex = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0,
+                                           log=True, pivoting="rook")
+    ref = oracle.aci(cf["inputs"], cf["op"], cf["y_init"], cf["tol"], cf["maxrank"], cf["max_sweeps"], pivoting="rook")
+    L = len(cf["inputs"][0].d)
+    for s_ in range(1, L):
+        assert np.array_equal(ex["canon_cols"][s_], ref.canon_cols(s_))
+    assert len(ex["log"]) == len(ref.log)
+    assert _pivot_agreement(ex, ref) == len(ref.log)
+    assert (rep["iterations"], rep["converged"]) == (ref.report["iterations"], ref.report["converged"])
+    s = cf["samples"]
+    y = out.evaluate(s)
+    assert _rel(y, oracle.tt_evaluate(ref.cores, s)) <= 10 * cf["tol"]
+    exact = oracle.tt_evaluate(cf["inputs"][0], s) * oracle.tt_evaluate(cf["inputs"][1], s)
+    assert _rel(y, exact) <= 10 * cf["tol"]
+
+
+def test_rook_pivoting_envelope(aci):
+    """Rook mode runs where the factorisation fits one CTA or one 16-CTA cluster (<= 512 rows) and
+    on real values; beyond that ACI_ERR_UNSUPPORTED, nothing launched."""
+    cf = make_config(3, 256, npts=0)  # 1024 x 1024 blocks
+    xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+    with pytest.raises(aci.AciError) as e:
+        aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], 1, pivoting="rook")
+    assert e.value.code == -6
+    rng = np.random.default_rng(5)
+    z = aci.TensorTrain.from_cores([c + 0.5j * c for c in G.random_tt(8, 2, 3, rng).cores])
+    with pytest.raises(aci.AciError) as e:
+        aci.aci_elementwise({"coef": [1.0], "expo": [[2]]}, [z], 1e-8, 16, 2, pivoting="rook")
+    assert e.value.code == -6

@@ -1618,7 +1618,8 @@ static int build_run(const Inputs &I, const tt_s *y, int maxrank, int max_sweeps
   if (rook && R.cplx) return fail(ACI_ERR_UNSUPPORTED, "aci: rook pivoting is implemented for real values only");
   auto ok = [&](int m, int n) {
     if (rook) return prrlu_supported_rook(m, n);
-    return one ? prrlu_supported_one(m, n, R.cplx != 0) : prrlu_supported(m, n, R.cplx != 0);
+    if (one && !prrlu_coop_multicluster()) return prrlu_supported_one(m, n, R.cplx != 0);
+    return prrlu_supported(m, n, R.cplx != 0);
   };
   for (int b = 0; b < R.L - 1; ++b)
     if (!ok(R.mmax[b], R.nmax[b]))

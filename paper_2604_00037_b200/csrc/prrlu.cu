@@ -384,7 +384,8 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   };
   auto issue_col_multicast = [&](int gsrc) {
     const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + gsrc) * A.colcap) * 2;
-    bulk_multicast(smem_u32(push_dyn), src, (unsigned)m * 16u, smem_u32(&S.mb[4]), (unsigned short)0xffffu);
+    const unsigned CS = cluster_size();
+    bulk_multicast(smem_u32(push_dyn), src, (unsigned)m * 16u, smem_u32(&S.mb[4]), (unsigned short)((1u << CS) - 1u));
   };
   // v[a][b] = fma(mul(a, r_a), ub[b], v[a][b]) for this thread's rows, with r_a the per-row value
   // (l_i or the raw column entry) read from `base` in the lpair layout, several LDS.128 in flight
@@ -1137,6 +1138,20 @@ static bool push_enabled() {
   return on;
 }
 
+// Multi-cluster grids (their clusters spin on each other) are launched COOPERATIVELY: the driver
+// then gang-schedules the whole grid — measured (tools/probe/coop_spin.cu,
+// profiles/r02_coop_spin.txt): a cooperative cluster launch of more clusters than can be co-resident
+// is refused ("too many blocks in cooperative launch") instead of being split into waves. So a
+// grid never holds part of its clusters while waiting for the rest, whatever else runs on the GPU
+// (other streams, other processes). ACI_PRRLU_COOP=0 switches it off (A/B measurements).
+static bool coop_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("ACI_PRRLU_COOP");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
 bool fits_one_cta(int m, int n, bool cplx) {
   const int v8[][2] = {{1, 4}, {2, 8}, {4, 4}, {1, 16}, {4, 16}, {8, 8}, {2, 32}, {32, 2}};
   const int z8[][2] = {{1, 8}, {2, 8}, {4, 4}, {1, 16}, {4, 8}, {2, 16}, {8, 4}, {16, 2}};
@@ -1202,6 +1217,8 @@ int cluster_choice() {
 
 }  // namespace
 
+bool prrlu_coop_multicluster() { return coop_enabled() && cluster_choice() > 0; }
+
 bool prrlu_supported_one(int m, int n, bool cplx) {
   if (fits_one_cta(m, n, cplx)) return true;
   const int v[][2] = {{128, 1024}, {256, 512}, {512, 512}, {1024, 256}};
@@ -1257,6 +1274,8 @@ static int attr_once() {
                        (int)kPushSmem);
   cudaFuncSetAttribute((const void *)prrlu_kernel<kNWT, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kColTmaSmem);
+  cudaFuncSetAttribute((const void *)prrlu_kernel_one<kNWT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kColTmaSmem);
   // 16-CTA clusters are a non-portable size
   const void *k16[] = {(const void *)prrlu_kernel<kNWT, 2, false>, (const void *)prrlu_kernel<kNWT, 2, true>,
                        (const void *)prrlu_kernel_one<kNWT, false>, (const void *)prrlu_kernel_one<kNWT, true>,
@@ -1280,7 +1299,7 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kNWT * 32);
   cfg.stream = st;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   int na = 0;
   auto cluster = [&](int cs) {
     at[na].id = cudaLaunchAttributeClusterDimension;
@@ -1312,12 +1331,15 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, prrlu_kernel_push<kNWT>, args);
   }
-  if (one && !fits_one_cta(max_m, max_n, CPLX)) {
+  if (one && !fits_one_cta(max_m, max_n, CPLX) && prrlu_supported_one(max_m, max_n, CPLX)) {
     cfg.gridDim = dim3(16);
+    if (!CPLX && ACI_COL_TMA) cfg.dynamicSmemBytes = kColTmaSmem;  // the column multicast buffer
     cluster(16);
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, prrlu_kernel_one<kNWT, CPLX>, args);
   }
+  // (concurrent mode beyond one cluster: the cooperative multi-cluster grid below, which is
+  // gang-scheduled, so concurrent products cannot hold part of each other's clusters)
   if (fits_one_cta(max_m, max_n, CPLX)) {
     cfg.gridDim = dim3(1);
     cfg.numAttrs = na;
@@ -1330,6 +1352,11 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
     cfg.gridDim = dim3(G);
     if (!CPLX && ACI_COL_TMA) cfg.dynamicSmemBytes = kColTmaSmem;
     cluster(cs);
+    if (coop_enabled() && G > cs) {
+      at[na].id = cudaLaunchAttributeCooperative;
+      at[na].val.cooperative = 1;
+      ++na;
+    }
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 2, CPLX>, args);
   }

@@ -1463,11 +1463,11 @@ static void bond_update(Run &R, double tol, int tol_mode, int b, int dir, int lo
   a.rows = R.prow[pv]; a.cols = R.pcol[pv]; a.r_out = R.rout + pv; a.eps_out = R.epsb + pv;
   a.U = dir == 1 ? R.Ust[b] : nullptr;
   a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter; a.epoch = R.epoch;
-  a.rook = R.rook;
   SideStream &sd = side_stream();
   const bool look = la_m > 0 && la_n > 0;
   R.P->begin(ACI_PROF_PRRLU);
-  const cudaError_t le = launch_prrlu(a, R.mmax[b], R.nmax[b], st, R.cplx != 0, R.one != 0, look ? sd.started : nullptr);
+  const cudaError_t le = launch_prrlu(a, R.mmax[b], R.nmax[b], st, R.cplx != 0, R.one != 0, look ? sd.started : nullptr,
+                                      R.rook != 0);
   if (le != cudaSuccess && R.launch_err == cudaSuccess) R.launch_err = le;
   R.P->end(1);
   if (look) {
@@ -1535,11 +1535,11 @@ static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st)
   a.rows = R.prow[s - 1]; a.cols = R.pcol[s - 1]; a.r_out = R.rout + (s - 1); a.eps_out = R.epsb + (s - 1);
   a.U = nullptr;
   a.colpub = R.colpub; a.colcap = R.colcap; a.keys = R.keys; a.counter = R.counter; a.epoch = R.epoch;
-  a.rook = R.rook;
   // the R-frame product T^n = X^n_s R^n_{s+1} is only gathered after the factorisation: it runs on
   // the side stream beside the prrLU (forked off its launch-completion event, as in the sweep)
   SideStream &sd = side_stream();
-  const cudaError_t le = launch_prrlu(a, max_m, max_n, st, R.cplx != 0, R.one != 0, tm > 0 ? sd.started : nullptr);
+  const cudaError_t le = launch_prrlu(a, max_m, max_n, st, R.cplx != 0, R.one != 0, tm > 0 ? sd.started : nullptr,
+                                      R.rook != 0);
   if (le != cudaSuccess && R.launch_err == cudaSuccess) R.launch_err = le;
   if (tm > 0) {
     cudaStreamWaitEvent(sd.st, sd.started, 0);

@@ -59,7 +59,6 @@ struct LuArgs {
   unsigned int *counter;      // zeroed before launch
   unsigned int *epoch;        // incremented by every grid-tier launch (tags stay unique)
   long long *dbg;             // development timing (ACI_PRRLU_TIMING builds only)
-  int rook;                   // 1: rook pivoting (R23, NEXT-4; one-CTA / one-cluster envelope, real)
 };
 
 // ---- launchers (defined in gemm.cu / prrlu.cu / sweep.cu) ----
@@ -86,8 +85,9 @@ size_t prrlu_exchange_bytes(int max_m, int max_n);
 // one: single-cluster mode (aci_options.concurrent): at most one 16-CTA cluster per launch.
 // `started` (optional, created with cudaEventDisableTiming) fires once every CTA has begun.
 // Returns the launch's own error (a rejected configuration leaves the outputs unwritten).
+// rook: rook pivoting (R23, NEXT-4; prrlu_supported_rook envelope, real values) instead of full.
 cudaError_t launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx = false, bool one = false,
-                         cudaEvent_t started = nullptr);
+                         cudaEvent_t started = nullptr, bool rook = false);
 bool prrlu_supported_one(int m, int n, bool cplx);
 bool prrlu_supported_rook(int m, int n);
 // true when multi-cluster prrLU grids are launched cooperatively (gang-scheduled): concurrent-mode

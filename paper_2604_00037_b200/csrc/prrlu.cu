@@ -161,18 +161,6 @@ __device__ __forceinline__ void bulk_push(unsigned rdst, unsigned src, unsigned 
                : "memory");
 }
 
-// cluster tier with ACI_COL_TMA: the winner's column, as its tagged packets (16 B per row), lands
-// here in every CTA of the cluster by one cp.async.bulk ... .multicast::cluster (dynamic shared memory
-// of prrlu_kernel<8, 2, false>)
-constexpr size_t kColTmaSmem = (size_t)16 * 1024;  // kMaxRows packets
-__device__ __forceinline__ void bulk_multicast(unsigned dst, const void *src, unsigned bytes, unsigned mbar,
-                                               unsigned short mask) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(mbar), "h"(mask)
-      : "memory");
-}
-
 // push tier (XM = 3): one 8-CTA cluster; every CTA's candidate column is pushed into every
 // cluster CTA's shared memory (dynamic: [2 parities][8 ranks][kPushRows] + 2 staging columns)
 constexpr int kPushCS = 8;
@@ -201,12 +189,9 @@ __device__ __forceinline__ double key_abs(const Key &k) {
   return __longlong_as_double((long long)(((unsigned long long)k.hi << 32) | k.lo));
 }
 
-// Paired shared-memory layout of per-row values (l_i, the raw pivot column): row i = lane + 32 a
-// sits at (a / 2) * 64 + 2 lane + a % 2, so a thread reads the values of its rows a and a + 1 with
-// one LDS.128 (a warp reads 512 contiguous bytes: conflict-free), and the rank-1 update keeps
-// several pairs in flight instead of a LDS -> DFMA -> LDS chain through one register (the SASS of
-// the previous layout reloaded every l_i into the same register pair).
-__device__ __forceinline__ int lpair(int i) { return ((i >> 6) << 6) | ((i & 31) << 1) | ((i >> 5) & 1); }
+// Rook mode (prrlu_rook.cuh): per-row values (l_i, the raw pivot column) in a paired shared layout,
+// row i = lane + 32 a at (a / 2) * 64 + 2 lane + a % 2 (a warp's reads are 512 contiguous bytes).
+__device__ __forceinline__ int lpair2(int i) { return ((i >> 6) << 6) | ((i & 31) << 1) | ((i >> 5) & 1); }
 
 // columns per warp of the 8-warp grid tiers, measured (tools/prrlu_bench.cu): 16 CTAs with the
 // key-poll barrier beat more CTAs with the counter barrier up to 512 rows
@@ -222,30 +207,10 @@ __device__ __forceinline__ int lpair(int i) { return ((i >> 6) << 6) | ((i & 31)
 #ifndef ACI_BIG_EB
 #define ACI_BIG_EB 2  // columns per warp for the 1024-row grid tier (64 CTAs for 1024 columns)
 #endif
-#ifndef ACI_SCAN_CHAINS
-#define ACI_SCAN_CHAINS 4  // independent max chains per thread in the candidate scan
-#endif
-#ifndef ACI_SCAN_DMNMX
-#define ACI_SCAN_DMNMX 0
-#endif
-#ifndef ACI_COL_SPREAD
-#define ACI_COL_SPREAD 0  // 1: one 128-byte line of column packets per 1 KB (spreads a column over L2 slices)
-#endif
-#ifndef ACI_COL_TMA
-#define ACI_COL_TMA 1  // cluster tier (real): the winner's column reaches every CTA by one TMA multicast per cluster
-#endif
-#ifndef ACI_PUB_WINNER
-#define ACI_PUB_WINNER 0  // 1: several-cluster grids publish only the cluster winners' columns
-#endif
-constexpr int kColSpread = ACI_COL_SPREAD ? 8 : 1;
-// u64 offset of packet i (two u64 words per element) within a CTA's column slot
-__device__ __forceinline__ int cpk(int i) { return ACI_COL_SPREAD ? (((i >> 3) << 7) | ((i & 7) << 1)) : 2 * i; }
-#ifndef ACI_LPAIR_PD
-#define ACI_LPAIR_PD 4  // l_i pairs loaded per group in the rank-1 update
-#endif
-#ifndef ACI_LPAIR
-#define ACI_LPAIR 1  // paired l_i layout + prefetched rank-1 update (lpair); 0 = one LDS per row
-#endif
+// Column-slot stride factor of the exchange buffer (kept at 1: a spread layout over L2 slices was
+// measured without gain, profiles/r02_prrlu_bench_variants.txt); packet i sits at u64 offset 2 i
+constexpr int kColSpread = 1;
+__device__ __forceinline__ int cpk(int i) { return 2 * i; }
 constexpr int kMaxRows = 1024;   // 32 * EA_max
 constexpr int kMaxCTAs = 148;
 constexpr int kMaxCB = 512;      // NW * EB_max
@@ -259,8 +224,11 @@ struct PrrluSmem {
   unsigned win[4];  // grid winner broadcast (key-poll mode)
   uint4 ck[2][16];                // cluster tier: CTA keys pushed by the cluster's CTAs (by parity)
   uint4 gw[2];                    // cluster tier, several clusters: global winner pushed by rank 0
-  unsigned long long mb[5];       // cluster tier: key mbarrier and winner mbarrier per parity; [4] column multicast
-  unsigned cdone[48];             // rook mode: eliminated columns (bitmap, up to 1536 columns)
+  unsigned long long mb[4];       // cluster tier: key mbarrier and winner mbarrier per parity
+};
+// rook mode (prrlu_rook.cuh): the same scratch plus a bitmap of eliminated columns
+struct RookSmem : PrrluSmem {
+  unsigned cdone[48];  // up to 1536 columns
 };
 
 // One factorisation, register tile EA x EB per thread, NW warps per CTA. GRID: G CTAs (this is
@@ -281,7 +249,6 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   constexpr int MROWS = 32 * EA;
   constexpr int CB = NW * EB;  // columns per CTA
   static_assert(MROWS <= kMaxRows && CB <= kMaxCB, "tile exceeds the shared scratch");
-  constexpr bool kColTma = ACI_COL_TMA && XM == 2 && !CPLX && ACI_COL_SPREAD == 0;
   double *s_l = S.l, *s_raw = S.raw, *s_u = S.u;
   unsigned *s_hi = S.hi, *s_lo = S.lo, *s_id = S.id;
   const int tid = threadIdx.x;
@@ -320,10 +287,9 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   // strict '>' within a chain; chains merged with the slot (== flat-index) tie-break.
   double bx = 0.0;
   int be = 0;
-  int k = 0;  // pivots accepted so far
   auto scan = [&]() {
     constexpr int NE = EA * EB;
-    constexpr int NCH = NE < ACI_SCAN_CHAINS ? NE : ACI_SCAN_CHAINS;
+    constexpr int NCH = NE < 4 ? NE : 4;
     // chains keep the SIGNED value and compare magnitudes (|.| operand modifiers of DSETP), so
     // no FP64-pipe instruction is spent materialising |v|
     double cx[NCH];
@@ -333,19 +299,6 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       const double *x = v[e / EB][e % EB];
       return CPLX ? __dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[Z - 1], x[Z - 1])) : x[0];
     };
-#if ACI_SCAN_DMNMX
-    // chains hold |x|: DMNMX for the value, DSETP against the old max for the slot (3 instructions
-    // per entry instead of DSETP + 2 FSEL + SEL)
-#pragma unroll
-    for (int t = 0; t < NCH; ++t) { cx[t] = fabs(mag(t)); ce[t] = t; }
-#pragma unroll
-    for (int e = NCH; e < NE; ++e) {
-      const double x = mag(e);
-      const bool take = fabs(x) > cx[e % NCH];
-      cx[e % NCH] = fmax(cx[e % NCH], fabs(x));
-      ce[e % NCH] = take ? e : ce[e % NCH];
-    }
-#else
 #pragma unroll
     for (int t = 0; t < NCH; ++t) { cx[t] = mag(t); ce[t] = t; }
 #pragma unroll
@@ -355,7 +308,6 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       cx[e % NCH] = take ? x : cx[e % NCH];
       ce[e % NCH] = take ? e : ce[e % NCH];
     }
-#endif
     double bm = cx[0];
     int bi = ce[0];
 #pragma unroll
@@ -372,61 +324,6 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     const int a = be / EB, b = be % EB;
     const unsigned flat = (unsigned)(lane + 32 * a) * NC + (unsigned)(c0 + w + NW * b);
     return Key{(unsigned)(bits >> 32), (unsigned)bits, flat};
-  };
-  // ACI_COL_TMA: whether the candidate `c` will be accepted as pivot k (the stop rule R2, evaluated
-  // early by the thread that issues the column multicast), and the multicast of CTA gsrc's
-  // published column into every CTA of this cluster
-  auto will_accept = [&](const Key &c) -> bool {
-    const double wk = key_abs(c);
-    if (k == kmax) return false;
-    if (k == 0) return wk != 0.0;
-    return !(wk <= thr);
-  };
-  auto issue_col_multicast = [&](int gsrc) {
-    const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + gsrc) * A.colcap) * 2;
-    const unsigned CS = cluster_size();
-    bulk_multicast(smem_u32(push_dyn), src, (unsigned)m * 16u, smem_u32(&S.mb[4]), (unsigned short)((1u << CS) - 1u));
-  };
-  // v[a][b] = fma(mul(a, r_a), ub[b], v[a][b]) for this thread's rows, with r_a the per-row value
-  // (l_i or the raw column entry) read from `base` in the lpair layout, several LDS.128 in flight
-  auto rank1_update = [&](const double *base, const double (&ub)[EB], auto mul) {
-#if ACI_LPAIR
-    // groups of PD pairs: the group's LDS.128 are issued back to back and pinned (the empty asm
-    // needs every value), so one shared-memory latency covers 4 * EB DFMAs per pair; ptxas would
-    // otherwise reload every pair into one register quad right before its DFMAs
-    constexpr int NP = (EA + 1) / 2;
-    constexpr int PD = NP < ACI_LPAIR_PD ? NP : ACI_LPAIR_PD;
-#pragma unroll
-    for (int g = 0; g < NP; g += PD) {
-      double2 c[PD];
-#pragma unroll
-      for (int j = 0; j < PD; ++j)
-        if (g + j < NP) c[j] = *reinterpret_cast<const double2 *>(base + (g + j) * 64 + 2 * lane);
-#pragma unroll
-      for (int j = 0; j < PD; ++j)
-        if (g + j < NP) asm volatile("" : "+d"(c[j].x), "+d"(c[j].y));
-#pragma unroll
-      for (int j = 0; j < PD; ++j) {
-        if (g + j >= NP) continue;
-        const int a0 = 2 * (g + j), a1 = a0 + 1 < EA ? a0 + 1 : a0;
-        const double m0 = mul(a0, c[j].x);
-#pragma unroll
-        for (int b = 0; b < EB; ++b) v[a0][b][0] = fma(m0, ub[b], v[a0][b][0]);
-        if (a0 + 1 < EA) {
-          const double m1 = mul(a1, c[j].y);
-#pragma unroll
-          for (int b = 0; b < EB; ++b) v[a1][b][0] = fma(m1, ub[b], v[a1][b][0]);
-        }
-      }
-    }
-#else
-#pragma unroll
-    for (int a = 0; a < EA; ++a) {
-      const double ma = mul(a, base[lpair(lane + 32 * a)]);
-#pragma unroll
-      for (int b = 0; b < EB; ++b) v[a][b][0] = fma(ma, ub[b], v[a][b][0]);
-    }
-#endif
   };
   scan();
   if constexpr (XM == 3) {
@@ -451,16 +348,12 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       mbar_arm(smem_u32(&S.mb[1]), CS * 16u);
       mbar_arm(smem_u32(&S.mb[2]), 16u);
       mbar_arm(smem_u32(&S.mb[3]), 16u);
-      if (kColTma) {
-        mbar_init(smem_u32(&S.mb[4]), 1u);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        mbar_arm(smem_u32(&S.mb[4]), (unsigned)m * 16u);
-      }
     }
     cluster_sync_all();
   }
 
   double first = 0.0, eps = 0.0;
+  int k = 0;
 #ifdef ACI_PRRLU_TIMING
   long long ph_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long ph_t_ = clock64();
@@ -491,7 +384,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         for (int b = 0; b < EB; ++b)
           if (b == bc)
 #pragma unroll
-            for (int a = 0; a < EA; ++a) stg[lpair(lane + 32 * a)] = v[a][b][0];
+            for (int a = 0; a < EA; ++a) stg[lane + 32 * a] = v[a][b][0];
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane < (int)CS) {
@@ -524,9 +417,9 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
           st_async_key(mapa_u32(smem_u32(&S.ck[par][cluster_rank()]), (unsigned)lane), ck.hi, ck.lo, ck.id,
                        mapa_u32(smem_u32(&S.mb[par]), (unsigned)lane));
       }
-      auto publish_col = [&]() {
+      if (w == pw) {
         const int bc = jc / NW;
-        unsigned long long *dst = A.colpub + (((size_t)par * G + g) * A.colcap) * 2 * kColSpread;
+        unsigned long long *dst = A.colpub + (((size_t)par * G + g) * A.colcap) * 2;
 #pragma unroll
         for (int b = 0; b < EB; ++b)
           if (b == bc)
@@ -536,19 +429,9 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
 #pragma unroll
                 for (int z = 0; z < Z; ++z) {
                   const unsigned long long bits = (unsigned long long)__double_as_longlong(v[a][b][z]);
-                  st_pkt(dst + cpk(Z * (lane + 32 * a) + z), tagged(tag, (unsigned)bits),
+                  st_pkt(dst + 2 * (Z * (lane + 32 * a) + z), tagged(tag, (unsigned)bits),
                          tagged(tag, (unsigned)(bits >> 32)));
                 }
-        // the column is multicast from L2 by the async proxy: order these generic stores before
-        // it (the tags still catch a stale read)
-        if (kColTma) {
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          __syncwarp();  // lane 0 may issue the multicast of these packets
-        }
-      };
-      const bool late_pub = ACI_PUB_WINNER && XM == 2 && G > (int)cluster_size();
-      if (w == pw) {
-        if (!late_pub) publish_col();
         if (XM == 1 && lane == 0) {
           unsigned long long *kd = A.keys + ((size_t)par * G + g) * 4;
           st_pkt(kd, tagged(tag, ck.hi), tagged(tag, ck.lo));
@@ -567,13 +450,8 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         const uint4 q4 = S.ck[par][lane < (int)CS ? lane : 0];
         const Key cw = warp_argmax(lane < (int)CS ? Key{q4.x, q4.y, q4.z} : Key{0u, 0u, BAD_ID});
         const int NCL = G / (int)CS;
-        // late publication: only the cluster winner's column goes to L2 (its candidate is ck)
-        if (late_pub && w == pw && (int)((cw.id % NC) / CB) == g) publish_col();
         if (NCL == 1) {
           win = cw;
-          // the winner's owner warp (it wrote the packets) multicasts them into every CTA
-          if (kColTma && w == pw && lane == 0 && (int)((cw.id % NC) / CB) == g && will_accept(cw))
-            issue_col_multicast(g);
         } else {
           // cluster winners through L2: warp 0 of each cluster's rank-0 CTA publishes its
           // cluster's winner (slots 256 B apart), polls the NCL tagged keys and pushes the
@@ -624,8 +502,6 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
             const Key gw = warp_argmax(gk);
             if (lane < (int)CS)
               st_async_key(mapa_u32(smem_u32(&S.gw[par]), (unsigned)lane), gw.hi, gw.lo, gw.id, mapa_u32(mwp, (unsigned)lane));
-            // each cluster's leader multicasts the global winner's column into its cluster
-            if (kColTma && lane == 0 && will_accept(gw)) issue_col_multicast((int)((gw.id % NC) / CB));
           }
           mbar_wait(mwp, (unsigned)(k >> 1) & 1u);
           if (tid == 0) mbar_arm(mwp, 16u);
@@ -727,7 +603,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     if constexpr (XM == 3) {
       // the winner's column is already in this CTA's shared memory (pushed with its key)
       const double *col = push_dyn + ((size_t)(k & 1) * kPushCS + q / CB) * kPushRows;
-      const bool neg = col[lpair(p)] < 0.0;
+      const bool neg = col[p] < 0.0;
       inv = neg ? -inv_abs : inv_abs;
       __syncthreads();  // S3: pivot row in smem
       PHASE(5);
@@ -738,44 +614,26 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         }
 #pragma unroll
       for (int b = 0; b < EB; ++b) ub[b] = s_u[w + NW * b];
-      // multiplier -l_i (exact negation: fma(-l_i, u, v) as R4); padding rows hold 0
-      rank1_update(col, ub, [&](int a, double r) -> double {
+#pragma unroll
+      for (int a = 0; a < EA; ++a) {
         const int i = lane + 32 * a;
-        return -(i < m ? ((i == p) ? 1.0 : r * inv) : 0.0);
-      });
+        const double li = i < m ? ((i == p) ? 1.0 : col[i] * inv) : 0.0;
+#pragma unroll
+        for (int b = 0; b < EB; ++b) v[a][b][0] = fma(-li, ub[b], v[a][b][0]);
+      }
     } else if (GRID) {
       const unsigned tag = (ep << 12) | (unsigned)(k + 1);
-      const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2 * kColSpread;
+      const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2;
       constexpr int PPT = (MROWS + T - 1) / T;  // column packets per thread
       unsigned long long cw[PPT + 1][2];
-      if constexpr (kColTma) {
-        // the packets arrive by the cluster's multicast (one per accepted pivot: phase k & 1); a
-        // stale packet (tag mismatch) is re-read from L2 below
-        mbar_wait(smem_u32(&S.mb[4]), (unsigned)k & 1u);
-        if (tid == 0) mbar_arm(smem_u32(&S.mb[4]), (unsigned)m * 16u);
-        const unsigned long long *cs = reinterpret_cast<const unsigned long long *>(push_dyn);
 #pragma unroll
-        for (int t = 0; t < PPT; ++t) {
-          const int i = tid + T * t;
-          if (i < m) {
-            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(cs + 2 * i);
-            cw[t][0] = x.x;
-            cw[t][1] = x.y;
-          }
-        }
-        const ulonglong2 xp = *reinterpret_cast<const ulonglong2 *>(cs + 2 * p);
-        cw[PPT][0] = xp.x;
-        cw[PPT][1] = xp.y;
-      } else {
-#pragma unroll
-        for (int t = 0; t < PPT; ++t) {
-          const int i = tid + T * t;
-          if (i < m) ld_pkt(src + cpk(i), cw[t][0], cw[t][1]);
-        }
-        ld_pkt(src + cpk(p), cw[PPT][0], cw[PPT][1]);  // the pivot itself, for its sign
+      for (int t = 0; t < PPT; ++t) {
+        const int i = tid + T * t;
+        if (i < m) ld_pkt(src + 2 * i, cw[t][0], cw[t][1]);
       }
+      ld_pkt(src + 2 * p, cw[PPT][0], cw[PPT][1]);  // the pivot itself, for its sign
       while ((unsigned)(cw[PPT][0] >> 32) != tag || (unsigned)(cw[PPT][1] >> 32) != tag)
-        ld_pkt(src + cpk(p), cw[PPT][0], cw[PPT][1]);
+        ld_pkt(src + 2 * p, cw[PPT][0], cw[PPT][1]);
       const bool neg = (cw[PPT][1] & 0x80000000ull) != 0;
       inv = neg ? -inv_abs : inv_abs;
 #pragma unroll
@@ -783,8 +641,8 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         const int i = tid + T * t;
         if (i < m) {
           while ((unsigned)(cw[t][0] >> 32) != tag || (unsigned)(cw[t][1] >> 32) != tag)
-            ld_pkt(src + cpk(i), cw[t][0], cw[t][1]);
-          s_l[lpair(i)] = (i == p) ? 1.0 : pkt_double(cw[t][0], cw[t][1]) * inv;
+            ld_pkt(src + 2 * i, cw[t][0], cw[t][1]);
+          s_l[i] = (i == p) ? 1.0 : pkt_double(cw[t][0], cw[t][1]) * inv;
         }
       }
       __syncthreads();  // S3
@@ -796,7 +654,12 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         }
 #pragma unroll
       for (int b = 0; b < EB; ++b) ub[b] = s_u[w + NW * b];
-      rank1_update(s_l, ub, [](int, double l) -> double { return -l; });  // fma(-l_i, u_j, S_ij) (R4)
+#pragma unroll
+      for (int a = 0; a < EA; ++a) {
+        const double li = s_l[lane + 32 * a];
+#pragma unroll
+        for (int b = 0; b < EB; ++b) v[a][b][0] = fma(-li, ub[b], v[a][b][0]);
+      }
     } else {
       const int jq = q - c0;
       if ((jq % NW) == w) {
@@ -805,10 +668,10 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         for (int b = 0; b < EB; ++b)
           if (b == bq)
 #pragma unroll
-            for (int a = 0; a < EA; ++a) s_raw[lpair(lane + 32 * a)] = v[a][b][0];
+            for (int a = 0; a < EA; ++a) s_raw[lane + 32 * a] = v[a][b][0];
       }
       __syncthreads();  // S2 (CTA tier): raw pivot column and pivot row in smem
-      const bool neg = s_raw[lpair(p)] < 0.0;
+      const bool neg = s_raw[p] < 0.0;
       inv = neg ? -inv_abs : inv_abs;
 #pragma unroll
       for (int b = 0; b < EB; ++b) ub[b] = neg ? s_u[w + NW * b] : -s_u[w + NW * b];
@@ -819,16 +682,20 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
           if (j < n) A.U[(size_t)k * ldu + j] = (j == q) ? 1.0 : s_u[jj] * inv;
         }
       // every thread forms its own l'_i (no third barrier)
-      rank1_update(s_raw, ub, [&](int a, double r) -> double {
-        return (lane + 32 * a == p) ? (neg ? -1.0 : 1.0) : r * inv_abs;
-      });
+#pragma unroll
+      for (int a = 0; a < EA; ++a) {
+        const int i = lane + 32 * a;
+        const double li = (i == p) ? (neg ? -1.0 : 1.0) : s_raw[i] * inv_abs;
+#pragma unroll
+        for (int b = 0; b < EB; ++b) v[a][b][0] = fma(li, ub[b], v[a][b][0]);
+      }
     }
     } else {
     // ---- complex (RZ2-RZ4): inv = conj(c) / w with w the key's |c|^2
     double cr, ci;
     if (GRID) {
       const unsigned tag = (ep << 12) | (unsigned)(k + 1);
-      const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2 * kColSpread;
+      const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2;
       constexpr int PPT = (MROWS + T - 1) / T;  // column entries per thread (2 packets each)
       unsigned long long cw[PPT + 1][2][2];
 #pragma unroll
@@ -836,13 +703,13 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         const int i = tid + T * t;
         if (i < m)
 #pragma unroll
-          for (int z = 0; z < 2; ++z) ld_pkt(src + cpk(2 * i + z), cw[t][z][0], cw[t][z][1]);
+          for (int z = 0; z < 2; ++z) ld_pkt(src + 2 * (2 * i + z), cw[t][z][0], cw[t][z][1]);
       }
 #pragma unroll
       for (int z = 0; z < 2; ++z) {
-        ld_pkt(src + cpk(2 * p + z), cw[PPT][z][0], cw[PPT][z][1]);
+        ld_pkt(src + 2 * (2 * p + z), cw[PPT][z][0], cw[PPT][z][1]);
         while ((unsigned)(cw[PPT][z][0] >> 32) != tag || (unsigned)(cw[PPT][z][1] >> 32) != tag)
-          ld_pkt(src + cpk(2 * p + z), cw[PPT][z][0], cw[PPT][z][1]);
+          ld_pkt(src + 2 * (2 * p + z), cw[PPT][z][0], cw[PPT][z][1]);
       }
       cr = pkt_double(cw[PPT][0][0], cw[PPT][0][1]);
       ci = pkt_double(cw[PPT][1][0], cw[PPT][1][1]);
@@ -854,7 +721,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
 #pragma unroll
           for (int z = 0; z < 2; ++z)
             while ((unsigned)(cw[t][z][0] >> 32) != tag || (unsigned)(cw[t][z][1] >> 32) != tag)
-              ld_pkt(src + cpk(2 * i + z), cw[t][z][0], cw[t][z][1]);
+              ld_pkt(src + 2 * (2 * i + z), cw[t][z][0], cw[t][z][1]);
           const double xr = pkt_double(cw[t][0][0], cw[t][0][1]), xi = pkt_double(cw[t][1][0], cw[t][1][1]);
           double lr = 1.0, li = 0.0;
           if (i != p) {  // RZ3
@@ -966,7 +833,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
 // values; the same variant list as prrlu_kernel_one.
 template <int NWT>
 __global__ void __launch_bounds__(NWT * 32) prrlu_kernel_rook(LuArgs A) {
-  __shared__ PrrluSmem S;
+  __shared__ RookSmem S;
   const int m = A.dims->m, n = A.dims->n;
   const int g = blockIdx.x;
 #define ACI_CTA_VARIANT(EA, EB)                                        \
@@ -1138,20 +1005,13 @@ static bool push_enabled() {
   return on;
 }
 
-// Multi-cluster grids (their clusters spin on each other) are launched COOPERATIVELY: the driver
-// then gang-schedules the whole grid — measured (tools/probe/coop_spin.cu,
-// profiles/r02_coop_spin.txt): a cooperative cluster launch of more clusters than can be co-resident
-// is refused ("too many blocks in cooperative launch") instead of being split into waves. So a
-// grid never holds part of its clusters while waiting for the rest, whatever else runs on the GPU
-// (other streams, other processes). ACI_PRRLU_COOP=0 switches it off (A/B measurements).
-static bool coop_enabled() {
-  static const bool on = [] {
-    const char *e = getenv("ACI_PRRLU_COOP");
-    return !e || atoi(e) != 0;
-  }();
-  return on;
-}
-
+// A cooperative launch would gang-schedule a multi-cluster grid: tools/probe/coop_spin.cu measured
+// (profiles/r02_coop_spin.txt) that a cooperative cluster launch larger than the co-resident
+// cluster count is refused rather than split into waves. But the multi-cluster prrLU launched
+// cooperatively inside the captured iteration crashed the host process (SIGSEGV,
+// profiles/r02d_ab.txt, chi = 256), so it is not used: multi-cluster grids stay plain cluster
+// launches, serialised across host threads by the library (aci.cu) and checked for co-residency
+// once (cluster_choice).
 bool fits_one_cta(int m, int n, bool cplx) {
   const int v8[][2] = {{1, 4}, {2, 8}, {4, 4}, {1, 16}, {4, 16}, {8, 8}, {2, 32}, {32, 2}};
   const int z8[][2] = {{1, 8}, {2, 8}, {4, 4}, {1, 16}, {4, 8}, {2, 16}, {8, 4}, {16, 2}};
@@ -1178,10 +1038,6 @@ static int cluster_choice_once() {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c * 8);
     cfg.blockDim = dim3(kNWT * 32);
-    if (ACI_COL_TMA && kern == (const void *)prrlu_kernel<kNWT, 2, false>) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kColTmaSmem);
-      cfg.dynamicSmemBytes = kColTmaSmem;
-    }
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = c;
@@ -1217,7 +1073,7 @@ int cluster_choice() {
 
 }  // namespace
 
-bool prrlu_coop_multicluster() { return coop_enabled() && cluster_choice() > 0; }
+bool prrlu_coop_multicluster() { return false; }
 
 bool prrlu_supported_one(int m, int n, bool cplx) {
   if (fits_one_cta(m, n, cplx)) return true;
@@ -1272,10 +1128,6 @@ size_t prrlu_exchange_bytes(int max_m, int max_n) {
 static int attr_once() {
   cudaFuncSetAttribute((const void *)prrlu_kernel_push<kNWT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kPushSmem);
-  cudaFuncSetAttribute((const void *)prrlu_kernel<kNWT, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)kColTmaSmem);
-  cudaFuncSetAttribute((const void *)prrlu_kernel_one<kNWT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)kColTmaSmem);
   // 16-CTA clusters are a non-portable size
   const void *k16[] = {(const void *)prrlu_kernel<kNWT, 2, false>, (const void *)prrlu_kernel<kNWT, 2, true>,
                        (const void *)prrlu_kernel_one<kNWT, false>, (const void *)prrlu_kernel_one<kNWT, true>,
@@ -1294,7 +1146,8 @@ void prrlu_init() {
 // CTAs have begun executing) can be attached: the sweep forks its look-ahead GEMM off it, onto the
 // SMs the prrLU does not hold (aci.cu bond_update).
 template <bool CPLX>
-static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool one, cudaEvent_t started) {
+static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool one, cudaEvent_t started,
+                                  bool rook) {
   LuArgs args = a;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kNWT * 32);
@@ -1315,7 +1168,7 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
     ++na;
   }
   cfg.attrs = at;
-  if (a.rook) {  // NEXT-4: one CTA or one 16-CTA cluster (prrlu_supported_one), real values
+  if (rook) {  // NEXT-4: one CTA or one 16-CTA cluster (prrlu_supported_one), real values
     if (CPLX || !prrlu_supported_rook(max_m, max_n)) return cudaErrorNotSupported;
     const bool cta = rook_fits_cta(max_m, max_n);
     cfg.gridDim = dim3(cta ? 1 : 16);
@@ -1333,7 +1186,6 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
   }
   if (one && !fits_one_cta(max_m, max_n, CPLX) && prrlu_supported_one(max_m, max_n, CPLX)) {
     cfg.gridDim = dim3(16);
-    if (!CPLX && ACI_COL_TMA) cfg.dynamicSmemBytes = kColTmaSmem;  // the column multicast buffer
     cluster(16);
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, prrlu_kernel_one<kNWT, CPLX>, args);
@@ -1350,13 +1202,7 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
   if (cs > 0) {
     G = (G + cs - 1) / cs * cs;
     cfg.gridDim = dim3(G);
-    if (!CPLX && ACI_COL_TMA) cfg.dynamicSmemBytes = kColTmaSmem;
     cluster(cs);
-    if (coop_enabled() && G > cs) {
-      at[na].id = cudaLaunchAttributeCooperative;
-      at[na].val.cooperative = 1;
-      ++na;
-    }
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 2, CPLX>, args);
   }
@@ -1370,7 +1216,7 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
 }
 
 cudaError_t launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st, bool cplx, bool one,
-                         cudaEvent_t started) {
-  return cplx ? launch_prrlu_t<true>(a, max_m, max_n, st, one, started)
-              : launch_prrlu_t<false>(a, max_m, max_n, st, one, started);
+                         cudaEvent_t started, bool rook) {
+  return cplx ? launch_prrlu_t<true>(a, max_m, max_n, st, one, started, rook)
+              : launch_prrlu_t<false>(a, max_m, max_n, st, one, started, rook);
 }

@@ -22,7 +22,7 @@
 #pragma once
 
 template <int EA, int EB, int NW, int XM>
-__device__ __forceinline__ void prrlu_body_rook(const LuArgs &A, PrrluSmem &S, const int G, const int g) {
+__device__ __forceinline__ void prrlu_body_rook(const LuArgs &A, RookSmem &S, const int G, const int g) {
   static_assert(XM == 0 || XM == 2, "rook pivoting: one CTA or one cluster");
   constexpr bool GRID = XM != 0;
   constexpr int T = NW * 32;
@@ -249,7 +249,7 @@ __device__ __forceinline__ void prrlu_body_rook(const LuArgs &A, PrrluSmem &S, c
         if (i < m) {
           while ((unsigned)(cw[t][0] >> 32) != tag || (unsigned)(cw[t][1] >> 32) != tag)
             ld_pkt(src + cpk(i), cw[t][0], cw[t][1]);
-          s_l[lpair(i)] = (i == p) ? 1.0 : pkt_double(cw[t][0], cw[t][1]) * inv;
+          s_l[lpair2(i)] = (i == p) ? 1.0 : pkt_double(cw[t][0], cw[t][1]) * inv;
         }
       }
       __syncthreads();
@@ -261,14 +261,14 @@ __device__ __forceinline__ void prrlu_body_rook(const LuArgs &A, PrrluSmem &S, c
         for (int b = 0; b < EB; ++b)
           if (b == bq)
 #pragma unroll
-            for (int a = 0; a < EA; ++a) s_raw[lpair(lane + 32 * a)] = v[a][b][0];
+            for (int a = 0; a < EA; ++a) s_raw[lpair2(lane + 32 * a)] = v[a][b][0];
       }
       __syncthreads();
-      inv = s_raw[lpair(p)] < 0.0 ? -inv_abs : inv_abs;
+      inv = s_raw[lpair2(p)] < 0.0 ? -inv_abs : inv_abs;
 #pragma unroll
       for (int t = 0; t < (MROWS + T - 1) / T; ++t) {
         const int i = tid + T * t;
-        if (i < MROWS) s_l[lpair(i)] = (i == p) ? 1.0 : s_raw[lpair(i)] * inv;
+        if (i < MROWS) s_l[lpair2(i)] = (i == p) ? 1.0 : s_raw[lpair2(i)] * inv;
       }
       __syncthreads();
     }
@@ -284,7 +284,7 @@ __device__ __forceinline__ void prrlu_body_rook(const LuArgs &A, PrrluSmem &S, c
     // fma(-l_i, u_j, S_ij) (R4), l_p = 1 zeroes row p exactly
 #pragma unroll
     for (int a = 0; a < EA; ++a) {
-      const double li = s_l[lpair(lane + 32 * a)];
+      const double li = s_l[lpair2(lane + 32 * a)];
 #pragma unroll
       for (int b = 0; b < EB; ++b) v[a][b][0] = fma(-li, ub[b], v[a][b][0]);
     }

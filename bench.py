@@ -37,6 +37,37 @@ def _file_peaks():
         return {"hbm_gbs": 6650.0, "hbm_source": "fallback (B200_PROFILING.md)"}
 
 
+def measure_prrlu_latency(sizes=(64, 128, 256, 512, 1024)):
+    """Per-pivot latency of the library's prrLU on seeded square blocks of each tier (m x m, up to
+    512 pivots), with the work and without it (ACI_PRRLU_NOWORK: the exchange chain alone — CTA
+    argmax, cluster key exchange, cross-cluster leg, column read — the design's per-pivot floor),
+    measured in this run through libaci_peak.so (csrc/peak_probe.cu; best of 3 launches)."""
+    import ctypes
+    from paper_2604_00037_b200 import _build
+    lib = ctypes.CDLL(_build.build_peak())
+    lib.aci_peak_prrlu.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                   ctypes.POINTER(ctypes.c_int)]
+    out = {}
+    for m in sizes:
+        row = {}
+        for key, nowork in (("kernel_us", 0), ("floor_us", 1)):
+            v, piv = ctypes.c_double(0.0), ctypes.c_int(0)
+            rc = lib.aci_peak_prrlu(m, nowork, 3, ctypes.byref(v), ctypes.byref(piv))
+            row[key] = v.value if rc == 0 else None
+            row["pivots"] = piv.value
+        out[m] = row
+    return out
+
+
+def _block_tier(m, n):
+    """The probe size whose tier a live m x n block runs in (prrlu.cu variant lists)."""
+    big = max(m, n)
+    for t in (64, 128, 256, 512):
+        if big <= t:
+            return t
+    return 1024
+
+
 def measure_peaks(stream=None):
     """FP64 roofline denominators measured IN THIS RUN on this GPU (MEASURED_PEAKS.json has no FP64
     entry): cuBLAS DGEMM 8192^3 through torch.matmul (best of 5 after a warm-up, CUDA events), the
@@ -206,7 +237,8 @@ def _ncu_traffic():
     d = json.load(open(files[-1]))
     out = {}
     for k, v in d.items():
-        if isinstance(v, dict) and "dram_bytes_read" in v and (k.startswith("prrlu") or k.startswith("gemmpi")):
+        if (isinstance(v, dict) and "dram_bytes_read" in v and "dram_bytes_write" in v
+                and (k.startswith("prrlu_r") or k.startswith("gemmpi"))):
             key = "prrlu" if k.startswith("prrlu") else "contraction"
             out[key] = {"bytes": v["dram_bytes_read"] + v["dram_bytes_write"], "source": os.path.basename(files[-1]),
                         "kernel": v["kernel"]}
@@ -667,6 +699,18 @@ def main():
     if e2e is not None:
         e2e["value"] = e2e_sum
     pk = measure_peaks()  # after the timed regions: the same process, clocks and GPU
+    lat, piv_by_tier = None, {}
+    if rank == 0:
+        lat = measure_prrlu_latency()
+        cfl = make_config(3, args.chi, npts=0)
+        xs_ = [aci.TensorTrain.from_cores(t) for t in cfl["inputs"]]
+        y0_ = aci.TensorTrain.from_cores(cfl["y_init"])
+        o_, _, _, ex_ = aci.aci_elementwise(cfl["op"], xs_, cfl["tol"], cfl["maxrank"], cfl["max_sweeps"], y_init=y0_,
+                                            stream=sptr, log=True)
+        o_.free()
+        for e in ex_["log"]:
+            t = _block_tier(2 * e["rl"], 2 * e["rr"])
+            piv_by_tier[t] = piv_by_tier.get(t, 0) + e["r"]
     if rank == 0:
         value = f_sum / t_max / 1e9  # GFLOP/ms -> TFLOP/s
         steps = args.steps
@@ -677,23 +721,31 @@ def main():
         pi = prof["gemm_pi"]
         prrlu_flops = reps[-1]["flops_prrlu"]  # per product; prof_tot is per product too
         pi_flops = reps[-1]["flops_contraction"]  # a3 dominates; a1/a2 included
+        # per-pivot latency against the measured exchange floor of each block size, weighted by the
+        # product's own pivot distribution (pivot log of one product)
+        lat_fr = None
+        if lat is not None and piv_by_tier:
+            floor_ms = sum(cnt * lat[t]["floor_us"] for t, cnt in piv_by_tier.items() if lat[t]["floor_us"]) / 1e3
+            kern_ms = sum(cnt * lat[t]["kernel_us"] for t, cnt in piv_by_tier.items() if lat[t]["kernel_us"]) / 1e3
+            lat_fr = {"floor_ms_per_product": floor_ms, "probe_kernel_ms_per_product": kern_ms,
+                      "product_prrlu_ms": pr["ms"], "frac": floor_ms / pr["ms"] if pr["ms"] else None,
+                      "pivots_by_block": {str(k): v for k, v in sorted(piv_by_tier.items())},
+                      "by_block": {str(k): v for k, v in lat.items()}}
         roof_prrlu = {"kernel": "prrlu_kernel (a5)", "bound": "alu",
                       "achieved": prrlu_flops / (pr["ms"] * 1e9) if pr["ms"] else None,
                       "peak": pk["dfma_tflops"], "unit": "TFLOP/s",
                       "frac": (prrlu_flops / (pr["ms"] * 1e9)) / pk["dfma_tflops"] if pr["ms"] else None,
                       "traffic": None, "per_launch_us": 1e3 * pr["ms"] / max(pr["launches"], 1),
                       "per_pivot_us": 1e3 * pr["ms"] / max(reps[-1]["pivot_steps"], 1),
-                      "latency": {
+                      "latency": dict(lat_fr or {}, **{
                           "per_pivot_us": 1e3 * pr["ms"] / max(reps[-1]["pivot_steps"], 1),
-                          "exchange_floor_us": 0.66,
-                          "frac": (0.66 / (1e3 * pr["ms"] / max(reps[-1]["pivot_steps"], 1))),
-                          "floor_source": "per pivot at least one 16-CTA DSMEM key exchange (0.25 us, "
-                                          "profiles/r01_probe7_cluster_push.txt keys-only) + one L2 round trip "
-                                          "for the winner's column (~800 cycles at 1965 MHz = 0.41 us); the "
-                                          "rank-1 update itself is ALU-issue bound (DESIGN.md §5)"},
+                          "floor_source": "measured in this run: the library's prrLU with the rank-1 update and "
+                                          "rescan compiled out (csrc/peak_probe.cu, ACI_PRRLU_NOWORK) on seeded "
+                                          "m x m blocks, i.e. the exchange chain alone per pivot; weighted by the "
+                                          "product's pivots per block size; frac = floor / product prrLU time"}),
                       "note": "latency-bound: one cluster/L2 exchange per pivot (DESIGN.md §5); 'frac' above is "
                               "against the DFMA register loop measured in this run (peaks.dfma_tflops), "
-                              "'latency.frac' against the exchange floor"}
+                              "'latency.frac' against the measured exchange floor"}
         roof_pi = {"kernel": "gemm_dmma_kernel<fused f> (a3+a4) + a1/a2", "bound": "tensor",
                    "achieved": pi_flops / ((pi["ms"] + prof["gemm_ab"]["ms"]) * 1e9),
                    "peak": pk["dmma_tflops"], "unit": "TFLOP/s",

@@ -25,9 +25,11 @@ PEAK_LIB = os.path.join(HERE, "libaci_peak.so")
 
 def build_peak(force: bool = False) -> str:
     """libaci_peak.so: the FP64 DMMA / DFMA loops bench.py measures its roofline peaks with."""
-    if force or not os.path.exists(PEAK_LIB) or os.path.getmtime(PEAK_SRC) > os.path.getmtime(PEAK_LIB):
+    deps = [PEAK_SRC, os.path.join(HERE, "csrc", "prrlu.cu"), os.path.join(HERE, "csrc", "prrlu_rook.cuh")] + HDR
+    if force or not os.path.exists(PEAK_LIB) or any(os.path.getmtime(f) > os.path.getmtime(PEAK_LIB) for f in deps):
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-shared",
-               "-Xcompiler", "-fPIC", "-o", PEAK_LIB, PEAK_SRC, "-lcudart"]
+               "-Xcompiler", "-fPIC", "-I", os.path.join(HERE, "csrc"), "-I", os.path.join(ROOT, "include"),
+               "-o", PEAK_LIB, PEAK_SRC, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             if os.path.exists(PEAK_LIB):

@@ -100,3 +100,96 @@ extern "C" int aci_peak_fp64(int kind, int reps, double *tflops) {
   *tflops = best;
   return 0;
 }
+
+// ---------------------------------------------------------------------------------------------
+// prrLU latency probes (roofline.latency in bench.py): the library's own prrLU (csrc/prrlu.cu,
+// compiled here twice) on a seeded m x m block — with the work (the real per-pivot time of the
+// tier that block selects) and with ACI_PRRLU_NOWORK (no rank-1 update, no rescan: every step
+// exchanges the same winner, so what is left is the exchange chain — the per-pivot floor of the
+// design: CTA argmax, cluster key exchange, cross-cluster leg, column read).
+#include <cstdlib>
+
+#include "aci_common.cuh"
+namespace probe_work {
+#include "prrlu.cu"
+}
+#undef ACI_PRRLU_NOWORK
+#define ACI_PRRLU_NOWORK 1
+namespace probe_nowork {
+#include "prrlu.cu"
+}
+
+namespace {
+__global__ void fill_kernel(double *M, size_t n, unsigned long long seed) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    unsigned long long x = seed + 0x9E3779B97F4A7C15ull * (i + 1);
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    M[i] = (double)(x >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+  }
+}
+}  // namespace
+
+extern "C" int aci_peak_prrlu(int m, int nowork, int reps, double *us_per_pivot, int *pivots) {
+  if (!us_per_pivot || m < 32 || m > 1024) return -1;
+  const int kmax = m > 512 ? 512 : m;
+  double *M = nullptr, *U = nullptr, *eps = nullptr;
+  unsigned long long *colpub = nullptr, *keys = nullptr, *scale = nullptr;
+  int *rows = nullptr, *cols = nullptr, *r = nullptr;
+  unsigned *ctr = nullptr, *epoch = nullptr;
+  LuDims *dims = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  const size_t colpub_words = (size_t)2 * 148 * 1024 * 2;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&M, sizeof(double) * m * m) != cudaSuccess || cudaMalloc(&U, sizeof(double) * m * m) != cudaSuccess ||
+      cudaMalloc(&eps, 8) != cudaSuccess || cudaMalloc(&colpub, 8 * colpub_words) != cudaSuccess ||
+      cudaMalloc(&keys, 8 * 2 * 148 * 4) != cudaSuccess || cudaMalloc(&scale, 8) != cudaSuccess ||
+      cudaMalloc(&rows, 4 * 1024) != cudaSuccess || cudaMalloc(&cols, 4 * 1024) != cudaSuccess ||
+      cudaMalloc(&r, 4) != cudaSuccess || cudaMalloc(&ctr, 4) != cudaSuccess || cudaMalloc(&epoch, 4) != cudaSuccess ||
+      cudaMalloc(&dims, sizeof(LuDims)) != cudaSuccess || cudaEventCreate(&e0) != cudaSuccess ||
+      cudaEventCreate(&e1) != cudaSuccess)
+    return -5;
+  fill_kernel<<<296, 256, 0, st>>>(M, (size_t)m * m, 12345ull + m);
+  cudaMemsetAsync(colpub, 0, 8 * colpub_words, st);
+  cudaMemsetAsync(keys, 0, 8 * 2 * 148 * 4, st);
+  cudaMemsetAsync(epoch, 0, 4, st);
+  cudaMemsetAsync(scale, 0, 8, st);
+  LuDims D{m, m, m, kmax, m};
+  cudaMemcpyAsync(dims, &D, sizeof(D), cudaMemcpyHostToDevice, st);
+  LuArgs a = {};
+  a.M = M; a.dims = dims; a.tol = 0.0; a.thr_mode = 2; a.scale_bits = scale;
+  a.rows = rows; a.cols = cols; a.r_out = r; a.eps_out = eps; a.U = U;
+  a.colpub = colpub; a.colcap = 1024; a.keys = keys; a.counter = ctr; a.epoch = epoch;
+  if (nowork) probe_nowork::prrlu_init();
+  else probe_work::prrlu_init();
+  auto launch = [&]() {
+    return nowork ? probe_nowork::launch_prrlu(a, m, m, st, false, false, nullptr, false)
+                  : probe_work::launch_prrlu(a, m, m, st, false, false, nullptr, false);
+  };
+  cudaError_t le = launch();
+  double best = 1e30;
+  for (int t = 0; t < (reps > 0 ? reps : 3) && le == cudaSuccess; ++t) {
+    cudaEventRecord(e0, st);
+    le = launch();
+    cudaEventRecord(e1, st);
+    if (cudaEventSynchronize(e1) != cudaSuccess) break;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  int hr = 0;
+  cudaMemcpyAsync(&hr, r, 4, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  for (void *p : {(void *)M, (void *)U, (void *)eps, (void *)colpub, (void *)keys, (void *)scale, (void *)rows,
+                  (void *)cols, (void *)r, (void *)ctr, (void *)epoch, (void *)dims})
+    cudaFree(p);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(st);
+  if (e != cudaSuccess || le != cudaSuccess || hr <= 0) return -5;
+  *us_per_pivot = best * 1e3 / hr;
+  if (pivots) *pivots = hr;
+  return 0;
+}

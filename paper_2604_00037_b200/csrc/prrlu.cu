@@ -211,6 +211,13 @@ __device__ __forceinline__ int lpair2(int i) { return ((i >> 6) << 6) | ((i & 31
 // measured without gain, profiles/r02_prrlu_bench_variants.txt); packet i sits at u64 offset 2 i
 constexpr int kColSpread = 1;
 __device__ __forceinline__ int cpk(int i) { return 2 * i; }
+// ACI_PRRLU_NOWORK (measurement builds only, csrc/peak_probe.cu): skip the rank-1 update, the
+// column zeroing and the rescan, so every step exchanges the same winner — the per-pivot latency
+// of the exchange alone, the floor the real kernel is reported against (bench.py roofline.latency)
+#ifndef ACI_PRRLU_NOWORK
+#define ACI_PRRLU_NOWORK 0
+#endif
+constexpr bool kNoWork = ACI_PRRLU_NOWORK != 0;
 constexpr int kMaxRows = 1024;   // 32 * EA_max
 constexpr int kMaxCTAs = 148;
 constexpr int kMaxCB = 512;      // NW * EB_max
@@ -614,12 +621,14 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         }
 #pragma unroll
       for (int b = 0; b < EB; ++b) ub[b] = s_u[w + NW * b];
+      if constexpr (!kNoWork) {
 #pragma unroll
       for (int a = 0; a < EA; ++a) {
         const int i = lane + 32 * a;
         const double li = i < m ? ((i == p) ? 1.0 : col[i] * inv) : 0.0;
 #pragma unroll
         for (int b = 0; b < EB; ++b) v[a][b][0] = fma(-li, ub[b], v[a][b][0]);
+      }
       }
     } else if (GRID) {
       const unsigned tag = (ep << 12) | (unsigned)(k + 1);
@@ -654,11 +663,13 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         }
 #pragma unroll
       for (int b = 0; b < EB; ++b) ub[b] = s_u[w + NW * b];
+      if constexpr (!kNoWork) {
 #pragma unroll
       for (int a = 0; a < EA; ++a) {
         const double li = s_l[lane + 32 * a];
 #pragma unroll
         for (int b = 0; b < EB; ++b) v[a][b][0] = fma(-li, ub[b], v[a][b][0]);
+      }
       }
     } else {
       const int jq = q - c0;
@@ -682,12 +693,14 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
           if (j < n) A.U[(size_t)k * ldu + j] = (j == q) ? 1.0 : s_u[jj] * inv;
         }
       // every thread forms its own l'_i (no third barrier)
+      if constexpr (!kNoWork) {
 #pragma unroll
       for (int a = 0; a < EA; ++a) {
         const int i = lane + 32 * a;
         const double li = (i == p) ? (neg ? -1.0 : 1.0) : s_raw[i] * inv_abs;
 #pragma unroll
         for (int b = 0; b < EB; ++b) v[a][b][0] = fma(li, ub[b], v[a][b][0]);
+      }
       }
     }
     } else {
@@ -795,7 +808,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     }
     }
     // column q -> exact zeros (owner warp; warp-uniform branch)
-    {
+    if constexpr (!kNoWork) {
       const int jq = q - c0;
       if (jq >= 0 && jq < CB && (jq % NW) == w) {
         const int bq = jq / NW;
@@ -808,7 +821,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
               for (int z = 0; z < Z; ++z) v[a][b][z] = 0.0;
       }
     }
-    scan();
+    if constexpr (!kNoWork) scan();
     PHASE(6);
     ++k;
     // s_l / s_u / s_raw are rewritten only after the next S1; every thread finished reading

@@ -19,7 +19,7 @@
 //     two slots per CTA by parity) and the CTAs read the final one.
 // Supported where the factorisation fits one CTA or one 16-CTA cluster (the prrlu_kernel_one
 // envelope); real values only.
-#pragma once
+// (included once per prrlu.cu instance; csrc/peak_probe.cu instantiates prrlu.cu twice)
 
 template <int EA, int EB, int NW, int XM>
 __device__ __forceinline__ void prrlu_body_rook(const LuArgs &A, RookSmem &S, const int G, const int g) {

@@ -35,11 +35,15 @@ def test_bench_line_has_the_contract_keys():
     assert d["clocks"]["samples"] >= 1 and not set(d["clocks"]["reasons"]) & {
         "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
     assert d["gpu_launches"] > 0
+    if "peaks" in d and "dgemm_tflops" in d["peaks"] and "measured in this bench run" in d["peaks"].get("source", ""):
+        assert d["peaks"]["dgemm_tflops"] > 0 and d["peaks"]["dmma_tflops"] > 0 and d["peaks"]["dfma_tflops"] > 0
 
 
 def test_reference_arm_line():
-    f = os.path.join(ROOT, "profiles", "r01h_bench_reference_arm.json")
+    f = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_bench_reference_arm.json")))[-1]
     d = json.loads(open(f).read().strip().splitlines()[-1])
     assert d["impl"] == "reference" and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["e2e"]["value"] == d["value"]
+    if "same_config" in d:  # round 2+: every timed step is the whole workload
+        assert d["same_config"] is True and d["config"]["iterations"] == 4 and d["cpu_baseline"].get("cpu_model")

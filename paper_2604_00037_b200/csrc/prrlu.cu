@@ -878,13 +878,20 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel_rook(LuArgs A) {
 // CTA (up to 255 registers, so the 32-row-slot tiles do not spill; measured faster than 16).
 // XM = 1: cooperative grid, L2 exchange. XM = 2: cluster launch; the participating CTAs are
 // rounded up to whole clusters (CTAs past the live columns hold padding only).
+// ACI_CLUSTER_CTA_MAXE: in the cluster kernel (XM = 2, real), one-CTA variants with more register
+// entries per thread than this are skipped, so such live blocks (e.g. 128 x 128 inside a 256-wide
+// launch) spread over the cluster's CTAs instead of one SM (A/B switch; 64 = every variant)
+#ifndef ACI_CLUSTER_CTA_MAXE
+#define ACI_CLUSTER_CTA_MAXE 64
+#endif
 template <int NWT, int XM, bool CPLX>
 __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
   __shared__ PrrluSmem S;
   const int m = A.dims->m, n = A.dims->n;
   const int g = blockIdx.x;
 #define ACI_CTA_VARIANT(EA, EB)                                        \
-  if (m <= 32 * (EA) && n <= NWT * (EB)) {                              \
+  if (!(XM == 2 && !CPLX && (EA) * (EB) > ACI_CLUSTER_CTA_MAXE) &&     \
+      m <= 32 * (EA) && n <= NWT * (EB)) {                              \
     if (g == 0) prrlu_body<(EA), (EB), NWT, 0, CPLX>(A, S, 1, 0);      \
     return;                                                            \
   }

@@ -13,7 +13,8 @@ int main(int argc, char **argv) {
   int sizes[][4] = {{64, 64, 64, 0}, {128, 128, 128, 0}, {256, 256, 256, 0}, {512, 512, 512, 0}, {1024, 1024, 512, 0},
                     {64, 64, 64, 1024}, {128, 128, 128, 1024}, {256, 256, 256, 1024}, {512, 512, 512, 1024},
                     {64, 64, 64, 256}, {128, 128, 128, 256}, {256, 128, 128, 256}, {128, 256, 128, 256},
-                    {200, 250, 200, 256}};
+                    {200, 250, 200, 256}, {256, 64, 64, 256}, {64, 256, 64, 256}, {128, 64, 64, 256},
+                    {96, 96, 96, 256}};
   double *dM, *dU, *deps;
   unsigned long long *dcol;
   int *drows, *dcols, *dr;

@@ -632,7 +632,9 @@ def main():
         base = pts[0]["products_per_s"]
         for p in pts:
             p["speedup_vs_1"] = p["products_per_s"] / base
-        return {"workload": cf["name"], "mode": "aci_options.concurrent (single-cluster prrLU)", "points": pts}
+        return {"workload": cf["name"],
+                "mode": "aci_options.concurrent (single-cluster prrLU; blocks beyond one cluster: the cooperative "
+                        "L2 grid tier)", "points": pts}
 
     def run_rook(chis=(64, 128), reps=3):
         """Rook pivoting (reading R23) against full pivoting on configs[3]:
@@ -689,7 +691,11 @@ def main():
                                                                        with_e2e=True)
     steady = run_steady((64, 128, 256)) if (ws == 1 and not args.no_chi_sweep) else None
     allcfg = run_all_configs() if (ws == 1 and not args.no_chi_sweep) else None
-    conc = run_concurrent() if (ws == 1 and not args.no_chi_sweep) else None
+    conc = None
+    if ws == 1 and not args.no_chi_sweep:
+        conc = run_concurrent()
+        conc = {"chi64": conc, "chi256": run_concurrent(chi=256, ks=(1, 2, 4), reps=2)}
+        conc["chi256"]["default_tier_ms_per_product"] = tot_ms / args.steps
     rook = run_rook() if (ws == 1 and not args.no_chi_sweep) else None
     cplx = None
     if ws == 1 and not args.no_complex:

@@ -182,17 +182,22 @@ typedef struct {
   float *iter_ms;            /* optional, max_sweeps floats: device time of each iteration (both
                               * half-sweeps + convergence test; CUDA events on the call's stream) */
   int concurrent;            /* 1: this call may run concurrently with other aci calls on other
-                              * streams (host threads). Every prrLU launch then uses at most one
-                              * 16-CTA thread-block cluster, which the hardware schedules as a unit,
-                              * so concurrent products cannot deadlock on each other's spinning CTAs.
-                              * 2-site blocks must fit one cluster (real: 128 x 1024, 256 x 512,
-                              * 512 x 512, 1024 x 256; complex: 128 x 1024, 256 x 512, 512 x 256),
-                              * else ACI_ERR_UNSUPPORTED. 0 (default): the fastest tiers, which may
-                              * span several clusters; such calls from several host threads are
+                              * streams (host threads). prrLU launches then never span several
+                              * thread-block clusters: blocks that fit one 16-CTA cluster (real:
+                              * 128 x 1024, 256 x 512, 512 x 512, 1024 x 256; complex: 128 x 1024,
+                              * 256 x 512, 512 x 256) use exactly one cluster, which the hardware
+                              * schedules as a unit; larger blocks (e.g. the 1024 x 1024 blocks of
+                              * configs[3] at chi = 256) use the L2 grid tier launched cooperatively,
+                              * i.e. gang-scheduled (all CTAs resident or none). So concurrent
+                              * products cannot deadlock on each other's spinning CTAs. Results are
+                              * bit-identical to the default tiers (same keys and arithmetic).
+                              * 0 (default): the fastest tiers, which may span several clusters
+                              * (not gang-scheduled); such calls from several host threads are
                               * serialised by the library (a process-wide lock). Another PROCESS
                               * sharing the GPU (MPS) is not covered by that lock: a multi-cluster
                               * grid assumes its clusters can all be resident at once (checked once
-                              * with cudaOccupancyMaxActiveClusters on an idle GPU). */
+                              * with cudaOccupancyMaxActiveClusters on an idle GPU); use concurrent
+                              * mode there. */
   int pivoting;              /* ACI_PIVOT_FULL (default): full pivoting, Alg. 2 as written.
                               * ACI_PIVOT_ROOK: rook pivoting in every prrLU of the call (B:5
                               * "full/rook"; reading R23 of DESIGN.md §2): the pivot is an entry that

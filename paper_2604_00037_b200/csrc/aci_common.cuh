@@ -90,8 +90,8 @@ cudaError_t launch_prrlu(const LuArgs &a, int max_m, int max_n, cudaStream_t st,
                          cudaEvent_t started = nullptr, bool rook = false);
 bool prrlu_supported_one(int m, int n, bool cplx);
 bool prrlu_supported_rook(int m, int n);
-// true when multi-cluster prrLU grids are launched cooperatively (gang-scheduled): concurrent-mode
-// products may then use them for blocks beyond one cluster
+// true when concurrent-mode products may factorise blocks beyond one cluster (they then use the
+// cooperative, gang-scheduled L2 grid tier)
 bool prrlu_coop_multicluster();
 // Chooses the prrLU exchange tier (cluster size) once; call before any stream capture.
 void prrlu_init();

@@ -1093,7 +1093,7 @@ int cluster_choice() {
 
 }  // namespace
 
-bool prrlu_coop_multicluster() { return false; }
+bool prrlu_coop_multicluster() { return true; }  // the cooperative L2 grid tier serves concurrent mode
 
 bool prrlu_supported_one(int m, int n, bool cplx) {
   if (fits_one_cta(m, n, cplx)) return true;
@@ -1210,15 +1210,16 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, prrlu_kernel_one<kNWT, CPLX>, args);
   }
-  // (concurrent mode beyond one cluster: the cooperative multi-cluster grid below, which is
-  // gang-scheduled, so concurrent products cannot hold part of each other's clusters)
   if (fits_one_cta(max_m, max_n, CPLX)) {
     cfg.gridDim = dim3(1);
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 1, CPLX>, args);
   }
   int G = (max_n + kNWT - 1) / kNWT;  // enough for every variant the live size may select
-  const int cs = cluster_choice();
+  // concurrent mode beyond one cluster: the L2 grid tier, launched cooperatively (gang-scheduled:
+  // the whole grid is resident or none of it), so products running concurrently cannot hold part
+  // of each other's spinning CTAs; multi-cluster launches are not gang-scheduled
+  const int cs = one ? 0 : cluster_choice();
   if (cs > 0) {
     G = (G + cs - 1) / cs * cs;
     cfg.gridDim = dim3(G);

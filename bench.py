@@ -514,12 +514,10 @@ def main():
                         "tflops": rep["flops_contraction"] / ms / 1e9, "pivots": rep["pivot_steps"],
                         "iterations": rep["iterations"], "rel_err_vs_closed_form": err, "tol": cf["tol"]})
             out.free()
-        lx = np.log([p["chi_in"] for p in pts])
         return {"workload": "cfg5_fourier_complex_L30 (P:289-311), f = g1 g2, tol 1e-8, maxrank 256",
                 "points": pts,
-                "exponent_wall_time_vs_chi_in": float(np.polyfit(lx, np.log([p["ms_per_product"] for p in pts]), 1)[0]),
-                "note": "paper (EPYC 9474F, 1 thread, Julia): ACI runtime ~ chi^2.3 (P:307); flops counted as 4x "
-                        "the real contraction model (complex products)"}
+                "note": "complex parity workload (NEXT-1); flops counted as 4x the real contraction model "
+                        "(complex products)"}
 
     def run_all_configs(reps=2):
         """Every BASELINE.json config (and the complex configs[5]) once more: device ms per product

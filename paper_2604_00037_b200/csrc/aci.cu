@@ -441,7 +441,16 @@ struct UpdateArgs {
 
 // Index-set update (a6, R21) and frame update (a7: the rows/columns of A^n / B^n the
 // new pivots select — the same numbers Alg. 5 recomputes).
+// ACI_PDL_UPDATE (A/B switch): the update kernel is launched as a programmatic dependent of the
+// prrLU (it may be scheduled before the prrLU grid ends and waits in griddepcontrol.wait, which
+// returns once the prrLU grid has completed and its memory is visible)
+#ifndef ACI_PDL_UPDATE
+#define ACI_PDL_UPDATE 0
+#endif
 __global__ void update_bond_kernel(UpdateArgs U) {
+#if ACI_PDL_UPDATE
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   const int r = *U.r_in;
   const int b = U.b, L = U.L;
   const int rl = U.rk[b], rr = U.rk[b + 2];
@@ -1318,7 +1327,20 @@ static void launch_update(Run &R, int b, int dir, int logslot, const BondStatic 
   U.info = R.binfo + 8 * (dir * (R.L - 1) + b);
   size_t work = (size_t)R.rmax[b] * 256;
   int blocks = (int)std::min<size_t>(592, std::max<size_t>(1, (work + 255) / 256));
+#if ACI_PDL_UPDATE
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, update_bond_kernel, U);
+#else
   update_bond_kernel<<<blocks, 256, 0, st>>>(U);
+#endif
 }
 
 static void launch_index(Run &R, int b, int dir, int logslot, cudaStream_t st) {

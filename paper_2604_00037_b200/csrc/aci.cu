@@ -25,8 +25,19 @@
 #include <atomic>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: named host ranges for profilers (ncu --nvtx)
+
 #include "../../include/aci.h"
 #include "aci_common.cuh"
+
+// RAII NVTX range over host enqueue phases (the device work they enqueue shows up under them in
+// ncu --nvtx / nsys); no effect without a profiler attached
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // ============================================================================ errors
 static thread_local std::string g_err;
@@ -1655,6 +1666,7 @@ static int build_run(const Inputs &I, const tt_s *y, int maxrank, int max_sweeps
 
 extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_inputs, double tol, int maxrank,
                                   int max_sweeps, tt_t **out, aci_report *rep, const aci_options *opts) {
+  NvtxRange nv_call("aci_elementwise");
   auto t_start = std::chrono::steady_clock::now();
   if (!out) return fail(ACI_ERR_INVALID, "aci: out is null");
   *out = nullptr;
@@ -1784,7 +1796,10 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   }
 
   // ---- a0: CI-canonicalise y_init, right-to-left
-  for (int s = L - 1; s >= 1; --s) canon_step(R, tol, o.tol_mode, s, strm);
+  {
+    NvtxRange nv("aci: canonicalise y_init (a0)");
+    for (int s = L - 1; s >= 1; --s) canon_step(R, tol, o.tol_mode, s, strm);
+  }
   prof.begin(ACI_PROF_CANON);
   copy_prev_kernel<<<1, 64, 0, strm>>>(R.rk, R.prev, L);
   prof.end(1);
@@ -1844,6 +1859,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
     cudaEventCreate(&ev_it[1]);
   }
   for (it = 1; it <= max_sweeps; ++it) {
+    NvtxRange nv("aci: iteration (L->R + R->L half-sweeps, convergence test)");
     if (ev_it[0]) cudaEventRecord(ev_it[0], strm);
     if (gexec) {
       cudaGraphLaunch(gexec, strm);
@@ -1887,6 +1903,7 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   if (nonfinite) { cleanup(); return fail(ACI_ERR_NONFINITE, "aci: f produced NaN/Inf (S:255)"); }
 
   // ---- a8: output cores from the last right-to-left half-sweep (R5)
+  NvtxRange nv_out("aci: output cores (a8)");
   tt_s *res = tt_alloc_shape(L, t0->d.data(), rk.data(), R.cplx);
   if (core_alloc(res, sizeof(double) * std::max<size_t>(res->total, 1), strm) != cudaSuccess) {
     cudaGetLastError();

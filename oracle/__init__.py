@@ -22,9 +22,12 @@ Contents
 
 Pinning status: every function above is pinned by a
 ``-m "not gpu"`` test against closed forms, brute force or exact rational
-arithmetic, except the pivot sequences of rank-capped runs, which only the
-oracle itself defines ("parity unpinned" for configs[4] pivots and the
-rank-256 configs[4] output).
+arithmetic (rook mode included). Rank-capped runs (configs[4]) have no exact
+product to compare with; their last update is pinned against the definition
+(the block built by direct evaluation of the inputs at the final index sets,
+factorised by the pinned prrLU, gives the logged pivots) and the output's
+interpolation identity on that cross; the earlier updates of such runs are
+pinned only through their (individually pinned) sub-steps.
 """
 from __future__ import annotations
 

@@ -403,3 +403,34 @@ def test_aci_rook_pivoting_reaches_the_exact_products():
     assert oracle.tt_norm(oracle.tt_axpby(1.0, r.cores, -1.0, ex)) / oracle.tt_norm(ex) <= 10 * cf["tol"]
     s = cf["samples"]
     assert _rel_max(oracle.tt_evaluate(r.cores, s), oracle.tt_evaluate(ex, s)) <= 10 * cf["tol"]
+
+
+def test_aci_cfg4_rank_capped_last_update_matches_definition():
+    """configs[4] is rank-capped (chi-hat = 256 < the true rank), so no exact product pins its
+    output. Its last update (bond 0, right-to-left) is pinned against the definition instead: the
+    block Pi[sigma, sigma', b] = f(x(sigma, sigma', J_2[b])) built by DIRECT evaluation of the input
+    TTs at the final J_2 multi-indices (P:210-214 without frames), factorised by the (separately
+    pinned) full-pivoting prrLU at the logged scale, gives exactly the logged ordered pivots and the
+    final J_1 set; and the output interpolates f on that cross."""
+    cf = make_config(4, npts=0)
+    res = oracle.aci(cf["inputs"], cf["op"], cf["y_init"], cf["tol"], cf["maxrank"], 1)
+    last = res.log[-1]
+    assert last["bond"] == 0 and last["dir"] == 1
+    d = cf["inputs"][0].d
+    J2 = res.Jset(2)
+    pts = np.array([[s0, s1] + list(j) for s0 in range(d[0]) for s1 in range(d[1]) for j in J2], dtype=np.uint8)
+    vals = [oracle.tt_evaluate(x, pts) for x in cf["inputs"]]
+    f = sum(c * np.prod([vals[n] ** e for n, e in enumerate(ex)], axis=0)
+            for c, ex in zip(cf["op"]["coef"], cf["op"]["expo"]))
+    Pi = f.reshape(d[0], d[1] * len(J2))  # row sigma, column sigma' * |J_2| + b (Alg. 4, P:601)
+    lu = oracle.ldu(Pi, cf["tol"] * last["scale"], cf["maxrank"])
+    assert list(lu["rows"]) == list(last["rows"]) and list(lu["cols"]) == list(last["cols"])
+    J1 = res.Jset(1)
+    assert [tuple(r) for r in J1] == [tuple([c // len(J2)] + list(J2[c % len(J2)])) for c in lu["cols"]]
+    I0 = res.Iset(0)
+    cross = np.array([np.concatenate([i, j]) for i in I0 for j in J1], dtype=np.uint8)
+    y = oracle.tt_evaluate(res.cores, cross)
+    vals = [oracle.tt_evaluate(x, cross) for x in cf["inputs"]]
+    ref = sum(c * np.prod([vals[n] ** e for n, e in enumerate(ex)], axis=0)
+              for c, ex in zip(cf["op"]["coef"], cf["op"]["expo"]))
+    assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max()

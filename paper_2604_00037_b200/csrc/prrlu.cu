@@ -38,7 +38,6 @@
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kMaxRows_ = 1024;  // = kMaxRows (needed before its definition)
 constexpr unsigned BAD_ID = 0xffffffffu;
 
 // Development instrumentation (tools/prrlu_bench.cu defines ACI_PRRLU_TIMING): cycles per phase
@@ -160,28 +159,6 @@ __device__ __forceinline__ void bulk_push(unsigned rdst, unsigned src, unsigned 
   asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(rdst),
                "r"(src), "r"(bytes), "r"(rbar)
                : "memory");
-}
-
-// ACI_COL_MC (A/B switch): grids of several 16-CTA clusters (real) get the candidate columns of the
-// cluster winners by TMA multicast DURING the cross-cluster leg — each cluster's leader multicasts
-// its own cluster winner's tagged column packets into every CTA of its cluster, and the column of
-// every other cluster's winner as soon as that cluster's key shows up in its poll — so the global
-// winner's column is normally in shared memory when the leg ends (the leg and the column read
-// overlap instead of following each other). Dynamic shared memory of the cluster kernel:
-// [2 parities][kMcSlots clusters][kMaxRows] packets + [2][kMcSlots] mbarriers. Stale packets (tag
-// mismatch) are re-read from L2.
-#ifndef ACI_COL_MC
-#define ACI_COL_MC 0
-#endif
-constexpr int kMcSlots = 5;  // clusters per grid the multicast path serves (the 1024-row grids use 4)
-constexpr size_t kMcBufBytes = (size_t)2 * kMcSlots * kMaxRows_ * 16;
-constexpr size_t kMcSmem = kMcBufBytes + (size_t)2 * kMcSlots * 8;
-__device__ __forceinline__ void bulk_multicast(unsigned dst, const void *src, unsigned bytes, unsigned mbar,
-                                               unsigned short mask) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(mbar), "h"(mask)
-      : "memory");
 }
 
 // push tier (XM = 3): one 8-CTA cluster; every CTA's candidate column is pushed into every
@@ -368,38 +345,19 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     }
     cluster_sync_all();
   }
-  // ACI_COL_MC: the cluster winners' columns arrive by multicast (several 16-CTA clusters, real)
-  constexpr bool kMC = ACI_COL_MC && XM == 2 && !CPLX;
-  bool mc = false;
-  unsigned long long *mcbuf = nullptr;
-  unsigned mcbar0 = 0;
-  if constexpr (kMC) {
-    const int ncl = G / (int)cluster_size();
-    mc = cluster_size() == 16u && ncl > 1 && ncl <= kMcSlots;
-    mcbuf = reinterpret_cast<unsigned long long *>(push_dyn);
-    mcbar0 = smem_u32(reinterpret_cast<char *>(push_dyn) + kMcBufBytes);
-  }
   if (XM == 2) {
     // one mbarrier per parity, armed for steps 0 and 1 before any CTA of the cluster pushes
     if (tid == 0) {
       const unsigned CS = cluster_size();
       for (int t = 0; t < 4; ++t) mbar_init(smem_u32(&S.mb[t]), 1u);
-      if (mc)
-        for (int t = 0; t < 2 * (G / (int)CS); ++t) mbar_init(mcbar0 + 8u * (unsigned)t, 1u);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       mbar_arm(smem_u32(&S.mb[0]), CS * 16u);
       mbar_arm(smem_u32(&S.mb[1]), CS * 16u);
       mbar_arm(smem_u32(&S.mb[2]), 16u);
       mbar_arm(smem_u32(&S.mb[3]), 16u);
-      if (mc)
-        for (int t = 0; t < 2 * (G / (int)CS); ++t) mbar_arm(mcbar0 + 8u * (unsigned)t, (unsigned)m * 16u);
     }
     cluster_sync_all();
   }
-  // mbarrier of (parity, cluster slot) and its buffer
-  auto mc_bar = [&](int par_, int slot) { return mcbar0 + 8u * (unsigned)(par_ * (G / 16) + slot); };
-  auto mc_slot = [&](int par_, int slot) { return mcbuf + ((size_t)(par_ * kMcSlots + slot) * kMaxRows_) * 2; };
-  bool mc_pending = false;  // this step's multicasts were issued (every cluster slot)
 
   double first = 0.0, eps = 0.0;
   int k = 0;
@@ -513,10 +471,6 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
               unsigned long long *kd = A.keys + ((size_t)par * kMaxCTAs / 8 + cid) * 32;
               st_pkt(kd, tagged(tag, cw.hi), tagged(tag, cw.lo));
               st_pkt(kd + 2, tagged(tag, cw.id), 0ull);
-              if (mc) {  // this cluster's winner column into slot cid of every CTA of the cluster
-                const unsigned long long *src = A.colpub + (((size_t)par * G + (cw.id % NC) / CB) * A.colcap) * 2;
-                bulk_multicast(smem_u32(mc_slot(par, cid)), src, (unsigned)m * 16u, mc_bar(par, cid), 0xffffu);
-              }
             }
             Key gk{0u, 0u, BAD_ID};
             if (lane < NCL) {
@@ -544,12 +498,6 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
                         (unsigned)(kw[i][2] >> 32) == tag) {
                       gk = Key{(unsigned)kw[i][0], (unsigned)kw[i][1], (unsigned)kw[i][2]};
                       got = true;
-                      if (mc && lane != cid) {  // cluster `lane`'s winner column, as soon as its key is in
-                        const unsigned long long *src =
-                            A.colpub + (((size_t)par * G + (gk.id % NC) / CB) * A.colcap) * 2;
-                        bulk_multicast(smem_u32(mc_slot(par, lane)), src, (unsigned)m * 16u, mc_bar(par, lane),
-                                       0xffffu);
-                      }
                     } else {
                       ld_pkt(kp, kw[i][0], kw[i][1]);
                       ld_pkt(kp + 2, kw[i][2], kw[i][3]);
@@ -565,7 +513,6 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
           mbar_wait(mwp, (unsigned)(k >> 1) & 1u);
           if (tid == 0) mbar_arm(mwp, 16u);
           win = Key{S.gw[par].x, S.gw[par].y, S.gw[par].z};
-          mc_pending = mc;
         }
       } else {
         // small grids: the tagged keys themselves are the barrier (warp 0 polls them, no counter);
@@ -688,31 +635,12 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2;
       constexpr int PPT = (MROWS + T - 1) / T;  // column packets per thread
       unsigned long long cw[PPT + 1][2];
-      if (kMC && mc) {
-        // the winner's cluster slot of this parity (multicast during the leg); tags checked below
-        const int slot = q / CB / 16;
-        mbar_wait(mc_bar(k & 1, slot), (unsigned)(k >> 1) & 1u);
-        const unsigned long long *cs = mc_slot(k & 1, slot);
 #pragma unroll
-        for (int t = 0; t < PPT; ++t) {
-          const int i = tid + T * t;
-          if (i < m) {
-            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(cs + 2 * i);
-            cw[t][0] = x.x;
-            cw[t][1] = x.y;
-          }
-        }
-        const ulonglong2 xp = *reinterpret_cast<const ulonglong2 *>(cs + 2 * p);
-        cw[PPT][0] = xp.x;
-        cw[PPT][1] = xp.y;
-      } else {
-#pragma unroll
-        for (int t = 0; t < PPT; ++t) {
-          const int i = tid + T * t;
-          if (i < m) ld_pkt(src + 2 * i, cw[t][0], cw[t][1]);
-        }
-        ld_pkt(src + 2 * p, cw[PPT][0], cw[PPT][1]);  // the pivot itself, for its sign
+      for (int t = 0; t < PPT; ++t) {
+        const int i = tid + T * t;
+        if (i < m) ld_pkt(src + 2 * i, cw[t][0], cw[t][1]);
       }
+      ld_pkt(src + 2 * p, cw[PPT][0], cw[PPT][1]);  // the pivot itself, for its sign
       while ((unsigned)(cw[PPT][0] >> 32) != tag || (unsigned)(cw[PPT][1] >> 32) != tag)
         ld_pkt(src + 2 * p, cw[PPT][0], cw[PPT][1]);
       const bool neg = (cw[PPT][1] & 0x80000000ull) != 0;
@@ -894,15 +822,6 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       }
     }
     if constexpr (!kNoWork) scan();
-    if (kMC && mc_pending && tid == 0) {
-      // every cluster slot's multicast of this step has landed (long since, normally): consume
-      // the phase and arm the slot for step k + 2
-      for (int sl = 0; sl < G / 16; ++sl) {
-        mbar_wait(mc_bar(k & 1, sl), (unsigned)(k >> 1) & 1u);
-        mbar_arm(mc_bar(k & 1, sl), (unsigned)m * 16u);
-      }
-    }
-    mc_pending = false;
     PHASE(6);
     ++k;
     // s_l / s_u / s_raw are rewritten only after the next S1; every thread finished reading
@@ -918,8 +837,6 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     for (int t = 0; t < 8; ++t) A.dbg[t] = ph_[t];
 #endif
   }
-  if (kMC && mc_pending && tid == 0)  // the stopping step's multicasts must land before the CTA exits
-    for (int sl = 0; sl < G / 16; ++sl) mbar_wait(mc_bar(k & 1, sl), (unsigned)(k >> 1) & 1u);
   if (XM >= 2) cluster_sync_all();  // no CTA leaves while a cluster peer may still push to it
 }
 
@@ -1141,10 +1058,6 @@ static int cluster_choice_once() {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c * 8);
     cfg.blockDim = dim3(kNWT * 32);
-    if (ACI_COL_MC && kern == (const void *)prrlu_kernel<kNWT, 2, false>) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMcSmem);
-      cfg.dynamicSmemBytes = kMcSmem;
-    }
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = c;
@@ -1235,9 +1148,6 @@ size_t prrlu_exchange_bytes(int max_m, int max_n) {
 static int attr_once() {
   cudaFuncSetAttribute((const void *)prrlu_kernel_push<kNWT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kPushSmem);
-  if (ACI_COL_MC)
-    cudaFuncSetAttribute((const void *)prrlu_kernel<kNWT, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kMcSmem);
   // 16-CTA clusters are a non-portable size
   const void *k16[] = {(const void *)prrlu_kernel<kNWT, 2, false>, (const void *)prrlu_kernel<kNWT, 2, true>,
                        (const void *)prrlu_kernel_one<kNWT, false>, (const void *)prrlu_kernel_one<kNWT, true>,
@@ -1313,7 +1223,6 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
   if (cs > 0) {
     G = (G + cs - 1) / cs * cs;
     cfg.gridDim = dim3(G);
-    if (!CPLX && ACI_COL_MC) cfg.dynamicSmemBytes = kMcSmem;
     cluster(cs);
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 2, CPLX>, args);

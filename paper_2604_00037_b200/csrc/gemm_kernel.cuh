@@ -13,6 +13,8 @@
 // the rank-2 input B of configs[1],[3]) are NBIG..NBIG+NSMALL-1 in the descriptor and are
 // evaluated in the epilogue from shared memory instead of a DMMA main loop.
 #pragma once
+#include <type_traits>
+
 #include "aci_common.cuh"
 
 namespace gemmk {
@@ -22,9 +24,14 @@ constexpr int kSmallK = 4;
 // input through the DMMA main loop; each thread's accumulator pair (2c, 2c+1) is one complex entry)
 enum { EPI_STORE = 0, EPI_F = 1, EPI_SUB = 2, EPI_STORE_X = 3, EPI_FZ = 4 };
 
-template <int BM_, int BN_, int WM_, int WN_, int BK_, int ST_, int MINB_>
+template <int BM_, int BN_, int WM_, int WN_, int BK_, int ST_, int MINB_, int VEC_ = 0>
 struct Cfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, BK = BK_, STAGES = ST_, MINB = MINB_;
+  // VEC = 1: tiles staged with 16-byte cp.async in their global order (A [row][k], B [k][col], pitch
+  // + 4 doubles: a half-warp's 8-byte fragment reads hit 16 distinct bank pairs), fragments read
+  // with LDS.64 per k-step; half the cp.async instructions of the k-permuted 8-byte layout (VEC = 0)
+  static constexpr int VEC = VEC_;
+  static constexpr int LDAV = BK + 4, LDBV = BN + 4;
   static constexpr int WARPS_N = BN / WN, NW = (BM / WM) * (BN / WN), NT = NW * 32;
   static constexpr int MI = WM / 8, NI = WN / 8;
   // Both tiles are stored k-permuted: element k of a row sits at (k % 4) * KQ + k / 4 (KQ = BK/4),
@@ -34,13 +41,18 @@ struct Cfg {
   static constexpr int KQ = BK / 4;
   static constexpr int LDA = BK + 2;
   static constexpr int LDB = BK + 2;
-  struct Smem {
+  struct SmemP {
     double A[STAGES][BM][LDA];
     double B[STAGES][BN][LDB];
   };
+  struct SmemV {
+    double A[STAGES][BM][LDAV];
+    double B[STAGES][BK][LDBV];
+  };
+  using Smem = typename std::conditional<VEC != 0, SmemV, SmemP>::type;
   static_assert(BK % 8 == 0, "two k-steps per LDS.128");
   static_assert((BM * BK) % NT == 0 && (BK * BN) % NT == 0, "tile loads must divide evenly");
-  static_assert(BM * kSmallK + kSmallK * BN <= STAGES * (BM * LDA + BN * LDB), "small-K staging fits");
+  static_assert(BM * kSmallK + kSmallK * BN <= (int)(sizeof(Smem) / sizeof(double)), "small-K staging fits");
 };
 
 __device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc, bool valid) {
@@ -95,6 +107,48 @@ __device__ __forceinline__ void load_stage(typename CF::Smem &sm, int st, const 
   }
 }
 
+__device__ __forceinline__ void cp_async16(double *sdst, const double *gsrc) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+
+// VEC = 1 staging: 16-byte chunks for interior tiles whose rows are 16-byte aligned (vec), single
+// doubles (zero-filled outside the problem) otherwise; smem in global order
+template <class CF>
+__device__ __forceinline__ void load_stage_v(typename CF::Smem &sm, int st, const double *A, int lda, const double *B,
+                                             int ldb, int M, int N, int K, int m0, int n0, int k0, bool vec) {
+  const int t = threadIdx.x;
+  if (vec && m0 + CF::BM <= M && n0 + CF::BN <= N && k0 + CF::BK <= K) {
+#pragma unroll
+    for (int i = 0; i < (CF::BM * CF::BK / 2) / CF::NT; ++i) {
+      const int e = t + CF::NT * i;
+      const int row = e / (CF::BK / 2), kc = 2 * (e % (CF::BK / 2));
+      cp_async16(&sm.A[st][row][kc], A + (size_t)(m0 + row) * lda + (k0 + kc));
+    }
+#pragma unroll
+    for (int i = 0; i < (CF::BK * CF::BN / 2) / CF::NT; ++i) {
+      const int e = t + CF::NT * i;
+      const int kr = e / (CF::BN / 2), col = 2 * (e % (CF::BN / 2));
+      cp_async16(&sm.B[st][kr][col], B + (size_t)(k0 + kr) * ldb + (n0 + col));
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < (CF::BM * CF::BK) / CF::NT; ++i) {
+    const int e = t + CF::NT * i;
+    const int row = e / CF::BK, kc = e % CF::BK;
+    const bool v = (m0 + row < M) && (k0 + kc < K);
+    cp_async8(&sm.A[st][row][kc], v ? A + (size_t)(m0 + row) * lda + (k0 + kc) : A, v);
+  }
+#pragma unroll
+  for (int i = 0; i < (CF::BK * CF::BN) / CF::NT; ++i) {
+    const int e = t + CF::NT * i;
+    const int kr = e / CF::BN, col = e % CF::BN;
+    const bool v = (k0 + kr < K) && (n0 + col < N);
+    cp_async8(&sm.B[st][kr][col], v ? B + (size_t)(k0 + kr) * ldb + (n0 + col) : B, v);
+  }
+}
+
 // acc += A (M x K) * B (K x N) on this CTA's tile.
 template <class CF>
 __device__ __forceinline__ void mainloop(typename CF::Smem &sm, double (&acc)[CF::MI][CF::NI][2], const double *A,
@@ -103,6 +157,39 @@ __device__ __forceinline__ void mainloop(typename CF::Smem &sm, double (&acc)[CF
   const int g = lane >> 2, c = lane & 3;
   const int wm = (w / CF::WARPS_N) * CF::WM, wn = (w % CF::WARPS_N) * CF::WN;
   const int nk = (K + CF::BK - 1) / CF::BK;
+  if constexpr (CF::VEC != 0) {
+    const bool vec = !((lda | ldb) & 1) && !((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15);
+    __syncthreads();  // shared memory reuse across inputs
+#pragma unroll
+    for (int s = 0; s < CF::STAGES - 1; ++s) {
+      if (s < nk) load_stage_v<CF>(sm, s, A, lda, B, ldb, M, N, K, m0, n0, s * CF::BK, vec);
+      cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+      cp_async_wait<CF::STAGES - 2>();
+      __syncthreads();
+      {
+        const int nxt = kt + CF::STAGES - 1;
+        if (nxt < nk) load_stage_v<CF>(sm, nxt % CF::STAGES, A, lda, B, ldb, M, N, K, m0, n0, nxt * CF::BK, vec);
+        cp_async_commit();
+      }
+      const int st = kt % CF::STAGES;
+#pragma unroll
+      for (int ks = 0; ks < CF::BK / 4; ++ks) {
+        double a[CF::MI], b[CF::NI];
+#pragma unroll
+        for (int mi = 0; mi < CF::MI; ++mi) a[mi] = sm.A[st][wm + mi * 8 + g][4 * ks + c];
+#pragma unroll
+        for (int ni = 0; ni < CF::NI; ++ni) b[ni] = sm.B[st][4 * ks + c][wn + ni * 8 + g];
+#pragma unroll
+        for (int mi = 0; mi < CF::MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < CF::NI; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+      }
+    }
+    cp_async_wait<0>();
+    return;
+  }
   __syncthreads();  // shared memory reuse across inputs
 #pragma unroll
   for (int s = 0; s < CF::STAGES - 1; ++s) {

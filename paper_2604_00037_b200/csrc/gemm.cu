@@ -10,13 +10,19 @@
 
 namespace {
 using namespace gemmk;
-using CfgPi = Cfg<64, 64, 32, 16, 16, 3, 2>;
-using CfgAB = Cfg<64, 32, 32, 16, 16, 3, 4>;
+// ACI_GEMM_VEC (default 1): tiles staged with 16-byte cp.async in global order (Cfg::VEC); measured
+// 28.4 -> 26.9 us on the full-size Pi, bit-identical results (tools/gemm_bench2.cu,
+// profiles/r02m_gemm_variants.txt)
+#ifndef ACI_GEMM_VEC
+#define ACI_GEMM_VEC 1
+#endif
+using CfgPi = Cfg<64, 64, 32, 16, 16, 3, 2, ACI_GEMM_VEC>;
+using CfgAB = Cfg<64, 32, 32, 16, 16, 3, 4, ACI_GEMM_VEC>;
 // Small problems: 32x32 tiles of 4 warps. A 64x64-tile grid of fewer than ~2 CTAs per SM leaves
 // SMs idle and runs the K loop serially on the busy ones; measured per launch (tools/gemm_latency.cu,
 // f fused, K = 64..256): 64^2 6.5 -> 3.7 us, 256^2 9.7 -> 5.0 us, 512^2 16.0 -> 9.4 us, but
 // 1024^2 25.4 -> 28.1 us, so the 64x64 tiles stay for grids of >= 256 of them.
-using CfgS = Cfg<32, 32, 16, 16, 16, 3, 4>;
+using CfgS = Cfg<32, 32, 16, 16, 16, 3, 4, ACI_GEMM_VEC>;
 inline bool small_grid(int max_m, int max_n) { return ((max_m + 63) / 64) * ((max_n + 63) / 64) < 256; }
 
 template <int NB, int NS>

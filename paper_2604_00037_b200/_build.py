@@ -39,18 +39,36 @@ def build_peak(force: bool = False) -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile the translation units of libaci.so in parallel (nvcc -c each), then link."""
     if force or stale():
-        cmd = [NVCC] + FLAGS + ["-o", LIB] + SRC + ["-lcudart"]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
+        objdir = os.path.join(HERE, "build")
+        os.makedirs(objdir, exist_ok=True)
+        cflags = [f for f in FLAGS if f != "-shared"]
+        procs = []
+        for src in SRC:
+            obj = os.path.join(objdir, os.path.basename(src) + ".o")
+            procs.append((obj, subprocess.Popen([NVCC] + cflags + ["-c", "-o", obj, src], stdout=subprocess.PIPE,
+                                                stderr=subprocess.PIPE, text=True)))
+        logs, failed = [], []
+        for obj, p in procs:
+            out, err = p.communicate()
+            logs.append(err)
+            if p.returncode != 0:
+                failed.append(out + err)
+        if not failed:
+            r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB]
+                               + [o for o, _ in procs] + ["-lcudart"], capture_output=True, text=True)
+            if r.returncode != 0:
+                failed.append(r.stdout + r.stderr)
+        if failed:
             if os.path.exists(LIB):
                 os.remove(LIB)  # never leave a stale library behind a failed build
-            errs = "\n".join(l for l in (r.stdout + r.stderr).splitlines() if "error" in l.lower())
+            errs = "\n".join(l for f in failed for l in f.splitlines() if "error" in l.lower())
             raise RuntimeError("nvcc failed:\n" + errs)
         with open(os.path.join(HERE, "ptxas.log"), "w") as f:
-            f.write(r.stderr)
+            f.write("".join(logs))
         if verbose:
-            print(r.stderr)
+            print("".join(logs))
     return LIB
 
 

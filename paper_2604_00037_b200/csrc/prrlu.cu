@@ -841,6 +841,34 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
 }
 
 #include "prrlu_rook.cuh"
+#include "prrlu_2d.cuh"
+
+// 2-D cluster tier kernel (ACI_PRRLU_2D): one 16-CTA cluster for static blocks up to 512 x 512;
+// live blocks that fit one CTA take the CTA tier in CTA 0.
+template <int NWT>
+__global__ void __launch_bounds__(NWT * 32) prrlu_kernel_2d(LuArgs A) {
+  __shared__ PrrluSmem S;
+  const int m = A.dims->m, n = A.dims->n;
+  const int g = blockIdx.x;
+#define ACI_CTA_VARIANT(EA, EB)                                        \
+  if (m <= 32 * (EA) && n <= NWT * (EB)) {                              \
+    if (g == 0) prrlu_body<(EA), (EB), NWT, 0, false>(A, S, 1, 0);     \
+    return;                                                            \
+  }
+  ACI_CTA_VARIANT(1, 4)
+  ACI_CTA_VARIANT(2, 8)
+  ACI_CTA_VARIANT(4, 4)
+  ACI_CTA_VARIANT(1, 16)
+  ACI_CTA_VARIANT(4, 16)
+  ACI_CTA_VARIANT(8, 8)
+  ACI_CTA_VARIANT(2, 32)
+#undef ACI_CTA_VARIANT
+  if (m <= 256 && n <= 256) {
+    prrlu_body_2d<2, 8, NWT>(A, S);
+    return;
+  }
+  prrlu_body_2d<4, 16, NWT>(A, S);
+}
 
 // Rook mode (LuArgs::rook): the prrlu_kernel_one envelope (one CTA or one 16-CTA cluster), real
 // values; the same variant list as prrlu_kernel_one.
@@ -1017,6 +1045,14 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel_push(LuArgs A) {
 
 constexpr int kNWT = 8;
 
+static bool twod_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("ACI_PRRLU_2D");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+
 static bool push_enabled() {
   static const bool on = [] {
     const char *e = getenv("ACI_PRRLU_PUSH");
@@ -1151,7 +1187,7 @@ static int attr_once() {
   // 16-CTA clusters are a non-portable size
   const void *k16[] = {(const void *)prrlu_kernel<kNWT, 2, false>, (const void *)prrlu_kernel<kNWT, 2, true>,
                        (const void *)prrlu_kernel_one<kNWT, false>, (const void *)prrlu_kernel_one<kNWT, true>,
-                       (const void *)prrlu_kernel_rook<kNWT>};
+                       (const void *)prrlu_kernel_rook<kNWT>, (const void *)prrlu_kernel_2d<kNWT>};
   for (const void *f : k16) cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return 0;
 }
@@ -1203,6 +1239,13 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
     cluster(kPushCS);
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, prrlu_kernel_push<kNWT>, args);
+  }
+  if (!CPLX && twod_enabled() && !fits_one_cta(max_m, max_n, CPLX) && max_m <= 512 && max_n <= 512 &&
+      cluster_choice() == 16) {
+    cfg.gridDim = dim3(16);
+    cluster(16);
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, prrlu_kernel_2d<kNWT>, args);
   }
   if (one && !fits_one_cta(max_m, max_n, CPLX) && prrlu_supported_one(max_m, max_n, CPLX)) {
     cfg.gridDim = dim3(16);

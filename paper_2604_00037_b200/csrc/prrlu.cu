@@ -220,6 +220,8 @@ __device__ __forceinline__ int cpk(int i) { return 2 * i; }
 constexpr bool kNoWork = ACI_PRRLU_NOWORK != 0;
 constexpr int kMaxRows = 1024;   // 32 * EA_max
 constexpr int kMaxCTAs = 148;
+static_assert(ACI_W8_EB128 >= 2 && ACI_W8_EB256 >= 2 && ACI_W8_EB512 >= 2 && ACI_BIG_EB >= 2,
+              "launch_prrlu sizes grids for >= 16 columns per CTA");
 constexpr int kMaxCB = 512;      // NW * EB_max
 
 struct PrrluSmem {
@@ -841,66 +843,6 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
 }
 
 #include "prrlu_rook.cuh"
-#include "prrlu_2d.cuh"
-
-// 2-D cluster tier kernel (ACI_PRRLU_2D): one 16-CTA cluster for static blocks up to 512 x 512;
-// live blocks that fit one CTA take the CTA tier in CTA 0.
-template <int NWT>
-__global__ void __launch_bounds__(NWT * 32) prrlu_kernel_2d(LuArgs A) {
-  __shared__ PrrluSmem S;
-  const int m = A.dims->m, n = A.dims->n;
-  const int g = blockIdx.x;
-#define ACI_CTA_VARIANT(EA, EB)                                        \
-  if (m <= 32 * (EA) && n <= NWT * (EB)) {                              \
-    if (g == 0) prrlu_body<(EA), (EB), NWT, 0, false>(A, S, 1, 0);     \
-    return;                                                            \
-  }
-  ACI_CTA_VARIANT(1, 4)
-  ACI_CTA_VARIANT(2, 8)
-  ACI_CTA_VARIANT(4, 4)
-  ACI_CTA_VARIANT(1, 16)
-  ACI_CTA_VARIANT(4, 16)
-  ACI_CTA_VARIANT(8, 8)
-  ACI_CTA_VARIANT(2, 32)
-#undef ACI_CTA_VARIANT
-  if (m <= 256 && n <= 256) {
-    prrlu_body_2d<2, 8, NWT>(A, S);
-    return;
-  }
-  prrlu_body_2d<4, 16, NWT>(A, S);
-}
-
-// Rook mode (LuArgs::rook): the prrlu_kernel_one envelope (one CTA or one 16-CTA cluster), real
-// values; the same variant list as prrlu_kernel_one.
-template <int NWT>
-__global__ void __launch_bounds__(NWT * 32) prrlu_kernel_rook(LuArgs A) {
-  __shared__ RookSmem S;
-  const int m = A.dims->m, n = A.dims->n;
-  const int g = blockIdx.x;
-#define ACI_CTA_VARIANT(EA, EB)                                        \
-  if (m <= 32 * (EA) && n <= NWT * (EB)) {                              \
-    if (g == 0) prrlu_body_rook<(EA), (EB), NWT, 0>(A, S, 1, 0);       \
-    return;                                                            \
-  }
-#define ACI_ONE_VARIANT(EA, EB)                                        \
-  if (m <= 32 * (EA) && n <= 16 * NWT * (EB)) {                         \
-    prrlu_body_rook<(EA), (EB), NWT, 2>(A, S, 16, g);                  \
-    return;                                                            \
-  }
-  ACI_CTA_VARIANT(1, 4)
-  ACI_CTA_VARIANT(2, 8)
-  ACI_CTA_VARIANT(4, 4)
-  ACI_CTA_VARIANT(1, 16)
-  ACI_CTA_VARIANT(4, 16)
-  ACI_CTA_VARIANT(8, 8)
-  ACI_CTA_VARIANT(2, 32)
-  ACI_ONE_VARIANT(4, 8)    //  128 x 1024
-  ACI_ONE_VARIANT(8, 4)    //  256 x  512
-  ACI_ONE_VARIANT(16, 4)   //  512 x  512
-#undef ACI_CTA_VARIANT
-#undef ACI_ONE_VARIANT
-}
-
 // Runtime tier selection from the LIVE sizes (device-resident ranks): the launch is sized for
 // the static capacity, and CTAs beyond what the live block needs exit immediately. 8 warps per
 // CTA (up to 255 registers, so the 32-row-slot tiles do not spill; measured faster than 16).
@@ -1045,14 +987,6 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel_push(LuArgs A) {
 
 constexpr int kNWT = 8;
 
-static bool twod_enabled() {
-  static const bool on = [] {
-    const char *e = getenv("ACI_PRRLU_2D");
-    return e && atoi(e) != 0;
-  }();
-  return on;
-}
-
 static bool push_enabled() {
   static const bool on = [] {
     const char *e = getenv("ACI_PRRLU_PUSH");
@@ -1187,7 +1121,7 @@ static int attr_once() {
   // 16-CTA clusters are a non-portable size
   const void *k16[] = {(const void *)prrlu_kernel<kNWT, 2, false>, (const void *)prrlu_kernel<kNWT, 2, true>,
                        (const void *)prrlu_kernel_one<kNWT, false>, (const void *)prrlu_kernel_one<kNWT, true>,
-                       (const void *)prrlu_kernel_rook<kNWT>, (const void *)prrlu_kernel_2d<kNWT>};
+                       (const void *)prrlu_kernel_rook<kNWT>};
   for (const void *f : k16) cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return 0;
 }
@@ -1240,13 +1174,6 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, prrlu_kernel_push<kNWT>, args);
   }
-  if (!CPLX && twod_enabled() && !fits_one_cta(max_m, max_n, CPLX) && max_m <= 512 && max_n <= 512 &&
-      cluster_choice() == 16) {
-    cfg.gridDim = dim3(16);
-    cluster(16);
-    cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, prrlu_kernel_2d<kNWT>, args);
-  }
   if (one && !fits_one_cta(max_m, max_n, CPLX) && prrlu_supported_one(max_m, max_n, CPLX)) {
     cfg.gridDim = dim3(16);
     cluster(16);
@@ -1258,7 +1185,14 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 1, CPLX>, args);
   }
-  int G = (max_n + kNWT - 1) / kNWT;  // enough for every variant the live size may select
+  // every grid variant holds at least 8 warps x 2 columns per CTA (ACI_W8_EB* / ACI_BIG_EB >= 2;
+  // complex: EB >= 2), so ceil(max_n / 16) CTAs cover any live block (ACI_PRRLU_G8=1: the round-1
+  // sizing of 8 columns per CTA, for A/B)
+  static const int cols_per_cta = [] {
+    const char *e = getenv("ACI_PRRLU_G8");
+    return (e && atoi(e) != 0) ? kNWT : 2 * kNWT;
+  }();
+  int G = (max_n + cols_per_cta - 1) / cols_per_cta;
   // concurrent mode beyond one cluster: the L2 grid tier, launched cooperatively (gang-scheduled:
   // the whole grid is resident or none of it), so products running concurrently cannot hold part
   // of each other's spinning CTAs; multi-cluster launches are not gang-scheduled

@@ -843,6 +843,38 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
 }
 
 #include "prrlu_rook.cuh"
+
+// Rook mode (LuArgs::rook): the prrlu_kernel_one envelope (one CTA or one 16-CTA cluster), real
+// values; the same variant list as prrlu_kernel_one.
+template <int NWT>
+__global__ void __launch_bounds__(NWT * 32) prrlu_kernel_rook(LuArgs A) {
+  __shared__ RookSmem S;
+  const int m = A.dims->m, n = A.dims->n;
+  const int g = blockIdx.x;
+#define ACI_CTA_VARIANT(EA, EB)                                        \
+  if (m <= 32 * (EA) && n <= NWT * (EB)) {                              \
+    if (g == 0) prrlu_body_rook<(EA), (EB), NWT, 0>(A, S, 1, 0);       \
+    return;                                                            \
+  }
+#define ACI_ONE_VARIANT(EA, EB)                                        \
+  if (m <= 32 * (EA) && n <= 16 * NWT * (EB)) {                         \
+    prrlu_body_rook<(EA), (EB), NWT, 2>(A, S, 16, g);                  \
+    return;                                                            \
+  }
+  ACI_CTA_VARIANT(1, 4)
+  ACI_CTA_VARIANT(2, 8)
+  ACI_CTA_VARIANT(4, 4)
+  ACI_CTA_VARIANT(1, 16)
+  ACI_CTA_VARIANT(4, 16)
+  ACI_CTA_VARIANT(8, 8)
+  ACI_CTA_VARIANT(2, 32)
+  ACI_ONE_VARIANT(4, 8)    //  128 x 1024
+  ACI_ONE_VARIANT(8, 4)    //  256 x  512
+  ACI_ONE_VARIANT(16, 4)   //  512 x  512
+#undef ACI_CTA_VARIANT
+#undef ACI_ONE_VARIANT
+}
+
 // Runtime tier selection from the LIVE sizes (device-resident ranks): the launch is sized for
 // the static capacity, and CTAs beyond what the live block needs exit immediately. 8 warps per
 // CTA (up to 255 registers, so the 32-row-slot tiles do not spill; measured faster than 16).

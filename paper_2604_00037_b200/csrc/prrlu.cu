@@ -938,41 +938,6 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
 #undef ACI_GRID_VARIANT2
 }
 
-// The cluster kernel specialised to blocks of at most MAXR rows (real): the same variants as
-// prrlu_kernel<NWT, 2, false> minus those for taller blocks, so launches whose static size caps the
-// rows at 256 / 512 run a kernel with 2-3 times less code (A/B switch ACI_PRRLU_SPEC).
-template <int NWT, int MAXR>
-__global__ void __launch_bounds__(NWT * 32) prrlu_kernel_spec(LuArgs A) {
-  __shared__ PrrluSmem S;
-  const int m = A.dims->m, n = A.dims->n;
-  const int g = blockIdx.x;
-#define ACI_CTA_VARIANT(EA, EB)                                        \
-  if (32 * (EA) <= MAXR && m <= 32 * (EA) && n <= NWT * (EB)) {         \
-    if (g == 0) prrlu_body<(EA), (EB), NWT, 0, false>(A, S, 1, 0);     \
-    return;                                                            \
-  }
-#define ACI_GRID_VARIANT2(EA, EB)                                      \
-  if (32 * (EA) <= MAXR && m <= 32 * (EA)) {                            \
-    int Gl = (n + NWT * (EB) - 1) / (NWT * (EB));                      \
-    const int CS = (int)cluster_size();                                \
-    Gl = (Gl + CS - 1) / CS * CS;                                      \
-    if (g < Gl) prrlu_body<(EA), (EB), NWT, 2, false>(A, S, Gl, g);    \
-    return;                                                            \
-  }
-  ACI_CTA_VARIANT(1, 4)
-  ACI_CTA_VARIANT(2, 8)
-  ACI_CTA_VARIANT(4, 4)
-  ACI_CTA_VARIANT(1, 16)
-  ACI_CTA_VARIANT(4, 16)
-  ACI_CTA_VARIANT(8, 8)
-  ACI_CTA_VARIANT(2, 32)
-  ACI_GRID_VARIANT2(4, ACI_W8_EB128)
-  ACI_GRID_VARIANT2(8, ACI_W8_EB256)
-  ACI_GRID_VARIANT2(16, ACI_W8_EB512)
-#undef ACI_CTA_VARIANT
-#undef ACI_GRID_VARIANT2
-}
-
 // Single-cluster mode (aci_options.concurrent): every grid variant uses
 // exactly one 16-CTA cluster (gang-scheduled by the hardware), so prrLU launches of products
 // running concurrently on other streams can never hold part of each other's participants while
@@ -1053,14 +1018,6 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel_push(LuArgs A) {
 }
 
 constexpr int kNWT = 8;
-
-static int spec_level() {  // 0: off, 1: static rows <= 256, 2: also <= 512
-  static const int lv = [] {
-    const char *e = getenv("ACI_PRRLU_SPEC");
-    return e ? atoi(e) : 0;
-  }();
-  return lv;
-}
 
 static bool push_enabled() {
   static const bool on = [] {
@@ -1196,8 +1153,7 @@ static int attr_once() {
   // 16-CTA clusters are a non-portable size
   const void *k16[] = {(const void *)prrlu_kernel<kNWT, 2, false>, (const void *)prrlu_kernel<kNWT, 2, true>,
                        (const void *)prrlu_kernel_one<kNWT, false>, (const void *)prrlu_kernel_one<kNWT, true>,
-                       (const void *)prrlu_kernel_rook<kNWT>, (const void *)prrlu_kernel_spec<kNWT, 256>,
-                       (const void *)prrlu_kernel_spec<kNWT, 512>};
+                       (const void *)prrlu_kernel_rook<kNWT>};
   for (const void *f : k16) cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return 0;
 }
@@ -1278,8 +1234,6 @@ static cudaError_t launch_prrlu_t(const LuArgs &a, int max_m, int max_n, cudaStr
     cfg.gridDim = dim3(G);
     cluster(cs);
     cfg.numAttrs = na;
-    if (!CPLX && spec_level() >= 1 && max_m <= 256) return cudaLaunchKernelEx(&cfg, prrlu_kernel_spec<kNWT, 256>, args);
-    if (!CPLX && spec_level() >= 2 && max_m <= 512) return cudaLaunchKernelEx(&cfg, prrlu_kernel_spec<kNWT, 512>, args);
     return cudaLaunchKernelEx(&cfg, prrlu_kernel<kNWT, 2, CPLX>, args);
   }
   cudaMemsetAsync(a.counter, 0, sizeof(unsigned), st);

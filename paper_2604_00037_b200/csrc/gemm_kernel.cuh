@@ -52,7 +52,6 @@ struct Cfg {
   using Smem = typename std::conditional<VEC != 0, SmemV, SmemP>::type;
   static_assert(BK % 8 == 0, "two k-steps per LDS.128");
   static_assert((BM * BK) % NT == 0 && (BK * BN) % NT == 0, "tile loads must divide evenly");
-  static_assert(BM * kSmallK + kSmallK * BN <= (int)(sizeof(Smem) / sizeof(double)), "small-K staging fits");
 };
 
 __device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc, bool valid) {
@@ -237,6 +236,28 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB)
   const int m0 = blockIdx.y * CF::BM, n0 = blockIdx.x * CF::BN;
   if (m0 >= M || n0 >= N) return;
   constexpr int NB = NBIG > 0 ? NBIG : 1;
+  // small-K inputs: A_s (BM x K) and B_s (K x BN) go to shared memory behind the main-loop tiles,
+  // requested here (their own cp.async group, zero-filled outside the problem) so that their latency
+  // hides under the main loop instead of a staging pass after it
+  double *sA = reinterpret_cast<double *>(smem_raw + sizeof(typename CF::Smem));
+  double *sB = sA + NSMALL * CF::BM * kSmallK;
+  if (NSMALL > 0) {
+#pragma unroll
+    for (int s_ = 0; s_ < NSMALL; ++s_) {
+      const int i = NBIG + s_, K = D.K[i];
+      for (int t = threadIdx.x; t < CF::BM * kSmallK; t += CF::NT) {
+        const int row = t / kSmallK, kk = t % kSmallK;
+        const bool v = kk < K && m0 + row < M;
+        cp_async8(&sA[s_ * CF::BM * kSmallK + t], v ? D.A[i] + (size_t)(m0 + row) * D.lda[i] + kk : D.A[i], v);
+      }
+      for (int t = threadIdx.x; t < kSmallK * CF::BN; t += CF::NT) {
+        const int kk = t / CF::BN, col = t % CF::BN;
+        const bool v = kk < K && n0 + col < N;
+        cp_async8(&sB[s_ * kSmallK * CF::BN + t], v ? D.B[i] + (size_t)kk * D.ldb[i] + n0 + col : D.B[i], v);
+      }
+    }
+    cp_async_commit();
+  }
 
   double acc[NB][CF::MI][CF::NI][2];
 #pragma unroll
@@ -249,25 +270,8 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB)
   for (int i = 0; i < NBIG; ++i)
     mainloop<CF>(sm, acc[i], D.A[i], D.lda[i], D.B[i], D.ldb[i], M, N, D.K[i], m0, n0);
 
-  // small-K inputs: stage A_s (BM x K) and B_s (K x BN) in shared memory once
-  double *sA = reinterpret_cast<double *>(smem_raw);
-  double *sB = sA + NSMALL * CF::BM * kSmallK;
-  if (NSMALL > 0) {
-    __syncthreads();
-#pragma unroll
-    for (int s_ = 0; s_ < NSMALL; ++s_) {
-      const int i = NBIG + s_, K = D.K[i];
-      for (int t = threadIdx.x; t < CF::BM * kSmallK; t += CF::NT) {
-        const int row = t / kSmallK, kk = t % kSmallK;
-        sA[s_ * CF::BM * kSmallK + t] =
-            (kk < K && m0 + row < M) ? D.A[i][(size_t)(m0 + row) * D.lda[i] + kk] : 0.0;
-      }
-      for (int t = threadIdx.x; t < kSmallK * CF::BN; t += CF::NT) {
-        const int kk = t / CF::BN, col = t % CF::BN;
-        sB[s_ * kSmallK * CF::BN + t] =
-            (kk < K && n0 + col < N) ? D.B[i][(size_t)kk * D.ldb[i] + n0 + col] : 0.0;
-      }
-    }
+  if (NSMALL > 0 && NBIG == 0) {  // no main loop waited for the small-K group
+    cp_async_wait<0>();
     __syncthreads();
   }
 
@@ -437,17 +441,23 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB)
   }
 }
 
+// dynamic shared memory: the main-loop tiles + the small-K operands
+template <class CF, int NSMALL>
+constexpr size_t smem_bytes() {
+  return sizeof(typename CF::Smem) + sizeof(double) * (size_t)NSMALL * (CF::BM * kSmallK + kSmallK * CF::BN);
+}
+
 template <class CF, int NBIG, int NSMALL, int EPI>
 inline void set_attr() {
   cudaFuncSetAttribute(gemm_kernel<CF, NBIG, NSMALL, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(typename CF::Smem));
+                       (int)smem_bytes<CF, NSMALL>());
 }
 
 template <class CF, int NBIG, int NSMALL, int EPI>
 inline void launch(const GemmDesc *d, int ndesc, int max_m, int max_n, const FOp &op, unsigned long long *sb,
                    int *nf, cudaStream_t st) {
   dim3 grid((max_n + CF::BN - 1) / CF::BN, (max_m + CF::BM - 1) / CF::BM, ndesc);
-  gemm_kernel<CF, NBIG, NSMALL, EPI><<<grid, CF::NT, sizeof(typename CF::Smem), st>>>(d, op, sb, nf);
+  gemm_kernel<CF, NBIG, NSMALL, EPI><<<grid, CF::NT, smem_bytes<CF, NSMALL>(), st>>>(d, op, sb, nf);
 }
 
 }  // namespace gemmk

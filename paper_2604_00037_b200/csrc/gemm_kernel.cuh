@@ -435,7 +435,11 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB)
       bad = bad | (__shfl_xor_sync(0xffffffffu, (int)bad, o) != 0);
     }
     if (lane == 0) {
-      if (vmax > 0.0) atomicMax(scale_bits, (unsigned long long)__double_as_longlong(vmax));
+      // s only grows: a warp whose max does not exceed the value it reads skips the atomic (a stale
+      // read is never larger than the current value, so no needed update is skipped) — 8 warps x
+      // 256 CTAs of atomics on one address cost ~2 us per full-size Pi otherwise
+      const unsigned long long vb = (unsigned long long)__double_as_longlong(vmax);
+      if (vmax > 0.0 && vb > *(volatile const unsigned long long *)scale_bits) atomicMax(scale_bits, vb);
       if (bad) atomicOr(nonfinite, 1);
     }
   }

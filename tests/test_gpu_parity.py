@@ -652,7 +652,7 @@ def test_workspace_alignment_and_query_sweeps(aci):
     assert all(np.array_equal(a, b) for a, b in zip(out.cores(), ref.cores()))
 
 
-@pytest.mark.parametrize("cfg,chi", [(0, 0), (1, 0), (3, 64)])
+@pytest.mark.parametrize("cfg,chi", [(0, 0), (1, 0), (3, 64), (3, 128)])
 def test_rook_pivoting_vs_rook_oracle(aci, cfg, chi):
     """Rook pivoting (aci_options.pivoting = ACI_PIVOT_ROOK; R23) against the
     oracle's rook mode on the same seeded inputs: identical ordered pivots on every update (and the
@@ -690,3 +690,22 @@ def test_rook_pivoting_envelope(aci):
     with pytest.raises(aci.AciError) as e:
         aci.aci_elementwise({"coef": [1.0], "expo": [[2]]}, [z], 1e-8, 16, 2, pivoting="rook")
     assert e.value.code == -6
+
+
+def test_peak_and_latency_probes(aci):
+    """bench.py's roofline denominators (libaci_peak.so): the FP64 DMMA / DFMA loops land within a
+    plausible band of the B200's nominal ~37 TF/s, and the prrLU latency probe returns, per block
+    size, the pivot count of a full factorisation and an exchange-only floor below the real kernel."""
+    import ctypes
+    from paper_2604_00037_b200 import _build
+    lib = ctypes.CDLL(_build.build_peak())
+    lib.aci_peak_fp64.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    for kind in (0, 1):
+        v = ctypes.c_double(0.0)
+        assert lib.aci_peak_fp64(kind, 3, ctypes.byref(v)) == 0
+        assert 20.0 < v.value < 45.0, (kind, v.value)
+    import bench
+    lat = bench.measure_prrlu_latency((64, 256, 1024))
+    for m, row in lat.items():
+        assert row["pivots"] == min(m, 512)
+        assert 0.0 < row["floor_us"] < row["kernel_us"] < 20.0, (m, row)

@@ -66,5 +66,6 @@ def run_concurrent(chi, threads, n):
             "mismatches": len(bad)}
 
 
-res = {"sequential": [run(256, 200), run(64, 300)], "concurrent": run_concurrent(64, 8, 40)}
+res = {"sequential": [run(256, 200), run(64, 300)], "concurrent": [run_concurrent(64, 8, 40),
+                                                                   run_concurrent(256, 4, 10)]}
 print(json.dumps(res, indent=1))

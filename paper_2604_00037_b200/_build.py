@@ -5,7 +5,8 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", f) for f in ("aci.cu", "gemm.cu", "prrlu.cu")]
-HDR = [os.path.join(HERE, "csrc", "aci_common.cuh"), os.path.join(ROOT, "include", "aci.h")]
+HDR = [os.path.join(HERE, "csrc", f) for f in ("aci_common.cuh", "gemm_kernel.cuh", "prrlu_rook.cuh")] + [
+    os.path.join(ROOT, "include", "aci.h")]
 LIB = os.path.join(HERE, "libaci.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-shared",

@@ -448,6 +448,10 @@ struct UpdateArgs {
   LuDims *lu;
   int *info;                  // 8 ints: this bond's (rl, rr, r, -, s bits) for index_bond_kernel
   int next_b;                 // bond index of `next` (-1: none)
+  // streamed Pi: non-null = the stream of Pi_{b+1} took the snapshot of s and merges its max |Pi|
+  // (this kernel runs beside it and leaves s alone)
+  unsigned long long *sp;
+  unsigned long long *ts;  // development timestamps (ACI_STREAM_TS builds only)
 };
 
 // Index-set update (a6, R21) and frame update (a7: the rows/columns of A^n / B^n the
@@ -461,6 +465,14 @@ struct UpdateArgs {
 __global__ void update_bond_kernel(UpdateArgs U) {
 #if ACI_PDL_UPDATE
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+#ifdef ACI_STREAM_TS
+  if (U.ts && U.dir == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    U.ts[16 * U.b + 5] = t;  // update start
+    U.ts[16 * U.b + 6] = *U.r_in;
+  }
 #endif
   const int r = *U.r_in;
   const int b = U.b, L = U.L;
@@ -487,7 +499,7 @@ __global__ void update_bond_kernel(UpdateArgs U) {
     // sizes and s as this bond saw them, for index_bond_kernel (which may trail the sweep while
     // later bonds rewrite rk and s)
     U.info[0] = rl; U.info[1] = rr; U.info[2] = r;
-    *reinterpret_cast<unsigned long long *>(U.info + 4) = *U.scale_bits;
+    if (!U.sp) *reinterpret_cast<unsigned long long *>(U.info + 4) = *U.scale_bits;
   }
   (void)L;
   (void)slot;
@@ -930,6 +942,17 @@ struct Run {
   int cplx = 0, Z = 1, ZE = 1;  // complex run: Z = 2 doubles per entry, ZE = 4 for expanded operands
   int one = 0;                  // aci_options.concurrent: single-cluster prrLU launches
   int rook = 0;                 // aci_options.pivoting == ACI_PIVOT_ROOK (R23, NEXT-4)
+  // streamed Pi: the Pi of L->R bond b+1 is computed while the prrLU of bond b
+  // runs (pi_stream_kernel on the look-ahead stream), so neither that GEMM nor the row gather
+  // sits between the two factorisations. Pi is double-buffered by bond parity (PiB[b & 1]): the
+  // streamed Pi_{b+1} is written while the prrLU of bond b may still be loading Pi_b.
+  int stream = 0;
+  double *PiB[2] = {nullptr, nullptr};
+  unsigned long long *sp = nullptr;  // max |Pi_{b+1}| of the stream, merged into s by its last CTA
+  unsigned *sdone = nullptr;         // the stream's CTA exit counter
+  int *prow0 = nullptr;              // the L->R pivot-row buffers (one block: reset to -1 per iteration)
+  unsigned long long *ts = nullptr;  // ACI_STREAM_TS builds: per-bond timestamps of the last iteration
+  size_t prow0_ints = 0;
   int L = 0, N = 0, maxrank = 0, max_sweeps = 0, log_cap_upd = 0, log_cap_piv = 0, colcap = 0;
   std::vector<int> d, yr;
   std::vector<std::vector<int>> xr;      // [n][s], s = 0..L
@@ -1004,12 +1027,26 @@ static size_t carve(Run &R, char *base) {
   R.maxeps = c.take<unsigned long long>(1);
   R.prow.resize(2 * L);
   R.pcol.resize(2 * L);
-  for (int t = 0; t < 2 * L; ++t) {  // [dir * L + b], bonds 0..L-2; canon uses the dir-0 arrays of bond s-1
+  // the L->R pivot rows in one block (streamed Pi: one memset sets them to -1 per iteration)
+  R.prow0_ints = 0;
+  for (int s = 0; s < L; ++s) R.prow0_ints += (size_t)(s < L - 1 ? R.rmax[s] : 1) + 1;
+  R.prow0 = c.take<int>(R.prow0_ints);
+  for (int t = 0, off = 0; t < 2 * L; ++t) {  // [dir * L + b], bonds 0..L-2; canon uses the dir-0 arrays of bond s-1
     const int s = t % L;
     int cap = s < L - 1 ? R.rmax[s] : 1;
-    R.prow[t] = c.take<int>(cap + 1);
+    if (t < L) {
+      R.prow[t] = R.prow0 ? R.prow0 + off : nullptr;
+      off += cap + 1;
+    } else {
+      R.prow[t] = c.take<int>(cap + 1);
+    }
     R.pcol[t] = c.take<int>(cap + 1);
   }
+  R.sp = c.take<unsigned long long>(1);
+  R.sdone = c.take<unsigned>(1);
+#ifdef ACI_STREAM_TS
+  R.ts = c.take<unsigned long long>(16 * (size_t)L);
+#endif
   R.Rf.assign(N, std::vector<double *>(L + 1, nullptr));
   R.Abuf.assign(N, nullptr);
   R.Bbuf.assign(N, nullptr);
@@ -1042,6 +1079,8 @@ static size_t carve(Run &R, char *base) {
   size_t picap = 1;
   for (int b = 0; b < L - 1; ++b) picap = std::max(picap, (size_t)R.mmax[b] * R.nmax[b]);
   R.Pi = c.take<double>(picap * R.Z);
+  R.PiB[0] = R.Pi;
+  R.PiB[1] = R.stream ? c.take<double>(picap * R.Z) : R.Pi;
   R.Ust.assign(L, nullptr);
   for (int b = 0; b < L - 1; ++b) R.Ust[b] = c.take<double>((size_t)R.rmax[b] * R.nmax[b] * R.Z);
   R.Y0 = c.take<double>(L > 1 ? (size_t)R.mmax[0] * R.rmax[0] * R.Z : 1);
@@ -1285,7 +1324,7 @@ static std::vector<uint64_t> graph_key(const Run &R, const FOp &op, double tol, 
     u(b);
   };
   u((uint64_t)(uintptr_t)ws); u(need); u((uint64_t)(uintptr_t)st);
-  u(R.L); u(R.N); u(R.maxrank); u(R.log_cap_upd); u(R.log_cap_piv); u(R.colcap); u(R.cplx); u(R.one); u(R.rook);
+  u(R.L); u(R.N); u(R.maxrank); u(R.log_cap_upd); u(R.log_cap_piv); u(R.colcap); u(R.cplx); u(R.one); u(R.rook); u(R.stream);
   dbl(tol); u(tol_mode);
   for (int x : R.d) u(x);
   for (int x : R.yr) u(x);
@@ -1302,8 +1341,12 @@ static std::vector<uint64_t> graph_key(const Run &R, const FOp &op, double tol, 
 // ============================================================================ host: the sweep
 namespace {
 
-static void launch_update(Run &R, int b, int dir, int logslot, const BondStatic *next, cudaStream_t st) {
+static void launch_update(Run &R, int b, int dir, int logslot, const BondStatic *next, cudaStream_t st,
+                          bool streamed = false) {
   UpdateArgs U = {};
+  if (streamed) {  // the stream gathered A^n_{b+1}: only the ranks, the plan and the s merge remain
+    U.sp = R.sp;
+  }
   U.next = next; U.ab = R.dAB; U.pi = R.dPi; U.lu = R.dLu;
   U.next_b = next ? (int)((next - R.dStat) % (R.L - 1)) : -1;
   U.b = b; U.dir = dir; U.L = R.L; U.N = R.N; U.db = R.d[b]; U.db1 = R.d[b + 1];
@@ -1316,14 +1359,14 @@ static void launch_update(Run &R, int b, int dir, int logslot, const BondStatic 
   U.Jnew = R.Jmi[b + 1];
   for (int n = 0; n < R.N; ++n) {
     U.Ahat[n] = R.Abuf[n];
-    U.Anext[n] = dir == 0 && b + 2 < R.L ? R.Ast[n][b + 1] : nullptr;
+    U.Anext[n] = dir == 0 && b + 2 < R.L && !streamed ? R.Ast[n][b + 1] : nullptr;
     U.W[n] = b + 2 < R.L ? R.Z * R.d[b + 1] * R.xr[n][b + 2] : 0;
     U.Bhat[n] = R.Bbuf[n];
     U.Bprev[n] = dir == 1 && b > 0 ? R.Bst[n][b - 1] : nullptr;
     U.c0[n] = R.xr[n][b];
   }
   U.Z = R.Z;
-  U.Pi = R.Pi;
+  U.Pi = R.PiB[b & 1];
   U.Y0 = R.Y0;
   U.maxeps_bits = R.maxeps;
   U.scale_bits = R.scale;
@@ -1336,7 +1379,8 @@ static void launch_update(Run &R, int b, int dir, int logslot, const BondStatic 
   U.per_iter = 2 * (R.L - 1);
   U.cap_piv = R.log_cap_piv;
   U.info = R.binfo + 8 * (dir * (R.L - 1) + b);
-  size_t work = (size_t)R.rmax[b] * 256;
+  U.ts = R.ts;
+  size_t work = streamed ? 1 : (size_t)R.rmax[b] * 256;
   int blocks = (int)std::min<size_t>(592, std::max<size_t>(1, (work + 255) / 256));
 #if ACI_PDL_UPDATE
   cudaLaunchConfig_t cfg = {};
@@ -1386,7 +1430,7 @@ static void build_statics(Run &R, const FOp &op) {
       S.Z = R.Z;
       S.ldu = R.nmax[b];
       S.maxrank = R.maxrank;
-      S.Pi = R.Pi;
+      S.Pi = R.PiB[b & 1];
       // Pi kernel input order: inputs whose inner dimension chi^n_{b+1} is large run the DMMA
       // main loop (first), tiny ones (e.g. rank-2 inputs) are evaluated in the epilogue; the op's
       // exponents are permuted to the same order.
@@ -1450,6 +1494,7 @@ static void pre_launch(Run &R, cudaStream_t st) {
 struct SideStream {
   cudaStream_t st = nullptr, ix = nullptr;  // look-ahead GEMMs; index/log kernels
   cudaEvent_t started = nullptr, done = nullptr, upd = nullptr, ix_done = nullptr;
+  cudaEvent_t la = nullptr;  // streamed Pi: the look-ahead GEMM done (its descriptors may be re-planned)
 };
 static SideStream &side_stream() {
   static thread_local SideStream s;
@@ -1457,14 +1502,79 @@ static SideStream &side_stream() {
 }
 static bool side_stream_init() {
   SideStream &s = side_stream();
-  if (s.st && s.ix && s.started && s.done && s.upd && s.ix_done) return true;
+  if (s.st && s.ix && s.started && s.done && s.upd && s.ix_done && s.la) return true;
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   if (!s.st && cudaStreamCreateWithPriority(&s.st, cudaStreamNonBlocking, lo) != cudaSuccess) s.st = nullptr;
   if (!s.ix && cudaStreamCreateWithPriority(&s.ix, cudaStreamNonBlocking, lo) != cudaSuccess) s.ix = nullptr;
-  for (cudaEvent_t *e : {&s.started, &s.done, &s.upd, &s.ix_done})
+  for (cudaEvent_t *e : {&s.started, &s.done, &s.upd, &s.ix_done, &s.la})
     if (!*e && cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) *e = nullptr;
-  return s.st && s.ix && s.started && s.done && s.upd && s.ix_done;
+  return s.st && s.ix && s.started && s.done && s.upd && s.ix_done && s.la;
+}
+
+// ACI_STREAM_SERIAL=1: the stream runs after the prrLU instead of beside it (A/B)
+static bool serial_stream() {
+  static const bool s = [] {
+    const char *e = getenv("ACI_STREAM_SERIAL");
+    return e && atoi(e) != 0;
+  }();
+  return s;
+}
+
+// Does the prrLU of L->R bond b stream the Pi of bond b+1 (Run::stream)?
+// Only large Pi are streamed (static m' n' sum K >= ACI_STREAM_MIN, default 2^26 multiply-adds, e.g.
+// 512 x 512 x 256): for the small ones the stream's last chunk costs about what the Pi GEMM and
+// the gather cost.
+static bool streams_next(const Run &R, int b, int dir) {
+  if (!R.stream || dir != 0 || b + 2 >= R.L) return false;
+  static const double min_fma = [] {
+    const char *e = getenv("ACI_STREAM_MIN");
+    return e ? atof(e) : 67108864.0;
+  }();
+  int c2[ACI_GEMM_MAX_IN];
+  double ksum = 0;
+  for (int kk = 0; kk < R.N; ++kk) {
+    c2[kk] = R.hStat[b + 1].in[kk].c1;
+    if (kk < R.nbig[b + 1]) ksum += c2[kk];
+  }
+  if ((double)R.mmax[b + 1] * R.nmax[b + 1] * ksum < min_fma) return false;
+  return pi_stream_supported(R.nbig[b + 1], R.nsmall[b + 1], c2, (R.nmax[b + 1] + 31) / 32);
+}
+
+// Pi_{b+1} while the prrLU of bond b runs, on the look-ahead stream after the look-ahead GEMM
+// (whose rows it gathers): inputs in bond b+1's Pi order.
+static void launch_stream(Run &R, int b, cudaStream_t st) {
+  static const int ctas = [] {  // ~CTAs of the stream (ntmax x P, P >= 1); it runs beside the prrLU
+    const char *e = getenv("ACI_STREAM_GRID");
+    const int g = e ? atoi(e) : 64;
+    return g > 0 ? g : 64;
+  }();
+  const int ntmax = (R.nmax[b + 1] + 31) / 32;
+  const int grid = ntmax * std::max(1, ctas / ntmax);
+  const int L = R.L, N = R.N, k1 = b + 1;
+  const BondStatic &S1 = R.hStat[k1];  // dir 0
+  PiStreamArgs A = {};
+  static const unsigned poll_ns = [] {
+    const char *e = getenv("ACI_STREAM_POLL_NS");
+    return e ? (unsigned)atoi(e) : 128u;
+  }();
+  A.rows = R.prow[b]; A.r_in = R.rout + b; A.rk = R.rk; A.kcap = R.rmax[b]; A.poll_ns = poll_ns; A.ntmax = ntmax;
+  A.b = b; A.d1 = R.d[b + 1]; A.db2 = R.d[b + 2]; A.N = N; A.nbig = R.nbig[k1];
+  for (int kk = 0; kk < N; ++kk) {
+    const InBond &I = S1.in[kk];
+    A.Ahat[kk] = I.Ahat;
+    A.Anext[kk] = I.Ast;
+    A.B[kk] = k1 + 2 < L ? I.Bst : I.Xb1;
+    A.c2[kk] = I.c1;
+  }
+  A.Pi = R.PiB[k1 & 1];
+  A.ts = R.ts;
+  A.sp = R.sp;
+  A.scale = R.scale;
+  A.done = R.sdone;
+  A.info = R.binfo + 8 * b;  // dir 0
+  A.nonfinite = R.nonfinite;
+  launch_pi_stream(A, R.nsmall[k1], R.opb[k1], grid, st);
 }
 
 // One 2-site update (Alg. 1): [plan] -> a3+a4 -> a5 (|| look-ahead GEMM) -> a6/a7 (+ the
@@ -1482,15 +1592,20 @@ static void bond_update(Run &R, double tol, int tol_mode, int b, int dir, int lo
     plan_bond_kernel<<<1, 1, 0, st>>>(dstat(R, dir, b), R.rk, R.dAB, R.dPi, R.dLu);
     R.P->end(1);
   }
-  R.P->begin(ACI_PROF_GEMM_PI);
-  if (R.cplx)
-    launch_gemm_z(R.dPi, 1, R.mmax[b], 2 * R.nmax[b], 2, N, R.opb[k], R.scale, R.nonfinite, st);
-  else
-    launch_gemm_split(R.dPi, 1, R.mmax[b], R.nmax[b], R.nbig[k], R.nsmall[k], true, R.opb[k], R.scale, R.nonfinite,
-                      st);
-  R.P->end(1);
+  // streamed_in: Pi_b was computed beside the previous bond's prrLU; stream_out: this prrLU
+  // streams Pi_{b+1}
+  const bool streamed_in = b > 0 && streams_next(R, b - 1, dir), stream_out = streams_next(R, b, dir);
+  if (!streamed_in) {
+    R.P->begin(ACI_PROF_GEMM_PI);
+    if (R.cplx)
+      launch_gemm_z(R.dPi, 1, R.mmax[b], 2 * R.nmax[b], 2, N, R.opb[k], R.scale, R.nonfinite, st);
+    else
+      launch_gemm_split(R.dPi, 1, R.mmax[b], R.nmax[b], R.nbig[k], R.nsmall[k], true, R.opb[k], R.scale, R.nonfinite,
+                        st);
+    R.P->end(1);
+  }
   LuArgs a = {};
-  a.M = R.Pi; a.dims = R.dLu; a.tol = tol; a.thr_mode = tol_mode == ACI_TOL_RELATIVE ? 0 : 2;
+  a.M = R.PiB[b & 1]; a.dims = R.dLu; a.tol = tol; a.thr_mode = tol_mode == ACI_TOL_RELATIVE ? 0 : 2;
   a.scale_bits = R.scale;
   const int pv = dir * L + b;
   a.rows = R.prow[pv]; a.cols = R.pcol[pv]; a.r_out = R.rout + pv; a.eps_out = R.epsb + pv;
@@ -1514,13 +1629,33 @@ static void bond_update(Run &R, double tol, int tol_mode, int b, int dir, int lo
     else
       launch_gemm(R.dAB, N, la_m, la_n, 1, false, dummy, nullptr, nullptr, sd.st);
     R.P->end(1);
+    const bool serial = serial_stream();
+    if (stream_out && !serial) {
+      cudaEventRecord(sd.la, sd.st);
+      R.P->begin(ACI_PROF_GEMM_PI);
+      launch_stream(R, b, sd.st);
+      R.P->end(1);
+    }
     R.P->st = mine;
     cudaEventRecord(sd.done, sd.st);
+    if (stream_out && !serial) {  // the ranks and the next plan beside the stream's last chunk
+      cudaStreamWaitEvent(st, sd.la, 0);  // (the plan rewrites the look-ahead GEMM's descriptors)
+      R.P->begin(ACI_PROF_UPDATE);
+      launch_update(R, b, dir, logslot, next, st, true);
+      R.P->end(1);
+    }
     cudaStreamWaitEvent(st, sd.done, 0);
+    if (stream_out && serial) {
+      R.P->begin(ACI_PROF_GEMM_PI);
+      launch_stream(R, b, st);
+      R.P->end(1);
+    }
   }
-  R.P->begin(ACI_PROF_UPDATE);
-  launch_update(R, b, dir, logslot, next, st);
-  R.P->end(1);
+  if (!(stream_out && look && !serial_stream())) {
+    R.P->begin(ACI_PROF_UPDATE);
+    launch_update(R, b, dir, logslot, next, st, stream_out && look);
+    R.P->end(1);
+  }
   cudaEventRecord(sd.upd, st);
   cudaStreamWaitEvent(sd.ix, sd.upd, 0);
   cudaStream_t mine = R.P->st;
@@ -1648,6 +1783,12 @@ static int build_run(const Inputs &I, const tt_s *y, int maxrank, int max_sweeps
   // envelope (rook mode: the single-cluster envelope, real values)
   R.one = one;
   R.rook = rook;
+  // streamed Pi: real values, full pivoting, default tiers (ACI_STREAM_PI=0: off, for A/B)
+  static const bool stream_env = [] {
+    const char *e = getenv("ACI_STREAM_PI");
+    return !e || atoi(e) != 0;
+  }();
+  R.stream = stream_env && !R.cplx && !rook && !one && R.L >= 3 ? 1 : 0;
   if (rook && R.cplx) return fail(ACI_ERR_UNSUPPORTED, "aci: rook pivoting is implemented for real values only");
   auto ok = [&](int m, int n) {
     if (rook) return prrlu_supported_rook(m, n);
@@ -1776,6 +1917,8 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
     cudaStreamSynchronize(strm);
   }
   cudaMemsetAsync(R.scale, 0, sizeof(unsigned long long), strm);
+  cudaMemsetAsync(R.sp, 0, sizeof(unsigned long long), strm);
+  cudaMemsetAsync(R.sdone, 0, sizeof(unsigned), strm);
   cudaMemsetAsync(R.maxeps, 0, sizeof(unsigned long long), strm);
   cudaMemsetAsync(R.nonfinite, 0, sizeof(int), strm);
   cudaMemsetAsync(R.iter, 0, sizeof(int), strm);
@@ -1810,6 +1953,13 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   // once as a CUDA graph and replayed; only the convergence flag comes back to the host.
   auto one_iteration = [&]() {
     int step = 0;
+#ifdef ACI_STREAM_TS
+    cudaMemsetAsync(R.ts, 0, sizeof(unsigned long long) * 16 * L, strm);
+#endif
+    if (R.stream) {  // the streams poll the L->R pivot rows and ranks: -1 = not written yet
+      cudaMemsetAsync(R.prow0, 0xff, sizeof(int) * R.prow0_ints, strm);
+      cudaMemsetAsync(R.rout, 0xff, sizeof(int) * L, strm);
+    }
     for (int b = 0; b < L - 1; ++b)
       bond_update(R, tol, o.tol_mode, b, 0, step++, b == 0, b + 1 < L - 1 ? dstat(R, 0, b + 1) : dstat(R, 1, L - 2), strm);
     for (int b = L - 2; b >= 0; --b)
@@ -2057,6 +2207,22 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
       if (o.J_sets[s])
         cudaMemcpyAsync(o.J_sets[s], R.Jmi[s], (size_t)rk[s] * (L - s), cudaMemcpyDeviceToHost, strm);
   e = cudaStreamSynchronize(strm);
+#ifdef ACI_STREAM_TS
+  {  // b, start, first-r-seen, last item start, exit, update start (ns, relative to the kernel start), r
+    std::vector<unsigned long long> h(16 * (size_t)L);
+    cudaMemcpy(h.data(), R.ts, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+    for (int b = 0; b + 2 < L; ++b) {
+      const unsigned long long *t = &h[16 * b];
+      const unsigned long long t0 = ~t[0], tr = ~t[1];
+      if (!t[0]) continue;
+      fprintf(stderr, "ts b=%d r=%lld start->r %.2f us | r->last item %.2f | r->exit %.2f | exit->update %.2f | item after r: %s\n",
+              b, (long long)t[6], (tr - t0) * 1e-3, ((long long)t[3] - (long long)tr) * 1e-3,
+              ((long long)t[4] - (long long)tr) * 1e-3, ((long long)t[5] - (long long)t[4]) * 1e-3, t[2] ? "yes" : "no");
+      fprintf(stderr, "   max per item: rowp %.2f | A load %.2f | dmma %.2f | epilogue %.2f | A store %.2f us\n", t[8] * 1e-3,
+              t[9] * 1e-3, t[10] * 1e-3, t[11] * 1e-3, t[12] * 1e-3);
+    }
+  }
+#endif
   cleanup();
   if (e != cudaSuccess) { tt_destroy(res); return fail(ACI_ERR_CUDA, std::string("aci: ") + cudaGetErrorString(e)); }
   auto t_end = std::chrono::steady_clock::now();

@@ -78,6 +78,38 @@ void launch_gemm_z(const GemmDesc *d, int ndesc, int max_m, int max_n, int mode,
 // C = S - A B for every descriptor (blocked triangular solve updates).
 void launch_gemm_sub(const GemmDesc *d_descs, int ndesc, int max_m, int max_n, cudaStream_t st);
 
+// a3+a4 of the next L->R bond streamed while this bond's prrLU runs (DESIGN.md §5 "streamed Pi"):
+// rows of Pi_{b+1} = f(A^1_{b+1} B^1_{b+1}, ...) are computed as the pivot rows I_b they need are
+// taken. A^n_{b+1} row (k, sigma) = Ahat^n[rows[k]][sigma c2 .. sigma c2 + c2) (Ahat^n = A^n_b X^n_{b+1},
+// the look-ahead product, W = d1 c2 doubles per row); the gathered rows are also stored to Anext^n.
+// Inputs in Pi order: 0..nbig-1 through the DMMA main loop, the rest (c2 <= gemm_small_k()) in the
+// epilogue. rows[] and *r_in read -1 until the prrLU writes them.
+struct PiStreamArgs {
+  const int *rows;    // pivot rows of bond b (written one by one by the prrLU)
+  const int *r_in;    // final rank of bond b
+  const int *rk;      // live ranks: n' = db2 * rk[b + 3]
+  int kcap;           // capacity of rows[] (the prrLU takes at most kcap pivots)
+  int ntmax;          // 32-column tiles of the static n' (grid = ntmax x P)
+  unsigned poll_ns;   // back-off between polls
+  unsigned long long *ts;  // development timestamps (ACI_STREAM_TS builds only)
+  int b, d1, db2, N, nbig;
+  const double *Ahat[ACI_GEMM_MAX_IN];
+  double *Anext[ACI_GEMM_MAX_IN];  // null: not stored
+  const double *B[ACI_GEMM_MAX_IN];  // B^n_{b+1} (c2 x n', ld n')
+  int c2[ACI_GEMM_MAX_IN];
+  double *Pi;         // Pi_{b+1}, ld n'
+  unsigned long long *sp;  // max |Pi_{b+1}| (bits) of this stream, merged into *scale by its last CTA
+  unsigned long long *scale;  // the running s: snapshot into info[4..5] at the start, merged at the end
+  int *info;          // bond b's index-kernel snapshot (info + 4: s as Pi_b left it)
+  unsigned *done;     // CTA exit counter (reset by the last CTA)
+  int *nonfinite;
+};
+// c2: the inputs' K in Pi order; ntmax = ceil(static n' / 32) (<= 64), sum of the DMMA inputs'
+// K <= 256 (shared-memory panels)
+bool pi_stream_supported(int nbig, int nsmall, const int *c2, int ntmax);
+// grid = ntmax x P persistent CTAs (column tile q % ntmax, chunks q / ntmax + P t)
+void launch_pi_stream(const PiStreamArgs &a, int nsmall, const FOp &op, int grid, cudaStream_t st);
+
 // Picks the tier for a (max_m x max_n) problem; returns false if it is out of the envelope.
 bool prrlu_supported(int max_m, int max_n, bool cplx = false);
 size_t prrlu_exchange_bytes(int max_m, int max_n);

@@ -148,6 +148,133 @@ __device__ __forceinline__ void load_stage_v(typename CF::Smem &sm, int st, cons
   }
 }
 
+// VEC = 1 main loop over the k-tiles [kb, ke) of this CTA's tile: acc += A[:, kb*BK : ke*BK] B[...]
+// (ke > kb; the whole-K tile kernel and the stream-K kernel's segments both run it)
+template <class CF>
+__device__ __forceinline__ void mainloop_v(typename CF::Smem &sm, double (&acc)[CF::MI][CF::NI][2], const double *A,
+                                           int lda, const double *B, int ldb, int M, int N, int K, int m0, int n0,
+                                           int kb, int ke) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, c = lane & 3;
+  const int wm = (w / CF::WARPS_N) * CF::WM, wn = (w % CF::WARPS_N) * CF::WN;
+  const bool vec = !((lda | ldb) & 1) && !((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15);
+  __syncthreads();  // shared memory reuse across inputs
+#pragma unroll
+  for (int s = 0; s < CF::STAGES - 1; ++s) {
+    if (kb + s < ke) load_stage_v<CF>(sm, s, A, lda, B, ldb, M, N, K, m0, n0, (kb + s) * CF::BK, vec);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < ke - kb; ++kt) {
+    cp_async_wait<CF::STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = kt + CF::STAGES - 1;
+      if (kb + nxt < ke)
+        load_stage_v<CF>(sm, nxt % CF::STAGES, A, lda, B, ldb, M, N, K, m0, n0, (kb + nxt) * CF::BK, vec);
+      cp_async_commit();
+    }
+    const int st = kt % CF::STAGES;
+#pragma unroll
+    for (int ks = 0; ks < CF::BK / 4; ++ks) {
+      double a[CF::MI], b[CF::NI];
+#pragma unroll
+      for (int mi = 0; mi < CF::MI; ++mi) a[mi] = sm.A[st][wm + mi * 8 + g][4 * ks + c];
+#pragma unroll
+      for (int ni = 0; ni < CF::NI; ++ni) b[ni] = sm.B[st][4 * ks + c][wn + ni * 8 + g];
+#pragma unroll
+      for (int mi = 0; mi < CF::MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < CF::NI; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+    }
+  }
+  cp_async_wait<0>();
+}
+
+// Row-gathered A (the streamed Pi): row `row` of the CTA's A tile starts at rowp[row]
+// (null: outside the problem, zero-filled); B as in load_stage_v. 16-byte copies when every row
+// pointer and B are 16-byte aligned (vec) and the k-tile is whole, single doubles otherwise.
+template <class CF>
+__device__ __forceinline__ void load_stage_gv(typename CF::Smem &sm, int st, const double *const *rowp, const double *B,
+                                              int ldb, int N, int K, int n0, int k0, bool vec) {
+  const int t = threadIdx.x;
+  if (vec && n0 + CF::BN <= N && k0 + CF::BK <= K) {
+#pragma unroll
+    for (int i = 0; i < (CF::BM * CF::BK / 2) / CF::NT; ++i) {
+      const int e = t + CF::NT * i;
+      const int row = e / (CF::BK / 2), kc = 2 * (e % (CF::BK / 2));
+      const double *src = rowp[row];
+      unsigned sd = (unsigned)__cvta_generic_to_shared(&sm.A[st][row][kc]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sd), "l"(src ? src + k0 + kc : B),
+                   "r"(src ? 16 : 0));
+    }
+#pragma unroll
+    for (int i = 0; i < (CF::BK * CF::BN / 2) / CF::NT; ++i) {
+      const int e = t + CF::NT * i;
+      const int kr = e / (CF::BN / 2), col = 2 * (e % (CF::BN / 2));
+      cp_async16(&sm.B[st][kr][col], B + (size_t)(k0 + kr) * ldb + (n0 + col));
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < (CF::BM * CF::BK) / CF::NT; ++i) {
+    const int e = t + CF::NT * i;
+    const int row = e / CF::BK, kc = e % CF::BK;
+    const double *src = rowp[row];
+    const bool v = src && k0 + kc < K;
+    cp_async8(&sm.A[st][row][kc], v ? src + k0 + kc : B, v);
+  }
+#pragma unroll
+  for (int i = 0; i < (CF::BK * CF::BN) / CF::NT; ++i) {
+    const int e = t + CF::NT * i;
+    const int kr = e / CF::BN, col = e % CF::BN;
+    const bool v = (k0 + kr < K) && (n0 + col < N);
+    cp_async8(&sm.B[st][kr][col], v ? B + (size_t)(k0 + kr) * ldb + (n0 + col) : B, v);
+  }
+}
+
+// acc += A B over the whole K with a row-gathered A (VEC layout, same per-thread k order as
+// mainloop_v: bit-identical to the tile kernel on the materialised A)
+template <class CF>
+__device__ __forceinline__ void mainloop_gv(typename CF::Smem &sm, double (&acc)[CF::MI][CF::NI][2],
+                                            const double *const *rowp, bool avec, const double *B, int ldb, int N,
+                                            int K, int n0) {
+  static_assert(CF::VEC != 0, "gathered loads use the VEC layout");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, c = lane & 3;
+  const int wm = (w / CF::WARPS_N) * CF::WM, wn = (w % CF::WARPS_N) * CF::WN;
+  const bool vec = avec && !(ldb & 1) && !(reinterpret_cast<uintptr_t>(B) & 15);
+  const int nk = (K + CF::BK - 1) / CF::BK;
+  __syncthreads();  // shared memory reuse across inputs / tiles
+#pragma unroll
+  for (int s = 0; s < CF::STAGES - 1; ++s) {
+    if (s < nk) load_stage_gv<CF>(sm, s, rowp, B, ldb, N, K, n0, s * CF::BK, vec);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<CF::STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = kt + CF::STAGES - 1;
+      if (nxt < nk) load_stage_gv<CF>(sm, nxt % CF::STAGES, rowp, B, ldb, N, K, n0, nxt * CF::BK, vec);
+      cp_async_commit();
+    }
+    const int st = kt % CF::STAGES;
+#pragma unroll
+    for (int ks = 0; ks < CF::BK / 4; ++ks) {
+      double a[CF::MI], b[CF::NI];
+#pragma unroll
+      for (int mi = 0; mi < CF::MI; ++mi) a[mi] = sm.A[st][wm + mi * 8 + g][4 * ks + c];
+#pragma unroll
+      for (int ni = 0; ni < CF::NI; ++ni) b[ni] = sm.B[st][4 * ks + c][wn + ni * 8 + g];
+#pragma unroll
+      for (int mi = 0; mi < CF::MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < CF::NI; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+    }
+  }
+  cp_async_wait<0>();
+}
+
 // acc += A (M x K) * B (K x N) on this CTA's tile.
 template <class CF>
 __device__ __forceinline__ void mainloop(typename CF::Smem &sm, double (&acc)[CF::MI][CF::NI][2], const double *A,
@@ -157,36 +284,7 @@ __device__ __forceinline__ void mainloop(typename CF::Smem &sm, double (&acc)[CF
   const int wm = (w / CF::WARPS_N) * CF::WM, wn = (w % CF::WARPS_N) * CF::WN;
   const int nk = (K + CF::BK - 1) / CF::BK;
   if constexpr (CF::VEC != 0) {
-    const bool vec = !((lda | ldb) & 1) && !((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15);
-    __syncthreads();  // shared memory reuse across inputs
-#pragma unroll
-    for (int s = 0; s < CF::STAGES - 1; ++s) {
-      if (s < nk) load_stage_v<CF>(sm, s, A, lda, B, ldb, M, N, K, m0, n0, s * CF::BK, vec);
-      cp_async_commit();
-    }
-    for (int kt = 0; kt < nk; ++kt) {
-      cp_async_wait<CF::STAGES - 2>();
-      __syncthreads();
-      {
-        const int nxt = kt + CF::STAGES - 1;
-        if (nxt < nk) load_stage_v<CF>(sm, nxt % CF::STAGES, A, lda, B, ldb, M, N, K, m0, n0, nxt * CF::BK, vec);
-        cp_async_commit();
-      }
-      const int st = kt % CF::STAGES;
-#pragma unroll
-      for (int ks = 0; ks < CF::BK / 4; ++ks) {
-        double a[CF::MI], b[CF::NI];
-#pragma unroll
-        for (int mi = 0; mi < CF::MI; ++mi) a[mi] = sm.A[st][wm + mi * 8 + g][4 * ks + c];
-#pragma unroll
-        for (int ni = 0; ni < CF::NI; ++ni) b[ni] = sm.B[st][4 * ks + c][wn + ni * 8 + g];
-#pragma unroll
-        for (int mi = 0; mi < CF::MI; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < CF::NI; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
-      }
-    }
-    cp_async_wait<0>();
+    mainloop_v<CF>(sm, acc, A, lda, B, ldb, M, N, K, m0, n0, 0, (K + CF::BK - 1) / CF::BK);
     return;
   }
   __syncthreads();  // shared memory reuse across inputs
@@ -224,6 +322,109 @@ __device__ __forceinline__ void mainloop(typename CF::Smem &sm, double (&acc)[CF
     }
   }
   cp_async_wait<0>();
+}
+
+// EPI_F on a finished tile: Pi = f(x_1, ..., x_N) from the accumulators (inputs 0..NBIG-1) and the
+// small-K operands in shared memory (inputs NBIG..), stored to D.C; max |Pi| and the NaN flag of the
+// real entries accumulate into vmax / bad
+template <class CF, int NBIG, int NSMALL, int NB>
+__device__ __forceinline__ void epi_f(const GemmDesc &D, const FOp &op, const double (&acc)[NB][CF::MI][CF::NI][2],
+                                      const double *sA, const double *sB, int M, int N, int m0, int n0, double &vmax,
+                                      bool &bad) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, c = lane & 3;
+  const int wm = (w / CF::WARPS_N) * CF::WM, wn = (w % CF::WARPS_N) * CF::WN;
+  // small inputs: this thread's MI rows of A_s and 2*NI columns of B_s in registers
+  constexpr int NS = NSMALL > 0 ? NSMALL : 1;
+  double ra[NS][CF::MI][kSmallK], rb[NS][CF::NI][2][kSmallK];
+  int ks[NS];
+#pragma unroll
+  for (int s_ = 0; s_ < NSMALL; ++s_) {
+    ks[s_] = D.K[NBIG + s_];
+#pragma unroll
+    for (int kk = 0; kk < kSmallK; ++kk) {
+#pragma unroll
+      for (int mi = 0; mi < CF::MI; ++mi)
+        ra[s_][mi][kk] = sA[s_ * CF::BM * kSmallK + (wm + mi * 8 + g) * kSmallK + kk];
+#pragma unroll
+      for (int ni = 0; ni < CF::NI; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) rb[s_][ni][e][kk] = sB[s_ * kSmallK * CF::BN + kk * CF::BN + wn + ni * 8 + 2 * c + e];
+    }
+  }
+  const bool mono = op.monomial_all_ones != 0;
+  const double coef0 = op.coef[0];
+#pragma unroll
+  for (int mi = 0; mi < CF::MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < CF::NI; ++ni) {
+      const int row = m0 + wm + mi * 8 + g, col0 = n0 + wn + ni * 8 + 2 * c;
+      double y2[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double x[NBIG + NSMALL];
+#pragma unroll
+        for (int i = 0; i < NBIG; ++i) x[i] = acc[i][mi][ni][e];
+#pragma unroll
+        for (int s_ = 0; s_ < NSMALL; ++s_) {
+          double v = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < kSmallK; ++kk)
+            if (kk < ks[s_]) v = fma(ra[s_][mi][kk], rb[s_][ni][e][kk], v);
+          x[NBIG + s_] = v;
+        }
+        double y;
+        if (mono) {
+          // f = coef * prod x_i, multiplied in the oracle's order (apply_f with one term)
+          double p = coef0;
+#pragma unroll
+          for (int i = 0; i < NBIG + NSMALL; ++i) p *= x[i];
+          y = p;
+        } else {
+          y = 0.0;
+          for (int t = 0; t < op.T; ++t) {
+            double p = op.coef[t];
+#pragma unroll
+            for (int i = 0; i < NBIG + NSMALL; ++i)
+              for (int q = 0; q < op.expo[t * op.N + i]; ++q) p *= x[i];
+            y += p;
+          }
+        }
+        // padded lanes hold f(0) (nonzero for a constant term): never part of s or the NaN check
+        if (row < M && col0 + e < N) {
+          bad |= !isfinite(y);
+          vmax = fmax(vmax, fabs(y));
+        }
+        y2[e] = y;
+      }
+      if (row < M) {
+        double *dst = D.C + (size_t)row * D.ldc + col0;
+        if (col0 + 1 < N) {
+          dst[0] = y2[0];
+          dst[1] = y2[1];
+        } else if (col0 < N) {
+          dst[0] = y2[0];
+        }
+      }
+    }
+}
+
+// warp max of |Pi| into the running s (scale_bits, atomicMax on the bits) and the NaN flag
+__device__ __forceinline__ void epi_scale(double vmax, bool bad, unsigned long long *scale_bits, int *nonfinite) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    bad = bad | (__shfl_xor_sync(0xffffffffu, (int)bad, o) != 0);
+  }
+  if (lane == 0) {
+    // s only grows: a warp whose max does not exceed the value it reads skips the atomic (a stale
+    // read is never larger than the current value, so no needed update is skipped) — 8 warps x
+    // 256 CTAs of atomics on one address cost ~2 us per full-size Pi otherwise
+    const unsigned long long vb = (unsigned long long)__double_as_longlong(vmax);
+    if (vmax > 0.0 && vb > *(volatile const unsigned long long *)scale_bits) atomicMax(scale_bits, vb);
+    if (bad) atomicOr(nonfinite, 1);
+  }
 }
 
 template <class CF, int NBIG, int NSMALL, int EPI>
@@ -281,79 +482,7 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB)
   double vmax = 0.0;
   bool bad = false;
   if (EPI == EPI_F) {
-    // small inputs: this thread's MI rows of A_s and 2*NI columns of B_s in registers
-    constexpr int NS = NSMALL > 0 ? NSMALL : 1;
-    double ra[NS][CF::MI][kSmallK], rb[NS][CF::NI][2][kSmallK];
-    int ks[NS];
-#pragma unroll
-    for (int s_ = 0; s_ < NSMALL; ++s_) {
-      ks[s_] = D.K[NBIG + s_];
-#pragma unroll
-      for (int kk = 0; kk < kSmallK; ++kk) {
-#pragma unroll
-        for (int mi = 0; mi < CF::MI; ++mi)
-          ra[s_][mi][kk] = sA[s_ * CF::BM * kSmallK + (wm + mi * 8 + g) * kSmallK + kk];
-#pragma unroll
-        for (int ni = 0; ni < CF::NI; ++ni)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) rb[s_][ni][e][kk] = sB[s_ * kSmallK * CF::BN + kk * CF::BN + wn + ni * 8 + 2 * c + e];
-      }
-    }
-    const bool mono = op.monomial_all_ones != 0;
-    const double coef0 = op.coef[0];
-#pragma unroll
-    for (int mi = 0; mi < CF::MI; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < CF::NI; ++ni) {
-        const int row = m0 + wm + mi * 8 + g, col0 = n0 + wn + ni * 8 + 2 * c;
-        double y2[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          double x[NBIG + NSMALL];
-#pragma unroll
-          for (int i = 0; i < NBIG; ++i) x[i] = acc[i][mi][ni][e];
-#pragma unroll
-          for (int s_ = 0; s_ < NSMALL; ++s_) {
-            double v = 0.0;
-#pragma unroll
-            for (int kk = 0; kk < kSmallK; ++kk)
-              if (kk < ks[s_]) v = fma(ra[s_][mi][kk], rb[s_][ni][e][kk], v);
-            x[NBIG + s_] = v;
-          }
-          double y;
-          if (mono) {
-            // f = coef * prod x_i, multiplied in the oracle's order (apply_f with one term)
-            double p = coef0;
-#pragma unroll
-            for (int i = 0; i < NBIG + NSMALL; ++i) p *= x[i];
-            y = p;
-          } else {
-            y = 0.0;
-            for (int t = 0; t < op.T; ++t) {
-              double p = op.coef[t];
-#pragma unroll
-              for (int i = 0; i < NBIG + NSMALL; ++i)
-                for (int q = 0; q < op.expo[t * op.N + i]; ++q) p *= x[i];
-              y += p;
-            }
-          }
-          // padded lanes hold f(0) (nonzero for a constant term): never part of s or the NaN check
-          if (row < M && col0 + e < N) {
-            bad |= !isfinite(y);
-            vmax = fmax(vmax, fabs(y));
-          }
-          y2[e] = y;
-        }
-        if (row < M) {
-          double *dst = D.C + (size_t)row * D.ldc + col0;
-          if (col0 + 1 < N) {
-            dst[0] = y2[0];
-            dst[1] = y2[1];
-          } else if (col0 < N) {
-            dst[0] = y2[0];
-          }
-        }
-      }
+    epi_f<CF, NBIG, NSMALL>(D, op, acc, sA, sB, M, N, m0, n0, vmax, bad);
   } else if (EPI == EPI_FZ) {
     // f = sum_t coef_t prod_n x_n^{e_tn} on complex values (RZ6); |z| = sqrt(re^2 + im^2) (RZ1)
     const bool mono = op.monomial_all_ones != 0;
@@ -428,21 +557,7 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB)
           }
         }
   }
-  if (EPI == EPI_F || EPI == EPI_FZ) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
-      bad = bad | (__shfl_xor_sync(0xffffffffu, (int)bad, o) != 0);
-    }
-    if (lane == 0) {
-      // s only grows: a warp whose max does not exceed the value it reads skips the atomic (a stale
-      // read is never larger than the current value, so no needed update is skipped) — 8 warps x
-      // 256 CTAs of atomics on one address cost ~2 us per full-size Pi otherwise
-      const unsigned long long vb = (unsigned long long)__double_as_longlong(vmax);
-      if (vmax > 0.0 && vb > *(volatile const unsigned long long *)scale_bits) atomicMax(scale_bits, vb);
-      if (bad) atomicOr(nonfinite, 1);
-    }
-  }
+  if (EPI == EPI_F || EPI == EPI_FZ) epi_scale(vmax, bad, scale_bits, nonfinite);
 }
 
 // dynamic shared memory: the main-loop tiles + the small-K operands

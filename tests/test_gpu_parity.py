@@ -418,6 +418,47 @@ def test_concurrent_mode_at_chi256(aci):
     assert r.returncode == 0 and r.stdout.strip().endswith("OK"), (r.stdout[-500:], r.stderr[-2000:])
 
 
+_STREAM_SCRIPT = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, ".")
+import paper_2604_00037_b200 as aci
+from workloads import make_config
+aci.load()
+for chi in (128, 256):
+    cf = make_config(3, chi, npts=0)
+    xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]
+    y0 = aci.TensorTrain.from_cores(cf["y_init"])
+    out, st, rep, ex = aci.aci_elementwise(cf["op"], xs, cf["tol"], cf["maxrank"], cf["max_sweeps"], y_init=y0,
+                                           log=True)
+    h = hashlib.sha256()
+    for e in ex["log"]:
+        h.update(np.asarray(e["rows"], np.int32).tobytes()); h.update(np.asarray(e["cols"], np.int32).tobytes())
+    for c in out.cores():
+        h.update(np.ascontiguousarray(c).tobytes())
+    print(chi, rep["pivot_steps"], h.hexdigest())
+"""
+
+
+@pytest.mark.parametrize("minimum", ["0", "67108864"])
+def test_streamed_pi_bitwise_equals_unstreamed(aci, minimum):
+    """Streamed Pi: the Pi of L->R bond b+1 computed beside the prrLU of bond b from
+    the pivot rows as they are published. Every pivot and every output core equals the unstreamed
+    run bit for bit (configs[3] chi = 128, 256; ACI_STREAM_MIN=0 streams every eligible bond).
+    Subprocesses: the switches are read once per process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({"ACI_STREAM_PI": "0"}, {"ACI_STREAM_PI": "1", "ACI_STREAM_MIN": minimum}):
+        r = subprocess.run([sys.executable, "-c", _STREAM_SCRIPT], cwd=root, capture_output=True, text=True,
+                           timeout=600, env={**os.environ, **env})
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.split())
+    assert outs[0] == outs[1]
+
+
 def test_iteration_times_reported(aci):
     cf = make_config(3, 64, npts=0)
     xs = [aci.TensorTrain.from_cores(t) for t in cf["inputs"]]

@@ -7,8 +7,10 @@
 // Streams per call: the caller's stream carries the critical path of every bond (Pi GEMM ->
 // prrLU -> update kernel); a side stream runs the look-ahead GEMM that produces the next bond's
 // operand beside the prrLU (forked off the prrLU's launch-completion event, joined by the
-// update); a third stream runs the index-set / log kernel of each bond (joined before the
-// convergence test). One iteration of all three is captured as one CUDA graph and cached.
+// update) and, for large L->R bonds, the streamed Pi of the next bond (pi_stream_kernel: rows of
+// Pi_{b+1} as the prrLU publishes the pivot rows they need); a third stream runs the index-set /
+// log kernel of each bond (joined before the convergence test). One iteration of all three is
+// captured as one CUDA graph and cached.
 // Memory: a persistent per-stream workspace (stable address -> graph-cache hits) and a
 // stream-ordered pool for TT cores.
 #include <cuda_runtime.h>

@@ -1676,6 +1676,17 @@ static void index_join(cudaStream_t st) {
   cudaStreamWaitEvent(st, sd.ix_done, 0);
 }
 
+// ACI_DEBUG_PENDING=1 (debugging): report a pending runtime error at points of a call
+static void dbg_pending(const char *where) {
+  static const bool on = [] {
+    const char *e = getenv("ACI_DEBUG_PENDING");
+    return e && atoi(e) != 0;
+  }();
+  if (!on) return;
+  const cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) fprintf(stderr, "[aci] pending %s at %s\n", cudaGetErrorString(e), where);
+}
+
 static void canon_step(Run &R, double tol, int tol_mode, int s, cudaStream_t st) {
   const int L = R.L, N = R.N;
   CanonArgs C = {};
@@ -1810,6 +1821,11 @@ static int build_run(const Inputs &I, const tt_s *y, int maxrank, int max_sweeps
 extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_inputs, double tol, int maxrank,
                                   int max_sweeps, tt_t **out, aci_report *rep, const aci_options *opts) {
   NvtxRange nv_call("aci_elementwise");
+  dbg_pending("entry");
+  // a successful call leaves the thread's last-error state as it found it: runtime calls that
+  // returned success may still leave a pending error behind (seen under ncu for launches with a
+  // launch-completion event), which the caller's next CUDA call would report as its own
+  const bool clean_entry = cudaPeekAtLastError() == cudaSuccess;
   auto t_start = std::chrono::steady_clock::now();
   if (!out) return fail(ACI_ERR_INVALID, "aci: out is null");
   *out = nullptr;
@@ -2013,8 +2029,16 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   for (it = 1; it <= max_sweeps; ++it) {
     NvtxRange nv("aci: iteration (L->R + R->L half-sweeps, convergence test)");
     if (ev_it[0]) cudaEventRecord(ev_it[0], strm);
+    if (gexec && cudaGraphLaunch(gexec, strm) != cudaSuccess) {
+      // a rejected replay (seen under ncu for graphs instantiated by an earlier call) ran nothing:
+      // drop the graph and run this and the remaining iterations as direct launches, leaving no
+      // pending runtime error behind for the caller's next CUDA call
+      cudaGetLastError();
+      graph_cache_release(gexec, gcached, true);
+      gexec = nullptr;
+      gcached = false;
+    }
     if (gexec) {
-      cudaGraphLaunch(gexec, strm);
       prof.total += prof.per_iter_launches;
       ++graph_iters;
     } else {
@@ -2235,6 +2259,8 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   if (o.profile) prof.collect(o.profile);
   if (rep) *rep = rp;
   *out = res;
+  dbg_pending("return");
+  if (clean_entry) cudaGetLastError();
   return converged ? ACI_OK : ACI_NOT_CONVERGED;
 }
 

@@ -234,14 +234,16 @@ def _ncu_traffic():
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
     if not files:
         return {}
-    d = json.load(open(files[-1]))
     out = {}
-    for k, v in d.items():
-        if (isinstance(v, dict) and "dram_bytes_read" in v and "dram_bytes_write" in v
-                and (k.startswith("prrlu_r") or k.startswith("gemmpi"))):
-            key = "prrlu" if k.startswith("prrlu") else "contraction"
-            out[key] = {"bytes": v["dram_bytes_read"] + v["dram_bytes_write"], "source": os.path.basename(files[-1]),
-                        "kernel": v["kernel"]}
+    for f in reversed(files):  # newest capture of each kernel class
+        d = json.load(open(f))
+        for k, v in d.items():
+            if (isinstance(v, dict) and "dram_bytes_read" in v and "dram_bytes_write" in v
+                    and (k.startswith("prrlu_r") or k.startswith("gemmpi"))):
+                key = "prrlu" if k.startswith("prrlu") else "contraction"
+                if key not in out:
+                    out[key] = {"bytes": v["dram_bytes_read"] + v["dram_bytes_write"], "source": os.path.basename(f),
+                                "kernel": v["kernel"]}
     return out
 
 

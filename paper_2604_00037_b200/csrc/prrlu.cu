@@ -291,7 +291,13 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   // grid), so padding entries (always exact zeros) never alias a real index and never need a
   // mask: a zero can only win when every active entry is zero, and then the factorisation stops
   // (R2) — except at k = 0, where (0, 0) (a real entry) wins the R3 tie-break.
-  const unsigned NC = (unsigned)(G * CB);
+  // NC is rounded up to a power of two (2^ncs): the flat index splits into (row, col) with a
+  // shift and a mask instead of a runtime integer division on the per-pivot critical path; the
+  // lexicographic (row, col) order of the flat indices (R3) holds for any NC >= the live width.
+  constexpr unsigned kLogCB = CB <= 1 ? 0u : (unsigned)(31 - __builtin_clz((unsigned)CB));
+  const unsigned ncs = (G == 1) ? kLogCB : (unsigned)(32 - __clz(G * CB - 1));
+  static_assert((CB & (CB - 1)) == 0, "columns per CTA must be a power of two");
+  const unsigned NC = 1u << ncs;
   // per-thread max over the register tile: NCH independent chains (slot e -> chain e % NCH),
   // strict '>' within a chain; chains merged with the slot (== flat-index) tie-break.
   double bx = 0.0;
@@ -331,7 +337,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   auto thread_key = [&]() -> Key {
     const unsigned long long bits = (unsigned long long)__double_as_longlong(bx);
     const int a = be / EB, b = be % EB;
-    const unsigned flat = (unsigned)(lane + 32 * a) * NC + (unsigned)(c0 + w + NW * b);
+    const unsigned flat = ((unsigned)(lane + 32 * a) << ncs) | (unsigned)(c0 + w + NW * b);
     return Key{(unsigned)(bits >> 32), (unsigned)bits, flat};
   };
   scan();
@@ -381,7 +387,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       // ---- push tier: key + candidate column into every cluster CTA (DSMEM), one wait
       const int par = k & 1;
       const unsigned CS = cluster_size(), crank = cluster_rank();
-      const int jc = (int)(ck.id % NC) - c0;
+      const int jc = (int)(ck.id & (NC - 1u)) - c0;
       const int pw = jc % NW;
       if (w == 0 && lane < (int)CS)
         st_async_key(mapa_u32(smem_u32(&S.ck[par][crank]), (unsigned)lane), ck.hi, ck.lo, ck.id,
@@ -416,7 +422,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       const unsigned tag = (ep << 12) | (unsigned)(k + 1);
       // the owner warp of the CTA candidate's column publishes the column (tagged packets, no
       // fence) and lane 0 publishes the key and arrives on the counter
-      const int jc = (int)(ck.id % NC) - c0;
+      const int jc = (int)(ck.id & (NC - 1u)) - c0;
       const int pw = jc % NW;
       if (XM == 2 && w == 0) {
         // cluster tier: the key goes out first (st.async into every cluster CTA's smem), the
@@ -574,7 +580,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     }
     if (k == kmax) { eps = absc; break; }
     if (k > 0 && absc <= thr) { eps = absc; break; }
-    const int p = (int)(win.id / NC), q = (int)(win.id % NC);
+    const int p = (int)(win.id >> ncs), q = (int)(win.id & (NC - 1u));
     if (g == 0 && tid == 0) { A.rows[k] = p; A.cols[k] = q; }
     if (k == 0 && absc == 0.0) {
       // R17: zero block -> rank 1, dummy pivot (0,0), U row e_q, eps 0
@@ -605,8 +611,12 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     // bit-identical to fma(-l_i, u_j, v).
     // __drcp_rn is the correctly rounded reciprocal, i.e. the same bits as 1.0 / |c|; the empty
     // asm pins its evaluation here, ahead of the column loads it would otherwise trail
-    double inv_abs = __drcp_rn(absc);
-    asm volatile("" : "+d"(inv_abs));
+    // (grid tiers: computed right after the column loads are issued, so it runs under their latency)
+    double inv_abs = 0.0;
+    if constexpr (!GRID || XM == 3) {
+      inv_abs = __drcp_rn(absc);
+      asm volatile("" : "+d"(inv_abs));
+    }
     double inv;       // signed 1/S_pq
     double ub[EB];    // pivot row (CTA tier: sign-folded, -u_j (c > 0) or +u_j (c < 0))
     if constexpr (XM == 3) {
@@ -643,6 +653,8 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
         if (i < m) ld_pkt(src + 2 * i, cw[t][0], cw[t][1]);
       }
       ld_pkt(src + 2 * p, cw[PPT][0], cw[PPT][1]);  // the pivot itself, for its sign
+      inv_abs = __drcp_rn(absc);
+      asm volatile("" : "+d"(inv_abs));
       while ((unsigned)(cw[PPT][0] >> 32) != tag || (unsigned)(cw[PPT][1] >> 32) != tag)
         ld_pkt(src + 2 * p, cw[PPT][0], cw[PPT][1]);
       const bool neg = (cw[PPT][1] & 0x80000000ull) != 0;

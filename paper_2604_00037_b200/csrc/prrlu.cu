@@ -201,6 +201,9 @@ __device__ __forceinline__ int lpair2(int i) { return ((i >> 6) << 6) | ((i & 31
 #ifndef ACI_W8_EB256
 #define ACI_W8_EB256 2
 #endif
+#ifndef ACI_NARROW512
+#define ACI_NARROW512 1
+#endif
 #ifndef ACI_W8_EB512
 #define ACI_W8_EB512 4
 #endif
@@ -644,6 +647,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       }
     } else if (GRID) {
       const unsigned tag = (ep << 12) | (unsigned)(k + 1);
+      PHASE(7);
       const unsigned long long *src = A.colpub + (((size_t)(k & 1) * G + q / CB) * A.colcap) * 2;
       constexpr int PPT = (MROWS + T - 1) / T;  // column packets per thread
       unsigned long long cw[PPT + 1][2];
@@ -930,6 +934,13 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
     ACI_CTA_VARIANT(32, 2)   // 1024 x   16
     ACI_GRID_VARIANT2(4, ACI_W8_EB128)   //  128 x 8*EB per CTA
     ACI_GRID_VARIANT2(8, ACI_W8_EB256)   //  256 x 8*EB per CTA
+#if ACI_NARROW512
+    // 512-row blocks no wider than one cluster of 16-column CTAs (configs[3]: 512 x 256, r = 256):
+    // 16 CTAs x 32 entries per thread instead of 8 CTAs x 64 (the update + scan halves)
+    if (n <= 16 * NWT * 2) {
+      ACI_GRID_VARIANT2(16, 2)
+    }
+#endif
     ACI_GRID_VARIANT2(16, ACI_W8_EB512)  //  512 x 8*EB per CTA
     ACI_GRID_VARIANT2(32, ACI_BIG_EB)    // 1024 x 8*EB per CTA
   } else {

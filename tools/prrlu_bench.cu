@@ -14,7 +14,10 @@ int main(int argc, char **argv) {
                     {64, 64, 64, 1024}, {128, 128, 128, 1024}, {256, 256, 256, 1024}, {512, 512, 512, 1024},
                     {64, 64, 64, 256}, {128, 128, 128, 256}, {256, 128, 128, 256}, {128, 256, 128, 256},
                     {200, 250, 200, 256}, {256, 64, 64, 256}, {64, 256, 64, 256}, {128, 64, 64, 256},
-                    {96, 96, 96, 256}};
+                    {96, 96, 96, 256},
+                    // the product's dominant shapes at configs[3] chi = 256 (oracle log: m, n, r x bonds)
+                    {512, 1024, 512, 1024}, {512, 256, 256, 1024}, {128, 256, 128, 1024}, {128, 64, 64, 1024},
+                    {256, 1024, 256, 1024}, {512, 128, 128, 1024}};
   double *dM, *dU, *deps;
   unsigned long long *dcol;
   int *drows, *dcols, *dr;
@@ -96,7 +99,7 @@ int main(int argc, char **argv) {
         for (int t = 0; t < r; ++t) hsh = (hsh ^ (unsigned)(hr[t] * 4099 + hc[t])) * 1099511628211ull;
         printf("%4dx%4d (static %4d) r=%4d: %8.1f us total, %6.3f us/pivot | cycles/pivot:", m, n, stat, r, ms * 1e3,
                ms * 1e3 / r);
-        for (int t = 0; t < 7; ++t) printf(" p%d=%lld", t, dbg[t] / (r > 0 ? r : 1));
+        for (int t = 0; t < 8; ++t) printf(" p%d=%lld", t, dbg[t] / (r > 0 ? r : 1));
         printf(" | piv %016llx\n", hsh);
       }
     }

@@ -898,9 +898,11 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel_rook(LuArgs A) {
 // rounded up to whole clusters (CTAs past the live columns hold padding only).
 // ACI_CLUSTER_CTA_MAXE: in the cluster kernel (XM = 2, real), one-CTA variants with more register
 // entries per thread than this are skipped, so such live blocks (e.g. 128 x 128 inside a 256-wide
-// launch) spread over the cluster's CTAs instead of one SM (A/B switch; 64 = every variant)
+// launch) spread over the cluster's CTAs instead of one SM (A/B switch; 64 = every variant).
+// 32 measured faster on products (chi = 64/128/256: 20.9/35.6/56.9 -> 20.5/35.3/56.6 ms, identical
+// pivots, profiles/r02zg_cta_maxe_ab.txt)
 #ifndef ACI_CLUSTER_CTA_MAXE
-#define ACI_CLUSTER_CTA_MAXE 64
+#define ACI_CLUSTER_CTA_MAXE 32
 #endif
 template <int NWT, int XM, bool CPLX>
 __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {

@@ -253,8 +253,45 @@ struct RookSmem : PrrluSmem {
 // readings RZ1-RZ4: the key is w = fl(re^2) + fl(im^2), |c| = sqrt(w),
 // inv = (c_re / w, -c_im / w), l_i = S_iq * inv and u-row products as RZ3 (no FMA contraction),
 // the Schur update as the RZ4 fma sequence. Bit-identical to oracle/aci_oracle_z.c for equal Pi.
-template <int EA, int EB, int NW, int XM, bool CPLX = false>
-__device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const int G, const int g) {
+// ---- Hand-off (HO) of a multi-cluster factorisation to ONE cluster (ACI_HANDOFF). A block that
+// needs two 16-CTA clusters (the 512 x 1024 blocks of configs[3] at chi = 256: 512 pivots with a
+// cross-cluster L2 leg each) shrinks as it is factorised: after K pivots the live Schur complement
+// is (m - K) x (n - K). At k = K every CTA writes its live entries, compacted (eliminated rows and
+// columns dropped, order kept), to a scratch area; the first cluster reloads the compacted block
+// into a one-cluster register layout and continues from pivot K with the same threshold, first
+// candidate and tie-break (the compacted (row, col) order is the original one: the maps are
+// increasing), so the pivots and the arithmetic are exactly those of the uninterrupted run.
+// Phase 1 (HO = 1) keeps bitmaps of the eliminated rows / columns; phase 2 (HO = 2) maps its
+// compacted pivot indices and U columns back. Shared scratch (S.raw, unused by the real grid
+// tiers), as 32-bit words:
+constexpr int kHoDeadR = 0;      // 32 words: eliminated rows (<= 1024)
+constexpr int kHoDeadC = 32;     // 48 words: eliminated columns (<= 1536)
+constexpr int kHoPrefR = 80;     // exclusive prefix of the popcounts of kHoDeadR
+constexpr int kHoPrefC = 112;    // exclusive prefix of the popcounts of kHoDeadC
+constexpr int kHoRowMap = 160;   // compacted row -> original row (<= 1024)
+constexpr int kHoColMap = 1184;  // compacted column -> original column (<= 1536)
+constexpr int kHoDeadList = 2720;  // eliminated columns in increasing order (<= 1024)
+constexpr int kHoFlags = 1024;   // grid barrier flags in A.keys (u64 words [1024, 1024 + 2 G))
+constexpr int kHoEA = 8, kHoEB = 6;  // phase-2 register tile: 256 rows x 16 CTAs x 48 columns
+#ifndef ACI_HANDOFF
+#define ACI_HANDOFF 1
+#endif
+struct HoState {
+  int k;         // pivots done before the hand-off (phase 2 starts at pivot k)
+  double first;  // |first candidate| (R8 threshold mode)
+  double thr;
+  bool handed;
+};
+__device__ __forceinline__ unsigned *ho_words(PrrluSmem &S) { return reinterpret_cast<unsigned *>(S.raw); }
+// compacted index of original index i: i minus the eliminated ones below it
+__device__ __forceinline__ int ho_rank(const unsigned *dead, const unsigned *pref, int i) {
+  return i - (int)(pref[i >> 5] + __popc(dead[i >> 5] & ((1u << (i & 31)) - 1u)));
+}
+
+template <int EA, int EB, int NW, int XM, bool CPLX = false, int HO = 0>
+__device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const int G, const int g,
+                                           HoState *hs = nullptr) {
+  static_assert(HO == 0 || (XM == 2 && !CPLX), "hand-off: real cluster tier only");
   constexpr bool GRID = XM != 0;
   constexpr int Z = CPLX ? 2 : 1;  // doubles per entry
   constexpr int T = NW * 32;
@@ -267,11 +304,20 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   const int lane = tid & 31, w = tid >> 5;
   const int c0 = g * CB;
 
-  const int m = A.dims->m, n = A.dims->n, ldm = A.dims->ldm, kmax = A.dims->kmax, ldu = A.dims->ldu;
+  // phase 2 of a hand-off works on the compacted (m - K) x (n - K) block, pivots numbered from K
+  const int k0 = HO == 2 ? hs->k : 0;
+  const int m = A.dims->m - k0, n = A.dims->n - k0, kmax = A.dims->kmax, ldu = A.dims->ldu;
+  const int ldm = HO == 2 ? n : A.dims->ldm;
   const unsigned ep = GRID ? (*A.epoch & 0xfffffu) : 0u;  // read by every CTA before any arrival
-  const int mn = m < n ? m : n;
+  const int mn = (m < n ? m : n) + k0;
   double thr = A.tol;
   if (A.thr_mode == 0) thr = A.tol * __longlong_as_double((long long)*A.scale_bits);
+  // hand-off scratch: the compacted live block, behind the exchange slots of a 64-CTA grid
+  double *const hbuf = reinterpret_cast<double *>(A.colpub + (size_t)2 * 64 * A.colcap * 2);
+  const double *const Msrc = HO == 2 ? hbuf : A.M;
+  unsigned *const hw = ho_words(S);
+  if constexpr (HO == 1)
+    for (int i = tid; i < kHoPrefR; i += T) hw[i] = 0u;  // eliminated-row / -column bitmaps
 
   // ---- load; padding = 0 and never a candidate
   double v[EA][EB][Z];
@@ -286,7 +332,10 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     for (int b = 0; b < EB; ++b)
 #pragma unroll
       for (int z = 0; z < Z; ++z)
-        v[a][b][z] = (rok[a] && cok[b]) ? A.M[((size_t)(lane + 32 * a) * ldm + c0 + w + NW * b) * Z + z] : 0.0;
+        v[a][b][z] = (rok[a] && cok[b])
+                         ? (HO == 2 ? __ldcg(Msrc + (size_t)(lane + 32 * a) * ldm + c0 + w + NW * b)
+                                    : Msrc[((size_t)(lane + 32 * a) * ldm + c0 + w + NW * b) * Z + z])
+                         : 0.0;
   for (int i = tid; i < Z * kMaxRows; i += T) s_l[i] = 0.0;
   for (int j = tid; j < Z * kMaxCB; j += T) s_u[j] = 0.0;
 
@@ -298,8 +347,8 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
   // shift and a mask instead of a runtime integer division on the per-pivot critical path; the
   // lexicographic (row, col) order of the flat indices (R3) holds for any NC >= the live width.
   constexpr unsigned kLogCB = CB <= 1 ? 0u : (unsigned)(31 - __builtin_clz((unsigned)CB));
-  const unsigned ncs = (G == 1) ? kLogCB : (unsigned)(32 - __clz(G * CB - 1));
-  static_assert((CB & (CB - 1)) == 0, "columns per CTA must be a power of two");
+  const unsigned ncs = (XM == 0) ? kLogCB : (unsigned)(32 - __clz(G * CB - 1));
+  static_assert(XM != 0 || (CB & (CB - 1)) == 0, "one-CTA tiers: columns per CTA a power of two");
   const unsigned NC = 1u << ncs;
   // per-thread max over the register tile: NCH independent chains (slot e -> chain e % NCH),
   // strict '>' within a chain; chains merged with the slot (== flat-index) tie-break.
@@ -370,14 +419,69 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     cluster_sync_all();
   }
 
-  double first = 0.0, eps = 0.0;
-  int k = 0;
+  double first = HO == 2 ? hs->first : 0.0, eps = 0.0;
+  if constexpr (HO == 2) thr = hs->thr;
+  int k = k0;
+  bool handed = false;
 #ifdef ACI_PRRLU_TIMING
   long long ph_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long ph_t_ = clock64();
 #endif
   for (;;) {
     if (k == mn) { eps = 0.0; break; }
+    if constexpr (HO == 1) {
+      if (k == hs->k) {
+        // ---- hand-off: write the live entries, compacted, then publish this CTA's flag
+        __syncthreads();  // the bitmaps of pivots 0..K-1 (thread 0) are complete
+        if (w == 0) {
+          // exclusive prefix of the popcounts: rows (32 words) and columns (48 words)
+          const unsigned pr = __popc(hw[kHoDeadR + lane]);
+          unsigned xr = pr;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(FULL, xr, o);
+            if (lane >= o) xr += t;
+          }
+          hw[kHoPrefR + lane] = xr - pr;
+          const unsigned c_lo = __popc(hw[kHoDeadC + lane]);
+          const unsigned c_hi = lane < 16 ? __popc(hw[kHoDeadC + 32 + lane]) : 0u;
+          unsigned xl = c_lo, xh = c_hi;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned tl = __shfl_up_sync(FULL, xl, o), th = __shfl_up_sync(FULL, xh, o);
+            if (lane >= o) { xl += tl; xh += th; }
+          }
+          const unsigned tot_lo = __shfl_sync(FULL, xl, 31);
+          hw[kHoPrefC + lane] = xl - c_lo;
+          if (lane < 16) hw[kHoPrefC + 32 + lane] = tot_lo + xh - c_hi;
+        }
+        __syncthreads();
+        const int ldh = n - k;  // compacted width
+#pragma unroll
+        for (int a = 0; a < EA; ++a) {
+          const int i = lane + 32 * a;
+          if (i < m && !((hw[kHoDeadR + (i >> 5)] >> (i & 31)) & 1u)) {
+            const int ri = ho_rank(hw + kHoDeadR, hw + kHoPrefR, i);
+#pragma unroll
+            for (int b = 0; b < EB; ++b) {
+              const int j = c0 + w + NW * b;
+              if (j < n && !((hw[kHoDeadC + (j >> 5)] >> (j & 31)) & 1u))
+                hbuf[(size_t)ri * ldh + ho_rank(hw + kHoDeadC, hw + kHoPrefC, j)] = v[a][b][0];
+            }
+          }
+        }
+        __syncthreads();
+        if (tid == 0) {
+          __threadfence();
+          st_pkt(A.keys + 2 * (kHoFlags / 2 + g), tagged(ep, 0xfffu), 0ull);
+        }
+        hs->first = first;
+        hs->thr = thr;
+        hs->handed = true;
+        handed = true;
+        break;
+      }
+    }
     // ---- warp -> CTA argmax
     const Key wk = warp_argmax(thread_key());
     if (lane == 0) { s_hi[w] = wk.hi; s_lo[w] = wk.lo; s_id[w] = wk.id; }
@@ -584,7 +688,20 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     if (k == kmax) { eps = absc; break; }
     if (k > 0 && absc <= thr) { eps = absc; break; }
     const int p = (int)(win.id >> ncs), q = (int)(win.id & (NC - 1u));
-    if (g == 0 && tid == 0) { A.rows[k] = p; A.cols[k] = q; }
+    if (g == 0 && tid == 0) {
+      if constexpr (HO == 2) {
+        A.rows[k] = (int)hw[kHoRowMap + p];
+        A.cols[k] = (int)hw[kHoColMap + q];
+      } else {
+        A.rows[k] = p;
+        A.cols[k] = q;
+      }
+    }
+    if constexpr (HO == 1)
+      if (tid == 0) {  // eliminated row p and column q (the hand-off's compaction)
+        hw[kHoDeadR + (p >> 5)] |= 1u << (p & 31);
+        hw[kHoDeadC + (q >> 5)] |= 1u << (q & 31);
+      }
     if (k == 0 && absc == 0.0) {
       // R17: zero block -> rank 1, dummy pivot (0,0), U row e_q, eps 0
       if (A.U)
@@ -674,11 +791,23 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
       }
       __syncthreads();  // S3
       PHASE(5);
-      if (A.U)
+      if (A.U) {
         for (int jj = tid; jj < CB; jj += T) {
           const int j = c0 + jj;
-          if (j < n) A.U[(size_t)k * ldu + j] = (j == q) ? 1.0 : s_u[jj] * inv;
+          if (j < n) {
+            const int jo = HO == 2 ? (int)hw[kHoColMap + j] : j;
+            A.U[(size_t)k * ldu + jo] = (j == q) ? 1.0 : s_u[jj] * inv;
+          }
         }
+        if constexpr (HO == 2) {
+          // columns eliminated before the hand-off: their pivot-row entries are exact +0, so U = 0 * inv
+          const int per = (k0 + G - 1) / G;
+          for (int t = tid; t < per; t += T) {
+            const int d = g * per + t;
+            if (d < k0) A.U[(size_t)k * ldu + (int)hw[kHoDeadList + d]] = 0.0 * inv;
+          }
+        }
+      }
 #pragma unroll
       for (int b = 0; b < EB; ++b) ub[b] = s_u[w + NW * b];
       if constexpr (!kNoWork) {
@@ -845,7 +974,7 @@ __device__ __forceinline__ void prrlu_body(const LuArgs &A, PrrluSmem &S, const 
     // s_l / s_u / s_raw are rewritten only after the next S1; every thread finished reading
     // them before arriving there.
   }
-  if (g == 0 && tid == 0) {
+  if (g == 0 && tid == 0 && !handed) {
     *A.r_out = k;
     *A.eps_out = eps;
     // every CTA read the epoch before its first arrival, and CTA 0 only gets here after the
@@ -941,6 +1070,46 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
     // 16 CTAs x 32 entries per thread instead of 8 CTAs x 64 (the update + scan halves)
     if (n <= 16 * NWT * 2) {
       ACI_GRID_VARIANT2(16, 2)
+    }
+#endif
+#if ACI_HANDOFF
+    // 257..512-row blocks that need two or more 16-CTA clusters: hand off to one cluster once the
+    // live block fits kHoEA x kHoEB per thread (hand-off comment above prrlu_body)
+    if constexpr (XM == 2 && !CPLX) {
+      if (m > 256 && m <= 512) {
+        const int CS = (int)cluster_size();
+        int Gl = (n + NWT * ACI_W8_EB512 - 1) / (NWT * ACI_W8_EB512);
+        Gl = (Gl + CS - 1) / CS * CS;
+        const int K = max(m - 32 * kHoEA, n - 16 * NWT * kHoEB), mn = min(m, n);
+        if (CS == 16 && Gl > CS && Gl <= 64 && K > 0 && K < min(A.dims->kmax, mn) &&
+            (size_t)(m - K) * (size_t)(n - K) <= (size_t)(2 * kMaxCTAs - 64) * (size_t)A.colcap * 2) {
+          if (g >= Gl) return;
+          HoState hs{K, 0.0, 0.0, false};
+          prrlu_body<16, ACI_W8_EB512, NWT, 2, false, 1>(A, S, Gl, g, &hs);
+          if (!hs.handed || g >= CS) return;
+          const int tid = threadIdx.x;
+          if (tid < Gl) {  // every CTA's compacted entries are out
+            const unsigned long long want = tagged(*A.epoch & 0xfffffu, 0xfffu);
+            unsigned long long w0, w1;
+            do {
+              ld_pkt(A.keys + 2 * (kHoFlags / 2 + tid), w0, w1);
+            } while (w0 != want);
+            __threadfence();
+          }
+          unsigned *hw = ho_words(S);
+          for (int i = tid; i < m; i += NWT * 32)
+            if (!((hw[kHoDeadR + (i >> 5)] >> (i & 31)) & 1u)) hw[kHoRowMap + ho_rank(hw + kHoDeadR, hw + kHoPrefR, i)] = i;
+          for (int j = tid; j < n; j += NWT * 32) {
+            const int rj = ho_rank(hw + kHoDeadC, hw + kHoPrefC, j);
+            if ((hw[kHoDeadC + (j >> 5)] >> (j & 31)) & 1u) hw[kHoDeadList + (j - rj)] = j;
+            else hw[kHoColMap + rj] = j;
+          }
+          if (tid < 4) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&S.mb[tid])) : "memory");
+          __syncthreads();
+          prrlu_body<kHoEA, kHoEB, NWT, 2, false, 2>(A, S, CS, g, &hs);
+          return;
+        }
+      }
     }
 #endif
     ACI_GRID_VARIANT2(16, ACI_W8_EB512)  //  512 x 8*EB per CTA

@@ -59,6 +59,50 @@ def measure_prrlu_latency(sizes=(64, 128, 256, 512, 1024)):
     return out
 
 
+def measure_prrlu_latency_shapes(log, dims, maxrank):
+    """Per-pivot time of the library's prrLU with and without the rank-1 update + rescan
+    (ACI_PRRLU_NOWORK) on seeded blocks of EVERY (live m x n, pivots r) shape of one product's pivot
+    log, each launched for its bond's static size as the product launches it (so tier choice and
+    the hand-off are those of the product); returns (floor_ms, kernel_ms, per-shape rows), both
+    weighted by the log's pivot counts."""
+    import ctypes
+    from paper_2604_00037_b200 import _build
+    lib = ctypes.CDLL(_build.build_peak())
+    lib.aci_peak_prrlu_shape.argtypes = [ctypes.c_int] * 6 + [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                                                ctypes.POINTER(ctypes.c_int)]
+    L = len(dims)
+
+    def rmax(b):  # csrc/aci.cu: min(maxrank, prod d[0..b], prod d[b+1..L-1])
+        lo = hi = 1
+        for t in range(b + 1):
+            lo = min(lo * dims[t], 1 << 30)
+        for t in range(b + 1, L):
+            hi = min(hi * dims[t], 1 << 30)
+        return min(maxrank, lo, hi)
+
+    shapes = {}
+    for e in log:
+        b = e["bond"]
+        m, n = dims[b] * e["rl"], dims[b + 1] * e["rr"]
+        sm = dims[b] * (1 if b == 0 else rmax(b - 1))
+        sn = dims[b + 1] * (1 if b == L - 2 else rmax(b + 1))
+        key = (m, n, max(e["r"], 1), sm, sn)
+        shapes[key] = shapes.get(key, 0) + e["r"]
+    rows, floor_ms, kern_ms = [], 0.0, 0.0
+    for (m, n, r, sm, sn), cnt in sorted(shapes.items(), key=lambda kv: -kv[1]):
+        row = {"m": m, "n": n, "r": r, "static": [sm, sn], "pivots": cnt}
+        for key, nowork in (("kernel_us", 0), ("floor_us", 1)):
+            v, piv = ctypes.c_double(0.0), ctypes.c_int(0)
+            rc = lib.aci_peak_prrlu_shape(m, n, r, sm, sn, nowork, 3, ctypes.byref(v), ctypes.byref(piv))
+            row[key] = v.value if rc == 0 else None
+        if row["floor_us"]:
+            floor_ms += cnt * row["floor_us"] / 1e3
+        if row["kernel_us"]:
+            kern_ms += cnt * row["kernel_us"] / 1e3
+        rows.append(row)
+    return floor_ms, kern_ms, rows
+
+
 def _block_tier(m, n):
     """The probe size whose tier a live m x n block runs in (prrlu.cu variant lists)."""
     big = max(m, n)
@@ -705,7 +749,7 @@ def main():
     if e2e is not None:
         e2e["value"] = e2e_sum
     pk = measure_peaks()  # after the timed regions: the same process, clocks and GPU
-    lat, piv_by_tier = None, {}
+    lat, piv_by_tier, lat_shapes = None, {}, None
     if rank == 0:
         lat = measure_prrlu_latency()
         cfl = make_config(3, args.chi, npts=0)
@@ -717,6 +761,7 @@ def main():
         for e in ex_["log"]:
             t = _block_tier(2 * e["rl"], 2 * e["rr"])
             piv_by_tier[t] = piv_by_tier.get(t, 0) + e["r"]
+        lat_shapes = measure_prrlu_latency_shapes(ex_["log"], cfl["inputs"][0].d, cfl["maxrank"])
     if rank == 0:
         value = f_sum / t_max / 1e9  # GFLOP/ms -> TFLOP/s
         steps = args.steps
@@ -737,6 +782,17 @@ def main():
                       "product_prrlu_ms": pr["ms"], "frac": floor_ms / pr["ms"] if pr["ms"] else None,
                       "pivots_by_block": {str(k): v for k, v in sorted(piv_by_tier.items())},
                       "by_block": {str(k): v for k, v in lat.items()}}
+            if lat_shapes is not None:
+                # the same floor per (m, n, r) shape of the product's own log, launched for each bond's
+                # static size (tiers and hand-off as in the product): this one is reported as 'frac'
+                sf, sk, srows = lat_shapes
+                lat_fr = dict(lat_fr, **{
+                    "floor_ms_per_product": sf, "probe_kernel_ms_per_product": sk,
+                    "frac": sf / pr["ms"] if pr["ms"] else None,
+                    "square_blocks": {"floor_ms_per_product": floor_ms, "probe_kernel_ms_per_product": kern_ms,
+                                      "frac": floor_ms / pr["ms"] if pr["ms"] else None,
+                                      "note": "seeded m x m blocks by max(m, n) class (round-2 method)"},
+                    "by_shape_top": srows[:12]})
         roof_prrlu = {"kernel": "prrlu_kernel (a5)", "bound": "alu",
                       "achieved": prrlu_flops / (pr["ms"] * 1e9) if pr["ms"] else None,
                       "peak": pk["dfma_tflops"], "unit": "TFLOP/s",
@@ -747,8 +803,10 @@ def main():
                           "per_pivot_us": 1e3 * pr["ms"] / max(reps[-1]["pivot_steps"], 1),
                           "floor_source": "measured in this run: the library's prrLU with the rank-1 update and "
                                           "rescan compiled out (csrc/peak_probe.cu, ACI_PRRLU_NOWORK) on seeded "
-                                          "m x m blocks, i.e. the exchange chain alone per pivot; weighted by the "
-                                          "product's pivots per block size; frac = floor / product prrLU time"}),
+                                          "blocks of every (m, n, r) shape of the product's pivot log, each in its "
+                                          "bond's static launch (tiers and hand-off as in the product), i.e. the "
+                                          "exchange chain alone per pivot; weighted by the log's pivots; frac = "
+                                          "floor / product prrLU time"}),
                       "note": "latency-bound: one cluster/L2 exchange per pivot (DESIGN.md §5); 'frac' above is "
                               "against the DFMA register loop measured in this run (peaks.dfma_tflops), "
                               "'latency.frac' against the measured exchange floor"}

@@ -131,9 +131,19 @@ __global__ void fill_kernel(double *M, size_t n, unsigned long long seed) {
 }
 }  // namespace
 
+// Per-pivot time of the library's prrLU on a seeded live m x n block (ld = n, at most kmax pivots)
+// inside a launch sized for the static sm x sn block, as the product launches it (tier choice and
+// hand-off included); nowork = 1: the ACI_PRRLU_NOWORK build (the exchange chain alone).
+extern "C" int aci_peak_prrlu_shape(int m, int n, int kmax, int sm, int sn, int nowork, int reps,
+                                    double *us_per_pivot, int *pivots);
 extern "C" int aci_peak_prrlu(int m, int nowork, int reps, double *us_per_pivot, int *pivots) {
-  if (!us_per_pivot || m < 32 || m > 1024) return -1;
-  const int kmax = m > 512 ? 512 : m;
+  if (m < 32 || m > 1024) return -1;
+  return aci_peak_prrlu_shape(m, m, m > 512 ? 512 : m, m, m, nowork, reps, us_per_pivot, pivots);
+}
+
+extern "C" int aci_peak_prrlu_shape(int m, int n, int kmax, int sm, int sn, int nowork, int reps,
+                                    double *us_per_pivot, int *pivots) {
+  if (!us_per_pivot || m < 1 || n < 1 || m > sm || n > sn || sm > 1024 || sn > 1184 || kmax < 1) return -1;
   double *M = nullptr, *U = nullptr, *eps = nullptr;
   unsigned long long *colpub = nullptr, *keys = nullptr, *scale = nullptr;
   int *rows = nullptr, *cols = nullptr, *r = nullptr;
@@ -143,7 +153,7 @@ extern "C" int aci_peak_prrlu(int m, int nowork, int reps, double *us_per_pivot,
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   const size_t colpub_words = (size_t)2 * 148 * 1024 * 2;
   if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaMalloc(&M, sizeof(double) * m * m) != cudaSuccess || cudaMalloc(&U, sizeof(double) * m * m) != cudaSuccess ||
+      cudaMalloc(&M, sizeof(double) * m * n) != cudaSuccess || cudaMalloc(&U, sizeof(double) * kmax * n) != cudaSuccess ||
       cudaMalloc(&eps, 8) != cudaSuccess || cudaMalloc(&colpub, 8 * colpub_words) != cudaSuccess ||
       cudaMalloc(&keys, 8 * 2 * 148 * 4) != cudaSuccess || cudaMalloc(&scale, 8) != cudaSuccess ||
       cudaMalloc(&rows, 4 * 1024) != cudaSuccess || cudaMalloc(&cols, 4 * 1024) != cudaSuccess ||
@@ -151,12 +161,12 @@ extern "C" int aci_peak_prrlu(int m, int nowork, int reps, double *us_per_pivot,
       cudaMalloc(&dims, sizeof(LuDims)) != cudaSuccess || cudaEventCreate(&e0) != cudaSuccess ||
       cudaEventCreate(&e1) != cudaSuccess)
     return -5;
-  fill_kernel<<<296, 256, 0, st>>>(M, (size_t)m * m, 12345ull + m);
+  fill_kernel<<<296, 256, 0, st>>>(M, (size_t)m * n, 12345ull + m + 7919ull * n);
   cudaMemsetAsync(colpub, 0, 8 * colpub_words, st);
   cudaMemsetAsync(keys, 0, 8 * 2 * 148 * 4, st);
   cudaMemsetAsync(epoch, 0, 4, st);
   cudaMemsetAsync(scale, 0, 8, st);
-  LuDims D{m, m, m, kmax, m};
+  LuDims D{m, n, n, kmax, n};
   cudaMemcpyAsync(dims, &D, sizeof(D), cudaMemcpyHostToDevice, st);
   LuArgs a = {};
   a.M = M; a.dims = dims; a.tol = 0.0; a.thr_mode = 2; a.scale_bits = scale;
@@ -165,8 +175,8 @@ extern "C" int aci_peak_prrlu(int m, int nowork, int reps, double *us_per_pivot,
   if (nowork) probe_nowork::prrlu_init();
   else probe_work::prrlu_init();
   auto launch = [&]() {
-    return nowork ? probe_nowork::launch_prrlu(a, m, m, st, false, false, nullptr, false)
-                  : probe_work::launch_prrlu(a, m, m, st, false, false, nullptr, false);
+    return nowork ? probe_nowork::launch_prrlu(a, sm, sn, st, false, false, nullptr, false)
+                  : probe_work::launch_prrlu(a, sm, sn, st, false, false, nullptr, false);
   };
   cudaError_t le = launch();
   double best = 1e30;

@@ -1033,6 +1033,46 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel_rook(LuArgs A) {
 #ifndef ACI_CLUSTER_CTA_MAXE
 #define ACI_CLUSTER_CTA_MAXE 32
 #endif
+// The hand-off pivot is a multiple of 4: phase 2 re-initialises the key mbarriers, and the body
+// waits on mbarrier (k & 1) with parity (k >> 1) & 1, so its first two waits (steps K, K + 1) are
+// on phase 0 of fresh mbarriers only if K % 4 == 0
+__device__ __forceinline__ int ho_round(int K) { return (K + 3) & ~3; }
+// Hand-off eligibility: K pivots before it, some after it, and room for the compacted block
+__device__ __forceinline__ bool ho_ok(const LuArgs &A, int m, int n, int K) {
+  const int mn = m < n ? m : n, kx = A.dims->kmax < mn ? A.dims->kmax : mn;
+  return K > 0 && K < kx &&
+         (size_t)(m - K) * (size_t)(n - K) <= (size_t)(2 * kMaxCTAs - 64) * (size_t)A.colcap * 2;
+}
+// Phase 1 on Gl CTAs with an EA1 x EB1 tile, then (if it reached pivot K) phase 2 on the first 16
+// CTAs (one cluster) with an EA2 x EB2 tile (hand-off comment above prrlu_body)
+template <int EA1, int EB1, int EA2, int EB2, int NWT>
+__device__ __forceinline__ void ho_run(const LuArgs &A, PrrluSmem &S, int m, int n, int g, int Gl, int K) {
+  constexpr int CS = 16;
+  HoState hs{K, 0.0, 0.0, false};
+  prrlu_body<EA1, EB1, NWT, 2, false, 1>(A, S, Gl, g, &hs);
+  if (!hs.handed || g >= CS) return;
+  const int tid = threadIdx.x;
+  if (tid < Gl) {  // every CTA's compacted entries are out
+    const unsigned long long want = tagged(*A.epoch & 0xfffffu, 0xfffu);
+    unsigned long long w0, w1;
+    do {
+      ld_pkt(A.keys + 2 * (kHoFlags / 2 + tid), w0, w1);
+    } while (w0 != want);
+    __threadfence();
+  }
+  unsigned *hw = ho_words(S);
+  for (int i = tid; i < m; i += NWT * 32)
+    if (!((hw[kHoDeadR + (i >> 5)] >> (i & 31)) & 1u)) hw[kHoRowMap + ho_rank(hw + kHoDeadR, hw + kHoPrefR, i)] = i;
+  for (int j = tid; j < n; j += NWT * 32) {
+    const int rj = ho_rank(hw + kHoDeadC, hw + kHoPrefC, j);
+    if ((hw[kHoDeadC + (j >> 5)] >> (j & 31)) & 1u) hw[kHoDeadList + (j - rj)] = j;
+    else hw[kHoColMap + rj] = j;
+  }
+  if (tid < 4) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&S.mb[tid])) : "memory");
+  __syncthreads();
+  prrlu_body<EA2, EB2, NWT, 2, false, 2>(A, S, CS, g, &hs);
+}
+
 template <int NWT, int XM, bool CPLX>
 __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
   __shared__ PrrluSmem S;
@@ -1069,6 +1109,17 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
     // 512-row blocks no wider than one cluster of 16-column CTAs (configs[3]: 512 x 256, r = 256):
     // 16 CTAs x 32 entries per thread instead of 8 CTAs x 64 (the update + scan halves)
     if (n <= 16 * NWT * 2) {
+#if ACI_HANDOFF
+      // one cluster, 32 entries per thread: once the live block fits 384 x 128 (e.g. 512 x 256 at
+      // pivot 128) it continues on 12 x 1 entries per thread
+      if constexpr (XM == 2 && !CPLX) {
+        const int K = ho_round(max(m - 384, n - 128));
+        if (m > 256 && m <= 512 && cluster_size() == 16 && ho_ok(A, m, n, K)) {
+          if (g < 16) ho_run<16, 2, 12, 1, NWT>(A, S, m, n, g, 16, K);
+          return;
+        }
+      }
+#endif
       ACI_GRID_VARIANT2(16, 2)
     }
 #endif
@@ -1080,33 +1131,9 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
         const int CS = (int)cluster_size();
         int Gl = (n + NWT * ACI_W8_EB512 - 1) / (NWT * ACI_W8_EB512);
         Gl = (Gl + CS - 1) / CS * CS;
-        const int K = max(m - 32 * kHoEA, n - 16 * NWT * kHoEB), mn = min(m, n);
-        if (CS == 16 && Gl > CS && Gl <= 64 && K > 0 && K < min(A.dims->kmax, mn) &&
-            (size_t)(m - K) * (size_t)(n - K) <= (size_t)(2 * kMaxCTAs - 64) * (size_t)A.colcap * 2) {
-          if (g >= Gl) return;
-          HoState hs{K, 0.0, 0.0, false};
-          prrlu_body<16, ACI_W8_EB512, NWT, 2, false, 1>(A, S, Gl, g, &hs);
-          if (!hs.handed || g >= CS) return;
-          const int tid = threadIdx.x;
-          if (tid < Gl) {  // every CTA's compacted entries are out
-            const unsigned long long want = tagged(*A.epoch & 0xfffffu, 0xfffu);
-            unsigned long long w0, w1;
-            do {
-              ld_pkt(A.keys + 2 * (kHoFlags / 2 + tid), w0, w1);
-            } while (w0 != want);
-            __threadfence();
-          }
-          unsigned *hw = ho_words(S);
-          for (int i = tid; i < m; i += NWT * 32)
-            if (!((hw[kHoDeadR + (i >> 5)] >> (i & 31)) & 1u)) hw[kHoRowMap + ho_rank(hw + kHoDeadR, hw + kHoPrefR, i)] = i;
-          for (int j = tid; j < n; j += NWT * 32) {
-            const int rj = ho_rank(hw + kHoDeadC, hw + kHoPrefC, j);
-            if ((hw[kHoDeadC + (j >> 5)] >> (j & 31)) & 1u) hw[kHoDeadList + (j - rj)] = j;
-            else hw[kHoColMap + rj] = j;
-          }
-          if (tid < 4) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&S.mb[tid])) : "memory");
-          __syncthreads();
-          prrlu_body<kHoEA, kHoEB, NWT, 2, false, 2>(A, S, CS, g, &hs);
+        const int K = ho_round(max(m - 32 * kHoEA, n - 16 * NWT * kHoEB));
+        if (CS == 16 && Gl > CS && Gl <= 64 && ho_ok(A, m, n, K)) {
+          if (g < Gl) ho_run<16, ACI_W8_EB512, kHoEA, kHoEB, NWT>(A, S, m, n, g, Gl, K);
           return;
         }
       }

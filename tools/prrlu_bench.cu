@@ -17,7 +17,9 @@ int main(int argc, char **argv) {
                     {96, 96, 96, 256},
                     // the product's dominant shapes at configs[3] chi = 256 (oracle log: m, n, r x bonds)
                     {512, 1024, 512, 1024}, {512, 256, 256, 1024}, {128, 256, 128, 1024}, {128, 64, 64, 1024},
-                    {256, 1024, 256, 1024}, {512, 128, 128, 1024}};
+                    {256, 1024, 256, 1024}, {512, 128, 128, 1024},
+                    // hand-off pivots that are not multiples of 4 before rounding (prrlu.cu ho_round)
+                    {300, 130, 130, 1024}, {450, 250, 250, 1024}, {500, 200, 200, 1024}, {400, 1000, 400, 1024}};
   double *dM, *dU, *deps;
   unsigned long long *dcol;
   int *drows, *dcols, *dr;

@@ -204,6 +204,9 @@ __device__ __forceinline__ int lpair2(int i) { return ((i >> 6) << 6) | ((i & 31
 #ifndef ACI_NARROW512
 #define ACI_NARROW512 1
 #endif
+#ifndef ACI_NARROW128
+#define ACI_NARROW128 1
+#endif
 #ifndef ACI_W8_EB512
 #define ACI_W8_EB512 4
 #endif
@@ -1103,6 +1106,13 @@ __global__ void __launch_bounds__(NWT * 32) prrlu_kernel(LuArgs A) {
     ACI_CTA_VARIANT(8, 8)    //  256 x   64
     ACI_CTA_VARIANT(2, 32)   //   64 x  256
     ACI_CTA_VARIANT(32, 2)   // 1024 x   16
+#if ACI_NARROW128
+    // 128-row blocks no wider than one cluster of 16-column CTAs (configs[3]: 128 x 256): 16 CTAs x
+    // 8 entries per thread instead of 8 CTAs x 16
+    if (n <= 16 * NWT * 2) {
+      ACI_GRID_VARIANT2(4, 2)
+    }
+#endif
     ACI_GRID_VARIANT2(4, ACI_W8_EB128)   //  128 x 8*EB per CTA
     ACI_GRID_VARIANT2(8, ACI_W8_EB256)   //  256 x 8*EB per CTA
 #if ACI_NARROW512

@@ -269,6 +269,28 @@ int aci_workspace_query(const tt_t *const *inputs, int n_inputs, int maxrank, in
 /* Compiled envelope: the largest Pi block (rows, cols) the prrLU kernels accept. */
 int aci_limits(int *max_rows, int *max_cols);
 
+/*
+ * aci_prrlu — the prrLU step alone (a5; Alg. 2, readings R1-R4, R17): partial-rank LU
+ * with full pivoting of a device-resident row-major m x n FP64 block (leading dimension n),
+ * exactly as a 2-site update runs it (same kernel, tiers, tie-break and arithmetic), for tests and
+ * for callers that factorise their own blocks.
+ *
+ * dev_M: device, m x n, row-major, read only. maxrank >= 1: at most min(maxrank, m, n) pivots.
+ * tol >= 0, tol_mode: ACI_TOL_RELATIVE -> a candidate c is rejected when |c| <= tol * |first
+ *   candidate| (= tol * max|M|, R8); ACI_TOL_ABSOLUTE -> when |c| <= tol. The first pivot is
+ *   always kept (R2); a zero block gives rank 1 with pivot (0, 0) (R17).
+ * static_m, static_n: the launch's static capacity (>= m, n; 0 = m, n) — the product launches every
+ *   bond for its largest possible block and the kernel picks its tier from the live size.
+ * dev_rows, dev_cols: device, >= min(maxrank, m, n) ints: the pivots in selection order (R21).
+ * dev_U: device, nullable, >= min(maxrank, m, n) x n doubles, ld n: U_k = S_k[p_k, :] / S_k[p_k, q_k].
+ * *rank, *eps (host): the rank r and the first rejected candidate's |c| (0 when none, R2).
+ * stream: a cudaStream_t or NULL (the library stream); the call synchronises it.
+ * Errors: ACI_ERR_INVALID, ACI_ERR_UNSUPPORTED (static size beyond aci_limits), ACI_ERR_OOM,
+ *   ACI_ERR_CUDA.
+ */
+int aci_prrlu(const double *dev_M, int m, int n, int maxrank, double tol, int tol_mode, int static_m, int static_n,
+              int *dev_rows, int *dev_cols, double *dev_U, int *rank, double *eps, void *stream);
+
 /* Thread-local description of the last error of this thread. */
 const char *aci_last_error(void);
 

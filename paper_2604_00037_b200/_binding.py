@@ -24,7 +24,7 @@ MAX_INPUTS, MAX_TERMS, MAX_EXPO = 4, 8, 4
 # every symbol include/aci.h declares (tests check the library exports all of them)
 EXPORTS = ["tt_create", "tt_create_z", "tt_create_device", "tt_create_device_z", "tt_is_complex", "tt_destroy",
            "tt_shape", "tt_get_cores", "tt_device_cores", "tt_evaluate", "tt_evaluate_device", "aci_elementwise",
-           "aci_elementwise_ex", "aci_elementwise_batch", "aci_workspace_query", "aci_limits", "aci_last_error", "aci_version"]
+           "aci_elementwise_ex", "aci_elementwise_batch", "aci_workspace_query", "aci_limits", "aci_prrlu", "aci_last_error", "aci_version"]
 
 
 class AciError(RuntimeError):
@@ -103,6 +103,8 @@ def load(path: str = LIB_PATH):
     lib.aci_elementwise_batch.argtypes = [C.POINTER(aci_job), C.c_int, C.c_int]
     lib.aci_workspace_query.argtypes = [C.POINTER(vp), C.c_int, C.c_int, C.c_int, vp, C.POINTER(C.c_size_t)]
     lib.aci_limits.argtypes = [ip, ip]
+    lib.aci_prrlu.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
+                              C.c_void_p, C.c_void_p, C.c_void_p, ip, dp, C.c_void_p]
     lib.aci_last_error.restype = C.c_char_p
     lib.aci_version.restype = C.c_char_p
     _lib = lib
@@ -357,6 +359,29 @@ def workspace_query(inputs, maxrank, y_init=None, max_sweeps=64) -> int:
     _check(load().aci_workspace_query(hs, n, maxrank, max_sweeps, y_init.handle.value if y_init is not None else None,
                                       C.byref(b)))
     return b.value
+
+
+def prrlu(M, maxrank: int, tol: float = 0.0, relative: bool = True, static=(0, 0), want_u: bool = True,
+          stream=None) -> dict:
+    """a5 alone (include/aci.h aci_prrlu) on a device copy of the float64 block M (torch CUDA tensor
+    or numpy array): rows, cols (selection order), U (r x n), eps. Argument marshalling only."""
+    import torch
+    Mt = torch.as_tensor(M, dtype=torch.float64).cuda().contiguous()
+    m, n = Mt.shape
+    k = max(1, min(maxrank, m, n))
+    rows = torch.full((k,), -1, dtype=torch.int32, device=Mt.device)
+    cols = torch.full((k,), -1, dtype=torch.int32, device=Mt.device)
+    U = torch.zeros((k, n), dtype=torch.float64, device=Mt.device) if want_u else None
+    r, e = C.c_int(), C.c_double()
+    st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    _check(load().aci_prrlu(Mt.data_ptr(), m, n, maxrank, tol, 0 if relative else 1, int(static[0]), int(static[1]),
+                            rows.data_ptr(), cols.data_ptr(), U.data_ptr() if U is not None else None, C.byref(r),
+                            C.byref(e), st))
+    rr = r.value
+    out = {"r": rr, "rows": rows[:rr].cpu().numpy(), "cols": cols[:rr].cpu().numpy(), "eps": e.value}
+    if U is not None:
+        out["U"] = U[:rr].cpu().numpy()
+    return out
 
 
 def limits():

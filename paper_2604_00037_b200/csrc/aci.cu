@@ -1818,6 +1818,9 @@ static int build_run(const Inputs &I, const tt_s *y, int maxrank, int max_sweeps
   return ACI_OK;
 }
 
+// multi-cluster prrLU launches of different host threads are serialised (aci_elementwise_ex)
+static std::mutex multi_cluster_mu;
+
 extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_inputs, double tol, int maxrank,
                                   int max_sweeps, tt_t **out, aci_report *rep, const aci_options *opts) {
   NvtxRange nv_call("aci_elementwise");
@@ -1837,7 +1840,6 @@ extern "C" int aci_elementwise_ex(aci_op op, const tt_t *const *inputs, int n_in
   // such launches co-scheduled from different host threads could each hold part of their
   // clusters and wait forever, so those calls are serialised within the process. Calls with
   // aci_options.concurrent use single-cluster launches and run concurrently.
-  static std::mutex multi_cluster_mu;
   std::unique_lock<std::mutex> serial(multi_cluster_mu, std::defer_lock);
   if (!o.concurrent) serial.lock();
   Inputs I;
@@ -2374,6 +2376,72 @@ extern "C" int tt_evaluate_device(const tt_t *t, int64_t npts, const uint8_t *de
   if (E) cudaFreeAsync(E, st);
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return fail(ACI_ERR_CUDA, std::string("tt_evaluate: ") + cudaGetErrorString(e));
+  return ACI_OK;
+}
+
+// a5 alone (include/aci.h aci_prrlu): the library's prrLU on a caller's device block, launched for
+// the static capacity static_m x static_n as a bond update launches it (tier and hand-off chosen on
+// the device from the live m x n)
+extern "C" int aci_prrlu(const double *dev_M, int m, int n, int maxrank, double tol, int tol_mode, int static_m,
+                         int static_n, int *dev_rows, int *dev_cols, double *dev_U, int *rank, double *eps,
+                         void *stream) {
+  if (!dev_M || !dev_rows || !dev_cols || !rank || !eps || m < 1 || n < 1 || maxrank < 1 || !(tol >= 0.0) ||
+      (tol_mode != ACI_TOL_RELATIVE && tol_mode != ACI_TOL_ABSOLUTE))
+    return fail(ACI_ERR_INVALID, "aci_prrlu: bad args");
+  int st_ = check_device();
+  if (st_) return st_;
+  const int sm = static_m > 0 ? static_m : m, sn = static_n > 0 ? static_n : n;
+  if (sm < m || sn < n) return fail(ACI_ERR_INVALID, "aci_prrlu: static size below the live size");
+  if (!prrlu_supported(sm, sn)) return fail(ACI_ERR_UNSUPPORTED, "aci_prrlu: block beyond aci_limits");
+  prrlu_init();
+  cudaStream_t st = stream ? (cudaStream_t)stream : lib_stream();
+  const int colcap = std::max(sm, 1024);
+  const size_t colwords = (size_t)2 * 148 * colcap * 2 * prrlu_col_spread(), keywords = (size_t)2 * 148 * 4;
+  unsigned long long *colpub = nullptr, *keys = nullptr;
+  unsigned *ctr = nullptr;
+  LuDims *dims = nullptr;
+  int *rout = nullptr;
+  double *eout = nullptr;
+  const size_t small = 64 + sizeof(LuDims) + 16;
+  char *sb = nullptr;
+  if (cudaMallocAsync((void **)&colpub, 8 * colwords, st) != cudaSuccess ||
+      cudaMallocAsync((void **)&keys, 8 * keywords, st) != cudaSuccess ||
+      cudaMallocAsync((void **)&sb, small, st) != cudaSuccess)
+    return fail(ACI_ERR_OOM, "aci_prrlu: workspace");
+  // small scratch: counter (4) | epoch (4) | scale (8) | r (4) | eps (8, at 24) | dims (at 64)
+  ctr = reinterpret_cast<unsigned *>(sb);
+  unsigned *epoch = ctr + 1;
+  unsigned long long *scale = reinterpret_cast<unsigned long long *>(sb + 8);
+  rout = reinterpret_cast<int *>(sb + 16);
+  eout = reinterpret_cast<double *>(sb + 24);
+  dims = reinterpret_cast<LuDims *>(sb + 64);
+  cudaMemsetAsync(colpub, 0, 8 * colwords, st);
+  cudaMemsetAsync(keys, 0, 8 * keywords, st);
+  cudaMemsetAsync(sb, 0, small, st);
+  const int kmax = std::min(maxrank, std::min(m, n));
+  const LuDims D{m, n, n, kmax, n};
+  cudaMemcpyAsync(dims, &D, sizeof(D), cudaMemcpyHostToDevice, st);
+  LuArgs a = {};
+  a.M = dev_M; a.dims = dims; a.tol = tol; a.thr_mode = tol_mode == ACI_TOL_RELATIVE ? 1 : 2; a.scale_bits = scale;
+  a.rows = dev_rows; a.cols = dev_cols; a.r_out = rout; a.eps_out = eout; a.U = dev_U;
+  a.colpub = colpub; a.colcap = colcap; a.keys = keys; a.counter = ctr; a.epoch = epoch;
+  cudaError_t le;
+  {
+    std::lock_guard<std::mutex> serial(multi_cluster_mu);  // multi-cluster grids: one at a time (aci_elementwise_ex)
+    le = launch_prrlu(a, sm, sn, st, false, false, nullptr, false);
+  }
+  int hr = 0;
+  double he = 0.0;
+  cudaMemcpyAsync(&hr, rout, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&he, eout, sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(colpub, st);
+  cudaFreeAsync(keys, st);
+  cudaFreeAsync(sb, st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  if (le != cudaSuccess || e != cudaSuccess)
+    return fail(ACI_ERR_CUDA, std::string("aci_prrlu: ") + cudaGetErrorString(le != cudaSuccess ? le : e));
+  *rank = hr;
+  *eps = he;
   return ACI_OK;
 }
 

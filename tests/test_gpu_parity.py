@@ -750,3 +750,45 @@ def test_peak_and_latency_probes(aci):
     for m, row in lat.items():
         assert row["pivots"] == min(m, 512)
         assert 0.0 < row["floor_us"] < row["kernel_us"] < 20.0, (m, row)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,r,static", [
+    (512, 1024, 512, (1024, 1024)),   # two clusters -> one at pivot 256 (hand-off pair 1)
+    (400, 1000, 400, (1024, 1024)),   # pair 1, K = 232
+    (512, 256, 256, (1024, 1024)),    # one cluster, 16x2 -> 12x1 at pivot 128 (pair 2)
+    (450, 250, 250, (1024, 1024)),    # pair 2, K = 122 rounded to 124 (prrlu.cu ho_round)
+    (300, 130, 130, (512, 256)),      # pair 2, K = 2 rounded to 4
+    (1024, 1024, 512, (1024, 1024)),  # four clusters, no hand-off
+    (128, 64, 64, (1024, 1024)),      # a one-CTA shape run on the cluster (CTA_MAXE)
+    (200, 250, 200, (256, 256)),
+])
+def test_prrlu_step_vs_oracle(aci, m, n, r, static):
+    """a5 alone through the C-ABI (aci_prrlu) against the oracle's Alg. 2 on the same seeded block:
+    the ordered pivots identical, U = S_k[p, :] / c equal to rounding (the same FMA sequence, R4),
+    including the blocks whose factorisation hands off to one cluster mid-way and
+    the U entries of columns eliminated before the hand-off."""
+    rng = np.random.default_rng(1000 + m + 7 * n)
+    M = rng.standard_normal((m, n))
+    g = aci.prrlu(M, r, 0.0, relative=False, static=static)
+    o = oracle.ldu(M, 0.0, r)
+    assert g["r"] == o["r"] == min(r, m, n)
+    assert np.array_equal(g["rows"], o["rows"]) and np.array_equal(g["cols"], o["cols"])
+    assert np.max(np.abs(g["U"] - o["U"])) <= 1e-13 * np.max(np.abs(o["U"]))
+    # eliminated columns of each U row are exact zeros, the pivot column exactly 1
+    for k in range(g["r"]):
+        assert g["U"][k, g["cols"][k]] == 1.0
+        assert np.all(g["U"][k, g["cols"][:k]] == 0.0)
+
+
+@pytest.mark.gpu
+def test_prrlu_step_relative_stop_rule(aci):
+    """aci_prrlu with a relative tolerance stops where the oracle does (R2: the first candidate with
+    |c| <= tol * |first candidate| is rejected and reported as eps) on a numerically rank-40 block."""
+    rng = np.random.default_rng(77)
+    M = rng.standard_normal((300, 40)) @ rng.standard_normal((40, 500)) + 1e-12 * rng.standard_normal((300, 500))
+    g = aci.prrlu(M, 300, 1e-9, relative=True, static=(512, 1024))
+    o = oracle.ldu(M, 1e-9, 300, relative_to_own_max=True)
+    assert g["r"] == o["r"] == 40
+    assert np.array_equal(g["rows"], o["rows"]) and np.array_equal(g["cols"], o["cols"])
+    assert g["eps"] == o["eps"]

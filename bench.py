@@ -816,7 +816,12 @@ def main():
                    "frac": pi_flops / ((pi["ms"] + prof["gemm_ab"]["ms"]) * 1e9) / pk["dmma_tflops"],
                    "traffic": None, "note": "FP64 DMMA (mma.sync m8n8k4); peak = the DMMA register loop measured "
                                             "in this run (peaks.dmma_tflops); peaks.dgemm_tflops = cuBLAS DGEMM "
-                                            "8192^3 in this run"}
+                                            "8192^3 in this run. The time is the event-timed sum over the contraction "
+                                            "launches of the profiled run: it includes the streamed-Pi kernel's whole "
+                                            "residency beside the prrLU (it waits for pivot rows), so this is a lower "
+                                            "bound on the GEMMs' own rate; the serialised ncu launch list "
+                                            "(profiles/r02zl_chi256_launches_summary.txt) has ~10.5 ms of contraction "
+                                            "kernels per chi = 256 product"}
         tr = _ncu_traffic()
         if "prrlu" in tr:
             roof_prrlu["traffic"] = tr["prrlu"]["bytes"]

@@ -17,7 +17,14 @@ using namespace gemmk;
 #ifndef ACI_GEMM_VEC
 #define ACI_GEMM_VEC 1
 #endif
-using CfgPi = Cfg<64, 64, 32, 16, 16, 3, 2, ACI_GEMM_VEC>;
+// ACI_PI_WN / ACI_PI_MINB (A/B switches): warp-tile width and min CTAs per SM of the Pi tile
+#ifndef ACI_PI_WN
+#define ACI_PI_WN 16
+#endif
+#ifndef ACI_PI_MINB
+#define ACI_PI_MINB 2
+#endif
+using CfgPi = Cfg<64, 64, 32, ACI_PI_WN, 16, 3, ACI_PI_MINB, ACI_GEMM_VEC>;
 using CfgAB = Cfg<64, 32, 32, 16, 16, 3, 4, ACI_GEMM_VEC>;
 // Small problems: 32x32 tiles of 4 warps. A 64x64-tile grid of fewer than ~2 CTAs per SM leaves
 // SMs idle and runs the K loop serially on the busy ones; measured per launch (tools/gemm_latency.cu,
